@@ -1,0 +1,142 @@
+"""Generate tests/golden/ fixtures FROM THE REFERENCE ITSELF (test infra only).
+
+Run in the build container, where the reference is importable:
+
+    PYTHONPATH=/root/reference/pkg/src python oracle/gen_golden.py
+
+The fixtures pin the oracle (oracle/ludax_oracle.c) and the device path to
+the reference's exact behaviour; the GPU box never needs /root/reference.
+Every fixture below is produced by the reference's public API:
+``engine.playout_random`` (engine.py:123-163), ``CompiledGame.legal_mask`` /
+``step`` (compiler.py:411-454), ``rng.hash_key`` / ``uniform`` (rng.py:26-42),
+``GameState.digest`` (state.py:180-188), and ``parser.parse_game``.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = os.environ.get("LUDAX_REFERENCE", "/root/reference/pkg")
+sys.path.insert(0, os.path.join(REF, "src"))
+
+import boardlang  # noqa: E402
+from boardlang import engine, rng  # noqa: E402
+from boardlang.parser import parse_game  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+GAMES_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                         "paper_2506_22609_b200", "games")
+GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente")
+PLAYOUT = {"tic_tac_toe": [(1024, 0), (512, 99)], "connect_four": [(256, 0), (256, 5)],
+           "hex": [(64, 0), (48, 21)], "reversi": [(64, 0), (64, 12)],
+           "pente": [(32, 0), (24, 3)]}
+
+
+def state_arrays(st, prefix):
+    out = {}
+    for name in ("board_piece", "board_owner", "current_player", "move_count", "terminated",
+                 "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags",
+                 "must_move", "last_mover", "last_kind", "last_source", "last_dest",
+                 "last_dest_by_player", "hopped_mask", "captured_mask", "promoted_mask",
+                 "comp_labels", "phase", "turn_pos"):
+        v = getattr(st, name)
+        if v is not None:
+            out[f"{prefix}{name}"] = v
+    return out
+
+
+def norm(x):
+    if dataclasses.is_dataclass(x):
+        return [type(x).__name__] + [[f.name, norm(getattr(x, f.name))]
+                                     for f in dataclasses.fields(x)]
+    if isinstance(x, tuple):
+        return [norm(i) for i in x]
+    return x
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    meta = {"reference": REF, "games": {}}
+    for name in GAMES:
+        text = open(os.path.join(GAMES_DIR, f"{name}.ldx")).read()
+        ref_text = open(os.path.join(REF, "games", f"{name}.ldx")).read()
+        g = boardlang.load_game(text)
+        assert norm(parse_game(text)) == norm(parse_game(ref_text)), name
+        arrays = {}
+        info = {"ast": norm(parse_game(text)), "describe": g.describe(), "playouts": []}
+        # (1) final states of seeded random playouts
+        for k, (B, seed) in enumerate(PLAYOUT[name]):
+            po = engine.playout_random(g, seed=seed, batch_size=B, max_turns=200)
+            arrays.update(state_arrays(po.final, f"p{k}_"))
+            info["playouts"].append({"batch": B, "seed": seed, "digest": po.final.digest(),
+                                     "turns": int(po.turns_taken.sum())})
+        # (2) a recorded trajectory: legal mask + sampled action per step
+        st = g.init(batch_size=4, seed=3)
+        masks, actions, digests = [], [], []
+        while not st.terminated.all() and len(actions) < 200:
+            masks.append(g.legal_mask(st))
+            u = rng.uniform(st.seeds, st.move_count.astype(np.uint64))
+            a = g.sample_actions(st, u)
+            actions.append(a)
+            live = ~st.terminated
+            g.step_into(st, a, rows=live, verify=False)
+            digests.append(st.digest())
+        arrays["traj_masks"] = np.packbits(np.stack(masks), axis=-1)
+        arrays["traj_actions"] = np.stack(actions)
+        info["traj_digests"] = digests
+        info["traj_mask_width"] = int(g.codec.size)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **arrays)
+        meta["games"][name] = info
+        print(name, "ok", [p["digest"] for p in info["playouts"]])
+
+    # (3) known-answer transcripts from the reference's own tests
+    kat = {}
+    ttt = boardlang.load_game(open(os.path.join(GAMES_DIR, "tic_tac_toe.ldx")).read())
+    s = engine.init(ttt, 1)
+    for a in [0, 1, 4, 2, 8]:                       # tests/test_engine.py:46-51
+        s = engine.step(ttt, s, a)
+    kat["ttt_diag"] = {"actions": [0, 1, 4, 2, 8], "digest": s.digest(),
+                       "outcome": int(s.outcome[0])}
+    c4 = boardlang.load_game(open(os.path.join(GAMES_DIR, "connect_four.ldx")).read())
+    kat["c4_initial_legal"] = np.nonzero(c4.legal_mask(c4.init(1))[0])[0].tolist()
+    rv = boardlang.load_game(open(os.path.join(GAMES_DIR, "reversi.ldx")).read())
+    kat["reversi_initial_legal"] = np.nonzero(rv.legal_mask(rv.init(1))[0])[0].tolist()
+    pe = boardlang.load_game(open(os.path.join(GAMES_DIR, "pente.ldx")).read())
+    for key, seq in (("pente_capture", [180, 181, 200, 182, 183]),      # test_compiler.py:182-195
+                     ("pente_no_capture3", [180, 181, 220, 182, 221, 183, 184])):
+        s = pe.init(1)
+        for a in seq:
+            s = pe.step(s, np.array([a]))
+        kat[key] = {"actions": seq, "digest": s.digest(),
+                    "owner": s.board_owner[0].tolist(), "scores": s.scores[0].tolist()}
+    # (4) RNG vectors (rng.py) incl. the benchmark's episode keys (evaluation.py:222-229)
+    seeds = rng.spawn_seeds(12345, 16)
+    mcs = np.arange(16, dtype=np.uint64) * 7
+    kat["rng"] = {"spawn_12345_16": [str(int(x)) for x in seeds],
+                  "uniform_hex": [float.hex(float(x)) for x in rng.uniform(seeds, mcs)],
+                  "episode_keys": {f"{b}_{e}": str(int(rng.hash_key(np.uint64(0), np.uint64(b),
+                                                                    np.uint64(e))))
+                                   for b in (1024, 1 << 20) for e in (0, 1, 10000, 10001)}}
+    # (5) C4 opening distribution (tests/test_agents.py:28-41) and TTT outcome counts
+    st = c4.init(batch_size=100_000, seed=77)
+    a = c4.sample_actions(st, rng.uniform(st.seeds, st.move_count.astype(np.uint64)))
+    vals, cnt = np.unique(a, return_counts=True)
+    kat["c4_opening_counts"] = dict(zip(map(str, vals.tolist()), cnt.tolist()))
+    f = engine.playout_random(ttt, seed=11, batch_size=10_000).final
+    kat["ttt_10000_seed11"] = {"p1": int((f.outcome == 1).sum()),
+                               "p2": int((f.outcome == 2).sum()),
+                               "draw": int((f.outcome == 0).sum()),
+                               "digest": f.digest()}
+    meta["kat"] = kat
+    with open(os.path.join(OUT, "golden.json"), "w") as fh:
+        json.dump(meta, fh, indent=0, sort_keys=True)
+    print("wrote", OUT)
+
+
+if __name__ == "__main__":
+    main()
