@@ -1,0 +1,357 @@
+"""Benchmark: env steps/s of uniform-random rollouts (Connect Four 6x7).
+
+Metric and protocol follow the reference benchmark (reference:
+pkg/src/boardlang/evaluation.py:197-233): one step of this bench = one
+synchronized batch episode -- B envs started from the program's start
+position with per-env seeds spawn(hash_key(0, B_total, e), global index),
+played with uniform legal actions until every env has terminated (cap 200
+plies); env steps = live envs advanced by one ply, summed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--game G]
+  python bench.py --impl reference ...      # CPU reference arm (oracle port)
+
+Under torchrun each rank plays its own slice [rank*B, (rank+1)*B) of the
+global env index space (weak scaling, no collective on the hot path); one
+NCCL all-reduce of the stats after the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env steps/sec (uniform-random rollouts) vs batch size at 1/2/4/8 B200"
+UNIT = "env_steps/s"
+GAME_FILES = {"connect_four": "Connect Four 6x7", "tic_tac_toe": "Tic-Tac-Toe",
+              "hex": "Hex 11x11", "reversi": "Reversi 8x8", "pente": "Pente 19x19"}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--batch", type=int, default=1 << 22, help="envs per GPU")
+    p.add_argument("--game", default="connect_four", choices=sorted(GAME_FILES))
+    p.add_argument("--max-turns", type=int, default=200)
+    p.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="target CPU time of the bounded CPU-baseline sample")
+    p.add_argument("--no-extras", action="store_true",
+                   help="skip the e2e / step-kernel / cpu-baseline legs")
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout
+                self.rows.append([x.strip() for x in out.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_rate(game, batch_total, seconds, threads, max_turns):
+    """Oracle port (plain C, all host threads) on a bounded sample of the same
+    workload: the first envs of episode 10000, repeated until ~seconds."""
+    from oracle import oracle as O
+    og = O.OracleGame(game)
+    seed = O.hash_key3(0, batch_total, 10000)
+    n = 4096
+    steps_total, t_total = 0, 0.0
+    while t_total < seconds:
+        seeds = O.spawn_seeds(seed, n)
+        st = og.init(n, seeds=seeds)
+        t0 = time.perf_counter()
+        _, steps = og.playout(state=st, max_turns=max_turns, threads=threads)
+        dt = time.perf_counter() - t0
+        steps_total += steps
+        t_total += dt
+        if dt < seconds / 8:
+            n = min(n * 2, batch_total)
+    return steps_total / t_total, steps_total, t_total, n
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    B_total = args.batch * max(ws, args.gpus)
+    rates = []
+    per = max(args.cpu_seconds / max(args.steps, 1), 0.5)
+    for w in range(args.warmup):
+        cpu_rate(args.game, B_total, min(per, 1.0), threads, args.max_turns)
+    sample = None
+    for _ in range(args.steps):
+        r, steps, dt, n = cpu_rate(args.game, B_total, per, threads, args.max_turns)
+        rates.append(r)
+        sample = f"{steps} env steps of the first {n} envs of episode 10000, {dt:.1f}s"
+    value = statistics.mean(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * per, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config(args, ws),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config(args, ws):
+    return {"workload": f"{GAME_FILES[args.game]} uniform-random rollouts, "
+                        f"{args.batch} envs per GPU, full episodes (cap {args.max_turns} plies)",
+            "game": args.game, "batch_per_gpu": args.batch,
+            "global_batch": args.batch * ws, "max_turns": args.max_turns,
+            "parallelism": f"env-shard x{ws}",
+            "l2": "final states written each step (48-128 B/env, > 126 MB L2 at 2^22 envs)"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_22609_b200 as lx
+    from paper_2506_22609_b200 import rng
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    game = lx.load_config_game(args.game)
+    B, B_total = args.batch, args.batch * ws
+    first = rank * B
+    state = game.empty_state(B)
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    work = torch.zeros(4, dtype=torch.int64, device="cuda")
+    acc = torch.zeros(8, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def episode(e):
+        # fresh envs from the episode seed, final states stored to `state`
+        seed = rng.episode_seed(0, B_total, e)
+        native_rollout(game, state, B, args.max_turns, seed, first, stats, work)
+        acc.add_(stats)
+
+    for w in range(args.warmup):
+        episode(w)
+    torch.cuda.synchronize()
+    acc.zero_()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for e in range(args.steps):
+            episode(10_000 + e)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    tot = acc.clone()
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot)
+        dist.barrier()
+    ms_max = float(t.item())
+    tot = tot.cpu().tolist()
+    value = tot[0] / (ms_max / 1000.0)
+
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        extras = measure_extras(args, game, lx, rng, B, B_total, value, ms_max / args.steps)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic (seeded random play from the start position)",
+                "config": config(args, ws), "clocks": clk.summary(),
+                "gpu_launches": args.steps,
+                "totals": {"env_steps": tot[0], "p1_wins": tot[1], "p2_wins": tot[2],
+                           "draws": tot[3], "truncated": tot[4], "envs": tot[5]},
+                "mean_plies": tot[0] / max(tot[5], 1)}
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def native_rollout(game, state, B, max_turns, seed, first, stats, work):
+    import ctypes
+
+    from paper_2506_22609_b200 import native
+    stuck = ctypes.c_int64(-1)
+    native.check(native.lib().lx_rollout(
+        game.handle, state.words.data_ptr(), B, int(max_turns), 1 | 2, int(seed), None,
+        int(first), stats.data_ptr(), work.data_ptr(), None, None, 0, ctypes.byref(stuck),
+        game._stream()))
+
+
+def measure_extras(args, game, lx, rng, B, B_total, value, ms_step):
+    """e2e through the public API, the HBM-bound step kernel, roofline data,
+    and the CPU baseline (rank 0, N=1 sizes)."""
+    import torch
+    out = {}
+    # ---- e2e: host seeds (pinned) -> device, fused rollout, outcomes -> host
+    seeds_h = torch.from_numpy(rng.spawn_seeds(rng.episode_seed(0, B_total, 20000), B)
+                               .view("int64")).pin_memory()
+    seeds_d = torch.empty_like(seeds_h, device="cuda")
+    outc_d = torch.empty(B, dtype=torch.int8, device="cuda")
+    outc_h = torch.empty(B, dtype=torch.int8).pin_memory()
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    work = torch.zeros(4, dtype=torch.int64, device="cuda")
+    state = game.empty_state(B)
+    steps = 0
+    K = max(3, min(args.steps, 10))
+    for it in range(K + 2):
+        if it == 2:
+            torch.cuda.synchronize()
+            steps = 0
+            t0 = time.perf_counter()
+        seeds_d.copy_(seeds_h, non_blocking=True)
+        game.rollout(seeds=seeds_d, out=state, max_turns=args.max_turns, store=True,
+                     truncate=True, check=False, stats=stats, work=work, outcomes=outc_d)
+        outc_h.copy_(outc_d, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        steps += int(stats[0].item())
+    e2e_s = time.perf_counter() - t0
+    out["e2e"] = {"value": steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * 8,
+                  "d2h_bytes_per_step": B + 64,
+                  "path": "B200Game.rollout(seeds=host->device) + outcomes device->host"}
+
+    # ---- roofline of the fused rollout kernel: integer issue bound
+    prof = load_profile(game)
+    clk_mhz = 1965.0
+    peak_warp_inst = 148 * 4 * clk_mhz * 1e6          # 1 warp-inst/clk/SMSP
+    rl = {"bound": "int_issue", "unit": "Gwarp-inst/s", "peak": peak_warp_inst / 1e9,
+          "peak_source": "148 SMs x 4 SMSP x 1 warp-inst/clk x 1965 MHz (B200_PROFILING.md)",
+          "kernel": "lx_rollout", "traffic": None, "achieved": None, "frac": None}
+    if prof:
+        ach = prof["warp_inst_per_env_step"] * value
+        rl.update({"achieved": ach / 1e9, "frac": ach / peak_warp_inst,
+                   "traffic": prof.get("dram_bytes_per_launch"),
+                   "inst_source": prof.get("source")})
+    out["roofline"] = rl
+
+    # ---- HBM-bound per-ply step kernel (PGX-style API path)
+    st = game.init(B, seed=1)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    plies = 8
+    ev0.record()
+    for _ in range(plies):
+        game.random_step(st, max_turns=args.max_turns)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / plies
+    nbytes = 2 * game.info["nq"] * 16 * B            # read + write the state words
+    gbs = nbytes / (ms / 1e3) / 1e9
+    peak_hbm = measured_hbm()
+    out["step_kernel"] = {"kernel": "lx_random_step", "plies_timed": plies,
+                          "ms_per_ply": ms, "env_steps_per_s_upper": B / (ms / 1e3),
+                          "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak_hbm,
+                                       "unit": "GB/s", "frac": gbs / peak_hbm,
+                                       "traffic": None,
+                                       "bytes_per_env_ply": 2 * game.info["nq"] * 16}}
+
+    # ---- CPU baseline (oracle port, all host threads, bounded sample)
+    threads = os.cpu_count() or 1
+    r, steps, dt, n = cpu_rate(args.game, B_total, args.cpu_seconds, threads, args.max_turns)
+    out["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": threads, "kind": "port",
+                           "sample": f"{steps} env steps, first {n} envs of episode 10000, "
+                                     f"{dt:.1f}s on {threads} threads"}
+    return out
+
+
+def measured_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def load_profile(game):
+    """Per-env-step instruction count of this exact kernel build, from the
+    committed ncu capture (profiles/rollout_<game>.json)."""
+    path = os.path.join(ROOT, "profiles", f"rollout_{game.info['name'].replace(' ', '_')}.json")
+    try:
+        with open(path) as f:
+            prof = json.load(f)
+    except Exception:
+        return None
+    if prof.get("cubin_key") and prof["cubin_key"] != game.lowered_key():
+        return None
+    return prof
+
+
+if __name__ == "__main__":
+    main()

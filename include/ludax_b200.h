@@ -1,0 +1,139 @@
+/*
+ * ludax_b200.h -- C-ABI of the B200 game-simulation backend.
+ *
+ * Replaces the reference's numpy runtime behind CompiledGame / engine
+ * (reference: pkg/src/boardlang/compiler.py:197-650, engine.py:27-163).
+ * Plain C types only: device pointers are `void*` / typed pointers into
+ * CUDA global memory (e.g. torch tensors' data_ptr()), streams are CUstream
+ * handles passed as `void*` (NULL = legacy default stream).  No C++
+ * exceptions cross this boundary; every entry point returns an LX_* status
+ * and lx_last_error() describes the last failure on the calling thread.
+ *
+ * One game = one handle = one NVRTC-compiled sm_100a module.  Handles are
+ * immutable after creation and may be shared across threads and streams;
+ * the library keeps no pointer to caller memory past a call.
+ */
+#ifndef LUDAX_B200_H
+#define LUDAX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python shim re-raises them as the reference exception
+   types (reference errors.py:59-76) */
+#define LX_OK 0
+#define LX_EILLEGAL_ACTION 1   /* IllegalAction   (mechanics.py:503-510, compiler.py:484-494) */
+#define LX_ETERMINAL_STATE 2   /* TerminalState   (engine.py:31-33, 43-44) */
+#define LX_EEMPTY_MASK 3       /* EmptyMask       (engine.py:142-147) */
+#define LX_ECOMPILE 4          /* CompileError    (errors.py:71-76), NVRTC stage */
+#define LX_ECUDA 5             /* driver / launch failure */
+#define LX_EINVALID 6          /* bad argument */
+
+typedef struct lx_game lx_game;
+
+/* Static facts of a compiled game (reference CompiledGame.describe,
+   compiler.py:628-650, plus the device state layout). */
+typedef struct {
+    int32_t num_cells;          /* C */
+    int32_t num_actions;        /* A = C (+1 pass), ActionCodec.size (codec.py:58-69) */
+    int32_t pass_index;         /* -1 when the game has no pass action */
+    int32_t board_words;        /* W: 32-bit words per player bitboard */
+    int32_t state_quads;        /* NQ: 16-byte quads per env in HBM */
+    int32_t num_sms;            /* SMs of the device the module is loaded on */
+    int32_t rollout_blocks;     /* persistent grid of lx_rollout (SMs x blocks/SM) */
+    int32_t rollout_threads;    /* block size of lx_rollout */
+} lx_game_info;
+
+/* Reference GameState field pointers (state.py:78-130); optional fields NULL.
+   Used by lx_export / lx_import to move between the device bitboard layout
+   and the reference's int8 cell arrays. */
+typedef struct {
+    int8_t *board_piece, *board_owner, *current_player;
+    int32_t *move_count;
+    uint8_t *terminated, *truncated;
+    int8_t *outcome;
+    uint64_t *seeds;
+    int32_t *scores;
+    int16_t *pass_streak;
+    uint8_t *pass_flags;
+    int8_t *last_mover, *last_kind;
+    int16_t *last_source, *last_dest, *last_dest_by_player, *comp_labels;
+    int8_t *phase;
+} lx_ref_state;
+
+int lx_version(void);
+const char *lx_last_error(void);
+
+/* Compile (or fetch from cache_dir) the generated translation unit and load
+   it on the current CUDA context.  Replaces CompiledGame.__init__
+   (compiler.py:200-286).  `source` is the lowering's output; headers are
+   resolved from include_dir; cubins are cached as <cache_dir>/<key>.cubin. */
+int lx_game_create(const char *source, const char *name, const char *include_dir,
+                   const char *cache_dir, lx_game **out);
+/* Compile to <cache_dir>/<key>.cubin only (no GPU needed); *key_out gets the
+   cache key (>= 65 bytes). */
+int lx_compile_only(const char *source, const char *name, const char *include_dir,
+                    const char *cache_dir, char *key_out);
+int lx_game_info_get(const lx_game *g, lx_game_info *out);
+int lx_game_destroy(lx_game *g);
+
+/* CompiledGame.init (compiler.py:357-364): seeds[i], or when seeds is NULL
+   spawn_seeds: hash_key(seed, first_index + i) (rng.py:52-54). */
+int lx_init(const lx_game *g, void *state, int64_t B, const uint64_t *seeds, uint64_t seed,
+            int64_t first_index, void *stream);
+
+/* CompiledGame.legal_mask / legal_counts (compiler.py:394-428):
+   mask (B, A) uint8 or NULL, counts (B,) int64 or NULL. */
+int lx_legal(const lx_game *g, const void *state, int64_t B, uint8_t *mask, int64_t *counts,
+             void *stream);
+
+/* CompiledGame.sample_actions (compiler.py:430-446): u (B,) float64 draws, or
+   NULL to draw uniform(seed, move_count) on device (engine.random_actions). */
+int lx_sample(const lx_game *g, const void *state, int64_t B, const double *u,
+              int64_t *actions, void *stream);
+
+/* CompiledGame.step_into (compiler.py:456-580), in place on rows (B,) uint8
+   (NULL = all) & ~terminated.  verify != 0 checks every live row first and
+   fails with LX_EILLEGAL_ACTION (*bad_row = first bad row) before mutating;
+   scratch is >= 8 bytes of device memory (used only when verifying). */
+int lx_step(const lx_game *g, void *state, int64_t B, const int64_t *actions,
+            const uint8_t *rows, int verify, void *scratch, int64_t *bad_row, void *stream);
+
+/* One fused ply of uniform-random play for rows with !terminated and
+   move_count < max_turns (engine.random_actions + step_into); actions_out
+   (B,) int64 or NULL receives the sampled actions (-1 for idle rows). */
+int lx_random_step(const lx_game *g, void *state, int64_t B, int max_turns,
+                   int64_t *actions_out, void *stream);
+
+/* Fused register-resident rollout (engine.playout_random, engine.py:123-163;
+   evaluation._run_episode, evaluation.py:197-211).
+   mode bit 0: start envs from seeds (seeds[i] or spawn(seed, first_index+i))
+                 else continue from `state`
+   mode bit 1: write final states to `state`
+   mode bit 2: mark unfinished envs terminated+truncated draws at max_turns
+   work: >= 32 bytes of device scratch (counter + stuck row), reset here.
+   stats: u64[8] device buffer, zeroed here: steps, p1 wins, p2 wins, draws,
+   truncated, envs.  outcomes (B,) int8 / turns (B,) int32, or NULL: per-env
+   outcome (0 draw, 1 P1, 2 P2) and final move_count.  stuck rows ->
+   LX_EEMPTY_MASK only when check != 0 (syncs). */
+int lx_rollout(const lx_game *g, void *state, int64_t B, int max_turns, int mode, uint64_t seed,
+               const uint64_t *seeds, int64_t first_index, uint64_t *stats, void *work,
+               int8_t *outcomes, int32_t *turns, int check, int64_t *stuck_row, void *stream);
+
+/* device state <-> reference GameState arrays (device pointers) */
+int lx_export(const lx_game *g, const void *state, int64_t B, const lx_ref_state *ref,
+              void *stream);
+int lx_import(const lx_game *g, void *state, int64_t B, const lx_ref_state *ref, void *stream);
+
+/* CompiledGame.observe planes (compiler.py:611-626): (B, 3, C) uint8 */
+int lx_observe(const lx_game *g, const void *state, int64_t B, int player, uint8_t *planes,
+               void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,219 @@
+// lx_core.cuh -- bitboard, RNG and sampling primitives for the per-game
+// NVRTC translation units (sm_100a).  Self-contained: no CUDA or libc
+// headers, so NVRTC compiles it without an include path to the toolkit.
+//
+// Board encoding: one bit per cell in row-major cell order (cell i is bit
+// i%32 of 32-bit word i/32).  Bit order == cell order, which is what makes
+// "r-th set bit" equal the reference's "r-th legal cell in ascending index"
+// (reference mechanics.py:488-492).
+#pragma once
+
+typedef unsigned int u32;
+typedef unsigned long long u64;
+typedef long long i64;
+
+namespace lx {
+
+template <int W>
+struct BB {
+    u32 w[W];
+};
+
+template <int W>
+__device__ __forceinline__ BB<W> bb_zero() {
+    BB<W> r;
+#pragma unroll
+    for (int i = 0; i < W; i++) r.w[i] = 0u;
+    return r;
+}
+
+template <int W>
+__device__ __forceinline__ BB<W> operator&(const BB<W>& a, const BB<W>& b) {
+    BB<W> r;
+#pragma unroll
+    for (int i = 0; i < W; i++) r.w[i] = a.w[i] & b.w[i];
+    return r;
+}
+template <int W>
+__device__ __forceinline__ BB<W> operator|(const BB<W>& a, const BB<W>& b) {
+    BB<W> r;
+#pragma unroll
+    for (int i = 0; i < W; i++) r.w[i] = a.w[i] | b.w[i];
+    return r;
+}
+template <int W>
+__device__ __forceinline__ BB<W> operator^(const BB<W>& a, const BB<W>& b) {
+    BB<W> r;
+#pragma unroll
+    for (int i = 0; i < W; i++) r.w[i] = a.w[i] ^ b.w[i];
+    return r;
+}
+// a & ~b
+template <int W>
+__device__ __forceinline__ BB<W> andnot(const BB<W>& a, const BB<W>& b) {
+    BB<W> r;
+#pragma unroll
+    for (int i = 0; i < W; i++) r.w[i] = a.w[i] & ~b.w[i];
+    return r;
+}
+template <int W>
+__device__ __forceinline__ bool any(const BB<W>& a) {
+    u32 o = 0u;
+#pragma unroll
+    for (int i = 0; i < W; i++) o |= a.w[i];
+    return o != 0u;
+}
+template <int W>
+__device__ __forceinline__ bool equal(const BB<W>& a, const BB<W>& b) {
+    u32 o = 0u;
+#pragma unroll
+    for (int i = 0; i < W; i++) o |= a.w[i] ^ b.w[i];
+    return o == 0u;
+}
+template <int W>
+__device__ __forceinline__ int popc(const BB<W>& a) {
+    int n = 0;
+#pragma unroll
+    for (int i = 0; i < W; i++) n += __popc(a.w[i]);
+    return n;
+}
+// select without dynamic register indexing: s ? b : a
+template <int W>
+__device__ __forceinline__ BB<W> sel(bool s, const BB<W>& a, const BB<W>& b) {
+    BB<W> r;
+#pragma unroll
+    for (int i = 0; i < W; i++) r.w[i] = s ? b.w[i] : a.w[i];
+    return r;
+}
+
+// gather: result bit x = a bit (x + S).  S > 0 moves bits towards lower
+// indices.  Caller masks with the direction's validity mask.
+template <int W, int S>
+__device__ __forceinline__ BB<W> gather(const BB<W>& a) {
+    BB<W> r;
+    if constexpr (S == 0) {
+        return a;
+    } else if constexpr (S > 0) {
+        constexpr int q = S / 32;
+        constexpr unsigned s = (unsigned)(S % 32);
+#pragma unroll
+        for (int i = 0; i < W; i++) {
+            const u32 lo = (i + q < W) ? a.w[i + q] : 0u;
+            const u32 hi = (i + q + 1 < W) ? a.w[i + q + 1] : 0u;
+            r.w[i] = s ? __funnelshift_r(lo, hi, s) : lo;
+        }
+    } else {
+        constexpr int q = (-S) / 32;
+        constexpr unsigned s = (unsigned)((-S) % 32);
+#pragma unroll
+        for (int i = 0; i < W; i++) {
+            const u32 hi = (i - q >= 0) ? a.w[i - q] : 0u;
+            const u32 lo = (i - q - 1 >= 0) ? a.w[i - q - 1] : 0u;
+            r.w[i] = s ? __funnelshift_l(lo, hi, s) : hi;
+        }
+    }
+    return r;
+}
+
+// dynamic single-bit helpers (cell index c known only at run time); written
+// as unrolled compare/select so the board never leaves registers
+template <int W>
+__device__ __forceinline__ BB<W> onehot(int c) {
+    BB<W> r;
+    const u32 word = (u32)c >> 5, bit = 1u << (c & 31);
+#pragma unroll
+    for (int i = 0; i < W; i++) r.w[i] = (word == (u32)i) ? bit : 0u;
+    return r;
+}
+template <int W>
+__device__ __forceinline__ bool test(const BB<W>& a, int c) {
+    const u32 word = (u32)c >> 5;
+    u32 v = 0u;
+#pragma unroll
+    for (int i = 0; i < W; i++) v = (word == (u32)i) ? a.w[i] : v;
+    return (v >> (c & 31)) & 1u;
+}
+template <int W>
+__device__ __forceinline__ void setbit(BB<W>& a, int c) {
+    const u32 word = (u32)c >> 5, bit = 1u << (c & 31);
+#pragma unroll
+    for (int i = 0; i < W; i++) a.w[i] |= (word == (u32)i) ? bit : 0u;
+}
+template <int W>
+__device__ __forceinline__ void clearbit(BB<W>& a, int c) {
+    const u32 word = (u32)c >> 5, bit = 1u << (c & 31);
+#pragma unroll
+    for (int i = 0; i < W; i++) a.w[i] &= (word == (u32)i) ? ~bit : 0xffffffffu;
+}
+
+// position of the r-th (0-based) set bit of a 32-bit word; r < popc(x)
+__device__ __forceinline__ int select32(u32 x, int r) {
+    int pos = 0, c;
+    c = __popc(x & 0xffffu);
+    if (r >= c) { r -= c; x >>= 16; pos += 16; }
+    c = __popc(x & 0xffu);
+    if (r >= c) { r -= c; x >>= 8; pos += 8; }
+    c = __popc(x & 0xfu);
+    if (r >= c) { r -= c; x >>= 4; pos += 4; }
+    c = __popc(x & 0x3u);
+    if (r >= c) { r -= c; x >>= 2; pos += 2; }
+    c = (int)(x & 1u);
+    if (r >= c) { pos += 1; }
+    return pos;
+}
+
+// cell index of the r-th set bit (ascending cell order); r < popc(a)
+template <int W>
+__device__ __forceinline__ int select_bit(const BB<W>& a, int r) {
+    u32 word = 0u;
+    int base = 0, rem = r;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+        const int c = __popc(a.w[i]);
+        const bool here = !found && rem < c;
+        word = here ? a.w[i] : word;
+        base = here ? 32 * i : base;
+        rem = (!found && !here) ? rem - c : rem;
+        found = found || here;
+    }
+    return base + select32(word, rem);
+}
+
+// ---- counter RNG: splitmix64 finaliser (reference rng.py:12-42) ----------
+__device__ __forceinline__ u64 mix64(u64 z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+constexpr u64 HASH_SEED = 0x243F6A8885A308D3ull;
+
+// hash_key(seed) folded once; per-ply key = mix64(seedmix ^ move_count)
+__device__ __forceinline__ u64 seed_mix(u64 seed) { return mix64(HASH_SEED ^ seed); }
+
+// r = min(int64(u * n), max(n-1, 0)) with u = (key >> 11) * 2^-53, computed in
+// IEEE float64 exactly as numpy does (reference compiler.py:440-441)
+__device__ __forceinline__ int draw_index(u64 key, int n) {
+    const double u = __dmul_rn((double)(key >> 11), 0x1p-53);
+    i64 r = __double2ll_rz(__dmul_rn(u, (double)n));
+    const i64 hi = n > 1 ? (i64)(n - 1) : 0;
+    return (int)(r < hi ? r : hi);
+}
+
+__device__ __forceinline__ double key_uniform(u64 key) {
+    return __dmul_rn((double)(key >> 11), 0x1p-53);
+}
+
+// register-resident state of one env (unpacked from the HBM state words)
+template <int W, int NX>
+struct State {
+    BB<W> own0, own1;
+    u32 ext[NX > 0 ? NX : 1];
+    u32 mc;
+    int cur, term, trunc, outcome, phase, last_mover, last_kind, last_dest;
+    int pass_streak, pf0, pf1, ldbp0, ldbp1, sc0, sc1;
+    u64 seed;
+};
+
+}  // namespace lx

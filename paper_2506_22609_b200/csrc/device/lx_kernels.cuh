@@ -1,0 +1,483 @@
+// lx_kernels.cuh -- kernel templates instantiated once per game.
+//
+// Included at the end of every generated translation unit, after the
+// lowering has defined `struct Game` (constants + rule device functions, see
+// paper_2506_22609_b200/lowering.py).  All kernels are extern "C" so the
+// native runtime finds them by name in the NVRTC cubin.
+//
+// HBM layout of a batch of B envs ("state words"): each env is NQ*4 32-bit
+// words, stored quad-major -- quad q of env i lives at uint4 index q*B + i --
+// so a warp moves 512 contiguous bytes per 128-bit load.  Word map:
+//   [0, W)        P1 stones        [W, 2W)       P2 stones
+//   [2W, 2W+NX)   rule-private words (e.g. edge-connected stone sets)
+//   then 7 meta words (see pack/unpack below), zero padding to NQ*4.
+#pragma once
+
+namespace lx {
+
+
+template <class G>
+struct Layout {
+    static constexpr int W = G::W, NX = G::NX;
+    static constexpr int META = 2 * W + NX;
+    static constexpr int NWORDS = META + 7;
+    static constexpr int NQ = (NWORDS + 3) / 4;
+};
+
+template <class G>
+__device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<G>::NQ * 4]) {
+    constexpr int W = G::W, M = Layout<G>::META;
+#pragma unroll
+    for (int i = 0; i < W; i++) { s.own0.w[i] = w[i]; s.own1.w[i] = w[W + i]; }
+#pragma unroll
+    for (int i = 0; i < G::NX; i++) s.ext[i] = w[2 * W + i];
+    s.mc = w[M];
+    const u32 f = w[M + 1];
+    s.cur = f & 1u;
+    s.term = (f >> 1) & 1u;
+    s.trunc = (f >> 2) & 1u;
+    s.outcome = (int)((f >> 3) & 3u) - 1;
+    s.phase = (f >> 5) & 7u;
+    s.last_mover = (int)((f >> 8) & 3u) - 1;
+    s.pf0 = (f >> 10) & 1u;
+    s.pf1 = (f >> 11) & 1u;
+    s.last_kind = (int)((f >> 12) & 7u) - 1;
+    s.last_dest = (short)(w[M + 2] & 0xffffu);
+    s.pass_streak = (short)(w[M + 2] >> 16);
+    s.ldbp0 = (short)(w[M + 3] & 0xffffu);
+    s.ldbp1 = (short)(w[M + 3] >> 16);
+    s.sc0 = (short)(w[M + 4] & 0xffffu);
+    s.sc1 = (short)(w[M + 4] >> 16);
+    s.seed = (u64)w[M + 5] | ((u64)w[M + 6] << 32);
+}
+
+template <class G>
+__device__ __forceinline__ void pack(const typename G::St& s, u32 (&w)[Layout<G>::NQ * 4]) {
+    constexpr int W = G::W, M = Layout<G>::META;
+#pragma unroll
+    for (int i = 0; i < W; i++) { w[i] = s.own0.w[i]; w[W + i] = s.own1.w[i]; }
+#pragma unroll
+    for (int i = 0; i < G::NX; i++) w[2 * W + i] = s.ext[i];
+    w[M] = s.mc;
+    w[M + 1] = (u32)s.cur | ((u32)s.term << 1) | ((u32)s.trunc << 2) |
+               ((u32)(s.outcome + 1) << 3) | ((u32)s.phase << 5) |
+               ((u32)(s.last_mover + 1) << 8) | ((u32)s.pf0 << 10) | ((u32)s.pf1 << 11) |
+               ((u32)(s.last_kind + 1) << 12);
+    w[M + 2] = ((u32)s.last_dest & 0xffffu) | ((u32)s.pass_streak << 16);
+    w[M + 3] = ((u32)s.ldbp0 & 0xffffu) | ((u32)s.ldbp1 << 16);
+    w[M + 4] = ((u32)s.sc0 & 0xffffu) | ((u32)s.sc1 << 16);
+    w[M + 5] = (u32)s.seed;
+    w[M + 6] = (u32)(s.seed >> 32);
+#pragma unroll
+    for (int i = Layout<G>::NWORDS; i < Layout<G>::NQ * 4; i++) w[i] = 0u;
+}
+
+template <class G>
+__device__ __forceinline__ void load_state(typename G::St& s, const u32* __restrict__ st,
+                                           i64 B, i64 i) {
+    constexpr int NQ = Layout<G>::NQ;
+    u32 w[NQ * 4];
+    const uint4* q4 = reinterpret_cast<const uint4*>(st);
+#pragma unroll
+    for (int q = 0; q < NQ; q++) {
+        const uint4 v = q4[(i64)q * B + i];
+        w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+    unpack<G>(s, w);
+}
+
+template <class G>
+__device__ __forceinline__ void store_state(const typename G::St& s, u32* __restrict__ st,
+                                            i64 B, i64 i) {
+    constexpr int NQ = Layout<G>::NQ;
+    u32 w[NQ * 4];
+    pack<G>(s, w);
+    uint4* q4 = reinterpret_cast<uint4*>(st);
+#pragma unroll
+    for (int q = 0; q < NQ; q++)
+        q4[(i64)q * B + i] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+
+// start position (reference compiler.py:329-345 _build_template + init)
+template <class G>
+__device__ __forceinline__ void init_state(typename G::St& s, u64 seed) {
+    s.own0 = bb_zero<G::W>();
+    s.own1 = bb_zero<G::W>();
+#pragma unroll
+    for (int i = 0; i < (G::NX > 0 ? G::NX : 1); i++) s.ext[i] = 0u;
+    s.mc = 0u;
+    s.cur = G::FIRST_PLAYER;
+    s.term = 0; s.trunc = 0; s.outcome = -1; s.phase = 0;
+    s.last_mover = -1; s.last_kind = -1; s.last_dest = -1;
+    s.pass_streak = 0; s.pf0 = 0; s.pf1 = 0; s.ldbp0 = -1; s.ldbp1 = -1;
+    s.sc0 = 0; s.sc1 = 0;
+    s.seed = seed;
+    G::start(s);
+}
+
+// uniform legal action for the current mover; -1 when stuck
+// (reference compiler.py:430-446, mechanics.py:488-492)
+template <class G>
+__device__ __forceinline__ int sample_action(const typename G::St& s, u64 smix) {
+    const BB<G::W> legal = G::legal(s);
+    const int n = popc(legal);
+    if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
+    const int r = draw_index(mix64(smix ^ (u64)s.mc), n);
+    return select_bit(legal, r);
+}
+
+// one ply for a live row (reference compiler.py:456-580, order preserved:
+// mechanic write, pass bookkeeping, effects, score clamp, advancement,
+// ordered end rules evaluated for the mover, counters)
+template <class G>
+__device__ __forceinline__ void apply_step(typename G::St& s, int action) {
+    const int mover = s.cur;
+    const int phase = s.phase;
+    const bool is_pass = (G::PASS >= 0) && action == G::PASS;
+    if (is_pass) {
+        s.last_kind = 4; s.last_dest = -1; s.last_mover = mover;
+    } else {
+        G::write_place(s, action, mover, phase);
+    }
+    if (G::L_PASSING) {
+        if (is_pass) {
+            s.pass_streak += 1;
+            if (mover) s.pf1 = 1; else s.pf0 = 1;
+        } else {
+            s.pass_streak = 0;
+            if (mover) s.pf1 = 0; else s.pf0 = 0;
+        }
+    }
+    if (!is_pass) G::effects(s, action, mover, phase);
+    if (G::L_SCORES) {
+        s.sc0 = s.sc0 < 0 ? 0 : s.sc0;
+        s.sc1 = s.sc1 < 0 ? 0 : s.sc1;
+    }
+    int next_player, next_phase;
+    G::advance(phase, mover, next_player, next_phase);
+    const int out = G::end_rules(s, mover);
+    if (out >= 0) { s.term = 1; s.outcome = out; }
+    s.mc += 1u;
+    s.cur = next_player;
+    s.phase = next_phase;
+}
+
+// legality of one action (reference mechanics.py:499-512, compiler.py:484-494)
+template <class G>
+__device__ __forceinline__ bool action_legal(const typename G::St& s, i64 a) {
+    const BB<G::W> legal = G::legal(s);
+    if (G::PASS >= 0 && a == G::PASS) return !any(legal) && G::force_pass(s.phase);
+    if (a < 0 || a >= G::C) return false;
+    return test(legal, (int)a);
+}
+
+__device__ __forceinline__ i64 gtid() { return (i64)blockIdx.x * blockDim.x + threadIdx.x; }
+
+}  // namespace lx
+
+
+// ---------------------------------------------------------------- kernels
+
+struct LxRefPtrs {               // reference GameState field pointers (state.py:78-130)
+    signed char* board_piece;    // (B, C) int8, -1 empty
+    signed char* board_owner;    // (B, C) int8, -1 empty
+    signed char* current_player; // (B,)
+    int* move_count;             // (B,) int32
+    unsigned char* terminated;   // (B,) bool
+    unsigned char* truncated;    // (B,) bool
+    signed char* outcome;        // (B,) int8
+    unsigned long long* seeds;   // (B,) uint64
+    int* scores;                 // (B, 2) int32        or null
+    short* pass_streak;          // (B,) int16          or null
+    unsigned char* pass_flags;   // (B, 2) bool         or null
+    signed char* last_mover;     // (B,) int8           or null
+    signed char* last_kind;      // (B,) int8
+    short* last_source;          // (B,) int16
+    short* last_dest;            // (B,) int16
+    short* last_dest_by_player;  // (B, 2) int16
+    short* comp_labels;          // (B, 1, C) int16     or null
+    signed char* phase;          // (B,) int8           or null
+};
+
+extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const u64* seeds,
+                                                          u64 seed_base, i64 first) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    const u64 seed = seeds ? seeds[i] : lx::mix64(lx::seed_mix(seed_base) ^ (u64)(first + i));
+    lx::init_state<Game>(s, seed);
+    lx::store_state<Game>(s, st, B, i);
+}
+
+// (B, A) uint8 mask (null to skip) and (B,) int64 counts (null to skip);
+// terminated rows are all-false / zero (reference compiler.py:394-428)
+extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
+                                                           unsigned char* mask, i64* counts) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    lx::BB<Game::W> legal = Game::legal(s);
+    if (s.term) legal = lx::bb_zero<Game::W>();
+    const int n = lx::popc(legal);
+    const bool pass_only = !s.term && n == 0 && Game::force_pass(s.phase);
+    if (counts) counts[i] = s.term ? 0 : (pass_only ? 1 : n);
+    if (mask) {
+        unsigned char* row = mask + i * (i64)Game::A;
+#pragma unroll
+        for (int wd = 0; wd < Game::W; wd++) {
+            const u32 v = legal.w[wd];
+            for (int b = 0; b < 32; b++) {
+                const int c = wd * 32 + b;
+                if (c < Game::C) row[c] = (v >> b) & 1u;
+            }
+        }
+        if (Game::PASS >= 0) row[Game::C] = pass_only;
+    }
+}
+
+// sampled action per row from u (when given) or from the row's own stream
+extern "C" __global__ void __launch_bounds__(256) lx_sample(const u32* st, i64 B,
+                                                            const double* u, i64* actions) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    if (s.term) { actions[i] = -1; return; }
+    if (!u) { actions[i] = lx::sample_action<Game>(s, lx::seed_mix(s.seed)); return; }
+    const lx::BB<Game::W> legal = Game::legal(s);
+    const int n = lx::popc(legal);
+    if (n == 0) { actions[i] = Game::force_pass(s.phase) ? Game::PASS : -1; return; }
+    i64 r = __double2ll_rz(__dmul_rn(u[i], (double)n));
+    r = r < (i64)(n - 1) ? r : (i64)(n - 1);
+    actions[i] = lx::select_bit(legal, (int)r);
+}
+
+// verification pass: *bad = min illegal live row (init to ~0 by the caller)
+extern "C" __global__ void __launch_bounds__(256) lx_verify(const u32* st, i64 B,
+                                                            const i64* actions,
+                                                            const unsigned char* rows,
+                                                            u64* bad) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    if (rows && !rows[i]) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    if (s.term) return;
+    if (!lx::action_legal<Game>(s, actions[i])) atomicMin(bad, (u64)i);
+}
+
+// in-place step of live rows (rows & ~terminated)
+extern "C" __global__ void __launch_bounds__(256) lx_step(u32* st, i64 B, const i64* actions,
+                                                          const unsigned char* rows) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    if (rows && !rows[i]) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    if (s.term) return;
+    lx::apply_step<Game>(s, (int)actions[i]);
+    lx::store_state<Game>(s, st, B, i);
+}
+
+// fused sample+step for live rows, one ply (engine.random_actions + step_into)
+extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B, int max_turns,
+                                                                 i64* actions_out) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    if (s.term || (int)s.mc >= max_turns) { if (actions_out) actions_out[i] = -1; return; }
+    const int a = lx::sample_action<Game>(s, lx::seed_mix(s.seed));
+    if (actions_out) actions_out[i] = a;
+    if (a < 0) return;
+    lx::apply_step<Game>(s, a);
+    lx::store_state<Game>(s, st, B, i);
+}
+
+// Fused rollout.  Persistent threads: each thread plays one env to the end
+// with the whole state in registers, then claims the next env index with a
+// warp-aggregated atomic, so no lane idles while a long game finishes.
+//   mode & 1: start each env from its seed (seeds[i] or spawn(seed_base, first+i))
+//             else load it from st
+//   mode & 2: store the final state to st
+//   mode & 4: truncate unfinished envs at max_turns (engine.playout_random)
+// stats (u64[8], zeroed by the caller): steps, p1 wins, p2 wins, draws,
+// truncated, envs finished.  *counter must be zero.  *stuck = min row that
+// had no legal action (init ~0).
+extern "C" __global__ void __launch_bounds__(256) lx_rollout(u32* st, i64 B, int max_turns,
+                                                             int mode, u64 seed_base,
+                                                             const u64* seeds, i64 first,
+                                                             u64* stats, u64* counter,
+                                                             u64* stuck, signed char* outcomes,
+                                                             int* turns) {
+    const unsigned lane = threadIdx.x & 31u;
+    u64 n_steps = 0, n_p1 = 0, n_p2 = 0, n_draw = 0, n_trunc = 0, n_done = 0;
+    Game::St s;
+    u64 smix = 0;
+    i64 idx = -1;
+    bool need = true, active = true;
+    while (true) {
+        const unsigned want = __ballot_sync(0xffffffffu, need && active);
+        if (want) {
+            u64 base = 0;
+            const unsigned leader = __ffs(want) - 1;
+            if (lane == leader) base = atomicAdd(counter, (u64)__popc(want));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (need && active) {
+                idx = (i64)(base + __popc(want & ((1u << lane) - 1u)));
+                if (idx >= B) {
+                    active = false;
+                } else {
+                    if (mode & 1) {
+                        const u64 seed = seeds ? seeds[idx]
+                                               : lx::mix64(lx::seed_mix(seed_base) ^ (u64)(first + idx));
+                        lx::init_state<Game>(s, seed);
+                    } else {
+                        lx::load_state<Game>(s, st, B, idx);
+                    }
+                    smix = lx::seed_mix(s.seed);
+                    need = false;
+                }
+            }
+        }
+        if (!__any_sync(0xffffffffu, active)) break;
+        if (active) {
+            bool done = s.term || (int)s.mc >= max_turns;
+            if (!done) {
+                const int a = lx::sample_action<Game>(s, smix);
+                if (a < 0) {
+                    atomicMin(stuck, (u64)idx);
+                    done = true;
+                } else {
+                    lx::apply_step<Game>(s, a);
+                    n_steps++;
+                    done = s.term || (int)s.mc >= max_turns;
+                }
+            }
+            if (done) {
+                if ((mode & 4) && !s.term) { s.term = 1; s.trunc = 1; s.outcome = 0; }
+                n_p1 += s.outcome == 1;
+                n_p2 += s.outcome == 2;
+                n_draw += s.outcome == 0;
+                n_trunc += s.trunc;
+                n_done += 1;
+                if (mode & 2) lx::store_state<Game>(s, st, B, idx);
+                if (outcomes) outcomes[idx] = (signed char)s.outcome;
+                if (turns) turns[idx] = (int)s.mc;
+                need = true;
+            }
+        }
+    }
+    // warp reduce, one atomic per warp per counter
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        n_steps += __shfl_xor_sync(0xffffffffu, n_steps, o);
+        n_p1 += __shfl_xor_sync(0xffffffffu, n_p1, o);
+        n_p2 += __shfl_xor_sync(0xffffffffu, n_p2, o);
+        n_draw += __shfl_xor_sync(0xffffffffu, n_draw, o);
+        n_trunc += __shfl_xor_sync(0xffffffffu, n_trunc, o);
+        n_done += __shfl_xor_sync(0xffffffffu, n_done, o);
+    }
+    if (lane == 0) {
+        atomicAdd(stats + 0, n_steps);
+        atomicAdd(stats + 1, n_p1);
+        atomicAdd(stats + 2, n_p2);
+        atomicAdd(stats + 3, n_draw);
+        atomicAdd(stats + 4, n_trunc);
+        atomicAdd(stats + 5, n_done);
+    }
+}
+
+// device state -> reference GameState SoA (state.py:78-130)
+extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B, LxRefPtrs p) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    signed char* own = p.board_owner + i * Game::C;
+    signed char* pc = p.board_piece + i * Game::C;
+    for (int c = 0; c < Game::C; c++) {
+        const bool a = lx::test(s.own0, c), b = lx::test(s.own1, c);
+        own[c] = a ? 0 : (b ? 1 : -1);
+        pc[c] = (a || b) ? 0 : -1;
+    }
+    p.current_player[i] = (signed char)s.cur;
+    p.move_count[i] = (int)s.mc;
+    p.terminated[i] = (unsigned char)s.term;
+    p.truncated[i] = (unsigned char)s.trunc;
+    p.outcome[i] = (signed char)s.outcome;
+    p.seeds[i] = s.seed;
+    if (p.scores) { p.scores[2 * i] = s.sc0; p.scores[2 * i + 1] = s.sc1; }
+    if (p.pass_streak) {
+        p.pass_streak[i] = (short)s.pass_streak;
+        p.pass_flags[2 * i] = (unsigned char)s.pf0;
+        p.pass_flags[2 * i + 1] = (unsigned char)s.pf1;
+    }
+    if (p.last_mover) {
+        p.last_mover[i] = (signed char)s.last_mover;
+        p.last_kind[i] = (signed char)s.last_kind;
+        p.last_source[i] = -1;
+        p.last_dest[i] = (short)s.last_dest;
+        p.last_dest_by_player[2 * i] = (short)s.ldbp0;
+        p.last_dest_by_player[2 * i + 1] = (short)s.ldbp1;
+    }
+    if (p.comp_labels) Game::labels(s, p.comp_labels + i * Game::C);
+    if (p.phase) p.phase[i] = (signed char)s.phase;
+}
+
+// reference GameState SoA -> device state (inverse of lx_export)
+extern "C" __global__ void __launch_bounds__(128) lx_import(u32* st, i64 B, LxRefPtrs p) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    lx::init_state<Game>(s, p.seeds[i]);
+    s.own0 = lx::bb_zero<Game::W>();
+    s.own1 = lx::bb_zero<Game::W>();
+    const signed char* own = p.board_owner + i * Game::C;
+    for (int c = 0; c < Game::C; c++) {
+        if (own[c] == 0) lx::setbit(s.own0, c);
+        else if (own[c] == 1) lx::setbit(s.own1, c);
+    }
+    s.cur = p.current_player[i];
+    s.mc = (u32)p.move_count[i];
+    s.term = p.terminated[i];
+    s.trunc = p.truncated[i];
+    s.outcome = p.outcome[i];
+    s.sc0 = p.scores ? p.scores[2 * i] : 0;
+    s.sc1 = p.scores ? p.scores[2 * i + 1] : 0;
+    if (p.pass_streak) {
+        s.pass_streak = p.pass_streak[i];
+        s.pf0 = p.pass_flags[2 * i];
+        s.pf1 = p.pass_flags[2 * i + 1];
+    }
+    if (p.last_mover) {
+        s.last_mover = p.last_mover[i];
+        s.last_kind = p.last_kind[i];
+        s.last_dest = p.last_dest[i];
+        s.ldbp0 = p.last_dest_by_player[2 * i];
+        s.ldbp1 = p.last_dest_by_player[2 * i + 1];
+    }
+    s.phase = p.phase ? p.phase[i] : 0;
+    Game::rebuild_ext(s);
+    lx::store_state<Game>(s, st, B, i);
+}
+
+// (B, 3, C) uint8 relative-owner planes (reference compiler.py:611-626;
+// single piece type: own stones, opponent stones, is-mover plane)
+extern "C" __global__ void __launch_bounds__(128) lx_observe(const u32* st, i64 B, int player,
+                                                             unsigned char* planes) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    const lx::BB<Game::W> me = player ? s.own1 : s.own0;
+    const lx::BB<Game::W> op = player ? s.own0 : s.own1;
+    unsigned char* out = planes + i * (i64)(3 * Game::C);
+    const unsigned char mv = s.cur == player;
+    for (int c = 0; c < Game::C; c++) {
+        out[c] = lx::test(me, c);
+        out[Game::C + c] = lx::test(op, c);
+        out[2 * Game::C + c] = mv;
+    }
+}

@@ -1,0 +1,492 @@
+"""B200Game: the CompiledGame-compatible face of one lowered game, and
+DeviceState: a batch of envs held as bitboard SoA in HBM.
+
+Drop-in surface (reference: pkg/src/boardlang/compiler.py:197-650):
+``init``, ``legal_mask``, ``legal_counts``, ``sample_actions``, ``step``,
+``step_into``, ``observe``, ``describe``, ``codec``, ``layout``,
+``action_space_size``, ``pass_index``.  Host-facing methods accept and
+return numpy arrays exactly like the reference; every computation runs in
+the game's sm_100a kernels.  ``*_device`` variants keep inputs and outputs
+as CUDA tensors for zero-copy pipelines (``env.LudaxEnvironment``).
+
+A DeviceState answers the reference GameState attribute names
+(``board_owner``, ``terminated``, ``scores``, ... state.py:78-130) by
+exporting the device words through ``lx_export`` on first access, so
+reference-style code (``state.terminated.all()``, ``state.digest()``)
+works unchanged.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .errors import CompileError, EmptyMask
+from .lowering import lower_game
+from .syntax import parse_game
+
+GAMES_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "games")
+
+FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
+          "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags", "must_move",
+          "last_mover", "last_kind", "last_source", "last_dest", "last_dest_by_player",
+          "hopped_mask", "captured_mask", "promoted_mask", "comp_labels", "phase", "turn_pos")
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2506_22609_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return torch
+
+
+@dataclass(frozen=True)
+class ActionCodec:
+    """Placement codec: action = cell, trailing pass (reference codec.py:16-69)."""
+    kind: str
+    num_cells: int
+    size: int
+    has_pass: bool
+
+    @property
+    def pass_index(self):
+        return self.size - 1 if self.has_pass else None
+
+    def encode(self, source, dest):
+        return dest
+
+    def decode(self, action):
+        if self.has_pass and action == self.pass_index:
+            return None, None
+        return None, action
+
+    def describe(self, action):
+        if self.has_pass and action == self.pass_index:
+            return {"kind": "pass"}
+        return {"kind": "place", "dest": action}
+
+
+@dataclass(frozen=True)
+class StateLayout:
+    """Which reference GameState fields this game materialises (state.py:34-66)."""
+    scores: bool = False
+    passing: bool = False
+    must_move: bool = False
+    last_action: bool = False
+    transient_masks: bool = False
+    connectivity: int = 0
+    phase: bool = False
+    turn_pos: bool = False
+
+
+class DeviceState:
+    """Batch of envs in HBM: int32 words shaped (NQ, B, 4), quad-major."""
+
+    def __init__(self, game, words, batch_size):
+        self.game = game
+        self.words = words
+        self.batch_size = batch_size
+        self._host = None
+
+    # -- value semantics --
+    def copy(self):
+        return DeviceState(self.game, self.words.clone(), self.batch_size)
+
+    def _touch(self):
+        self._host = None
+
+    # -- reference field view --
+    def host(self):
+        """dict of numpy arrays in the reference GameState layout."""
+        if self._host is None:
+            self._host = self.game._export(self)
+        return self._host
+
+    def __getattr__(self, name):
+        if name in FIELDS:
+            return self.host().get(name)
+        raise AttributeError(name)
+
+    def digest(self):
+        """Same bytes as the reference GameState.digest (state.py:180-188)."""
+        h = hashlib.blake2b(digest_size=16)
+        host = self.host()
+        for name in FIELDS:
+            v = host.get(name)
+            if v is not None:
+                h.update(name.encode())
+                h.update(np.ascontiguousarray(v).tobytes())
+        return h.hexdigest()
+
+    def nbytes(self):
+        return sum(v.nbytes for v in self.host().values())
+
+    def device_nbytes(self):
+        return self.words.numel() * 4
+
+    def rows(self, idx):
+        idx = np.atleast_1d(np.asarray(idx))
+        torch = _torch()
+        t = torch.as_tensor(idx, device=self.words.device, dtype=torch.long)
+        return DeviceState(self.game, self.words[:, t].contiguous(), len(idx))
+
+    @classmethod
+    def concat(cls, states):
+        torch = _torch()
+        w = torch.cat([s.words for s in states], dim=1).contiguous()
+        return cls(states[0].game, w, sum(s.batch_size for s in states))
+
+    def set_rows(self, idx, other):
+        torch = _torch()
+        t = torch.as_tensor(np.atleast_1d(np.asarray(idx)), device=self.words.device,
+                            dtype=torch.long)
+        self.words[:, t] = other.words
+        self._touch()
+
+    def equal(self, other):
+        return self.digest() == other.digest()
+
+
+class B200Game:
+    """One game lowered to sm_100a kernels (CompiledGame drop-in)."""
+
+    def __init__(self, spec, text=None):
+        self.spec = spec
+        lowered = lower_game(spec)
+        self.lowered = lowered
+        self.info = lowered.info
+        self.name = spec.name
+        self.num_cells = lowered.info["C"]
+        L = lowered.info["layout"]
+        self.layout = StateLayout(**{k: L[k] for k in StateLayout.__dataclass_fields__})
+        self.codec = ActionCodec("placement", self.num_cells, lowered.info["A"],
+                                 lowered.info["pass_index"] >= 0)
+        self.piece_names = tuple(p.name for p in spec.equipment.pieces)
+        self._native = None
+        self._nq = lowered.info["nq"]
+
+    # -- native handle (lazy: needs the CUDA context) --
+    @property
+    def native(self):
+        if self._native is None:
+            _torch().cuda.current_device()
+            self._native = native.NativeGame(self.lowered.source, self.name)
+        return self._native
+
+    @property
+    def handle(self):
+        return self.native.h
+
+    def lowered_key(self):
+        """Content hash of the generated translation unit (profiles are keyed on it)."""
+        return self.lowered.key
+
+    @staticmethod
+    def _stream():
+        torch = _torch()
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    @property
+    def action_space_size(self):
+        return self.codec.size
+
+    @property
+    def pass_index(self):
+        return self.codec.pass_index
+
+    @property
+    def observation_planes(self):
+        return 2 * len(self.piece_names) + 1
+
+    def describe(self):
+        b = self.spec.equipment.board
+        return {"name": self.name,
+                "board": {"kind": b.kind, "rows": b.rows, "cols": b.cols},
+                "num_cells": self.num_cells, "pieces": list(self.piece_names),
+                "action_space": {"kind": "placement", "size": self.codec.size,
+                                 "has_pass": self.codec.has_pass},
+                "observation_planes": self.observation_planes,
+                "phases": len(self.spec.phases),
+                "state_layout": {"scores": self.layout.scores, "passing": self.layout.passing,
+                                 "must_move": False, "last_action": self.layout.last_action,
+                                 "transient_masks": False,
+                                 "connectivity_plans": self.layout.connectivity,
+                                 "phase_index": self.layout.phase, "turn_position": False},
+                "device_state_bytes": self._nq * 16}
+
+    # -- allocation --
+    def empty_state(self, B):
+        torch = _torch()
+        w = torch.empty((self._nq, B, 4), dtype=torch.int32, device="cuda")
+        return DeviceState(self, w, B)
+
+    def init(self, batch_size=1, seed=0, seeds=None, first_index=0):
+        """CompiledGame.init (compiler.py:357-364); seeds spawned on device."""
+        torch = _torch()
+        st = self.empty_state(batch_size)
+        seeds_t = None
+        if seeds is not None:
+            seeds_t = _u64_tensor(seeds, batch_size)
+        native.check(native.lib().lx_init(
+            self.handle, st.words.data_ptr(), batch_size,
+            seeds_t.data_ptr() if seeds_t is not None else None,
+            int(seed) & (2 ** 64 - 1), int(first_index), self._stream()))
+        del torch
+        return st
+
+    # -- legality / sampling --
+    def legal_mask_device(self, state):
+        torch = _torch()
+        B = state.batch_size
+        mask = torch.empty((B, self.codec.size), dtype=torch.uint8, device="cuda")
+        native.check(native.lib().lx_legal(self.handle, state.words.data_ptr(), B,
+                                           mask.data_ptr(), None, self._stream()))
+        return mask.view(torch.bool)
+
+    def legal_counts_device(self, state):
+        torch = _torch()
+        B = state.batch_size
+        counts = torch.empty(B, dtype=torch.int64, device="cuda")
+        native.check(native.lib().lx_legal(self.handle, state.words.data_ptr(), B, None,
+                                           counts.data_ptr(), self._stream()))
+        return counts
+
+    def legal_mask(self, state, mover=None):
+        """(B, A) bool numpy; all-false for terminated rows (compiler.py:411-428)."""
+        _no_mover_override(mover, state)
+        return self.legal_mask_device(state).cpu().numpy()
+
+    def legal_counts(self, state, mover=None):
+        _no_mover_override(mover, state)
+        return self.legal_counts_device(state).cpu().numpy()
+
+    def sample_actions_device(self, state, u=None):
+        torch = _torch()
+        B = state.batch_size
+        out = torch.empty(B, dtype=torch.int64, device="cuda")
+        u_t = None
+        if u is not None:
+            u_t = u if isinstance(u, torch.Tensor) else torch.as_tensor(
+                np.ascontiguousarray(u, dtype=np.float64))
+            u_t = u_t.to(device="cuda", dtype=torch.float64).contiguous()
+        native.check(native.lib().lx_sample(self.handle, state.words.data_ptr(), B,
+                                            u_t.data_ptr() if u_t is not None else None,
+                                            out.data_ptr(), self._stream()))
+        return out
+
+    def sample_actions(self, state, u, mover=None):
+        """Uniform legal action per row from a (B,) float64 draw (compiler.py:430-446)."""
+        _no_mover_override(mover, state)
+        return self.sample_actions_device(state, u).cpu().numpy()
+
+    # -- stepping --
+    def step(self, state, actions):
+        """Pure step (compiler.py:450-454): copy, then verified step_into."""
+        out = state.copy()
+        self.step_into(out, actions, verify=True)
+        return out
+
+    def step_into(self, state, actions, rows=None, verify=True):
+        """In-place step on rows & ~terminated (compiler.py:456-580)."""
+        torch = _torch()
+        B = state.batch_size
+        a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(
+            np.broadcast_to(np.asarray(actions, dtype=np.int64), (B,)).copy())
+        a = a.to(device="cuda", dtype=torch.int64).contiguous()
+        r = None
+        if rows is not None:
+            r = rows if isinstance(rows, torch.Tensor) else torch.as_tensor(
+                np.ascontiguousarray(rows, dtype=bool))
+            r = r.to(device="cuda", dtype=torch.uint8).contiguous()
+        scratch = torch.empty(1, dtype=torch.int64, device="cuda") if verify else None
+        bad = ctypes.c_int64(-1)
+        st = native.lib().lx_step(self.handle, state.words.data_ptr(), B, a.data_ptr(),
+                                  r.data_ptr() if r is not None else None, int(bool(verify)),
+                                  scratch.data_ptr() if scratch is not None else None,
+                                  ctypes.byref(bad), self._stream())
+        native.check(st, bad.value)
+        state._touch()
+
+    def random_step(self, state, max_turns=200, record=False):
+        """One fused uniform-random ply for live rows; returns actions if record."""
+        torch = _torch()
+        B = state.batch_size
+        out = torch.empty(B, dtype=torch.int64, device="cuda") if record else None
+        native.check(native.lib().lx_random_step(self.handle, state.words.data_ptr(), B,
+                                                 int(max_turns),
+                                                 out.data_ptr() if out is not None else None,
+                                                 self._stream()))
+        state._touch()
+        return out
+
+    def rollout(self, batch_size=None, seed=0, seeds=None, state=None, max_turns=200,
+                store=True, truncate=True, first_index=0, check=True, stats=None, work=None,
+                outcomes=None, turns=None, out=None):
+        """Fused register-resident rollout (kernel lx_rollout).
+
+        Without ``state``: envs start from ``seeds`` (or spawn(seed, first_index+i))
+        and, with ``store``, the final states are written to ``out`` (allocated
+        when None) and returned.  With ``state``: continue those envs in place.
+        Returns (final DeviceState or None, stats tensor u64[8]: steps, p1, p2,
+        draws, truncated, envs).
+        """
+        torch = _torch()
+        mode = 0
+        if state is None:
+            mode |= 1
+            B = int(batch_size) if batch_size is not None else (
+                out.batch_size if out is not None else len(seeds))
+            if store:
+                state = out if out is not None else self.empty_state(B)
+        else:
+            B = state.batch_size
+        if store:
+            mode |= 2
+        if truncate:
+            mode |= 4
+        seeds_t = _u64_tensor(seeds, B) if seeds is not None else None
+        if stats is None:
+            stats = torch.empty(8, dtype=torch.int64, device="cuda")
+        if work is None:
+            work = torch.empty(4, dtype=torch.int64, device="cuda")
+        stuck = ctypes.c_int64(-1)
+        st = native.lib().lx_rollout(
+            self.handle, state.words.data_ptr() if state is not None else None, B,
+            int(max_turns), mode, int(seed) & (2 ** 64 - 1),
+            seeds_t.data_ptr() if seeds_t is not None else None, int(first_index),
+            stats.data_ptr(), work.data_ptr(),
+            outcomes.data_ptr() if outcomes is not None else None,
+            turns.data_ptr() if turns is not None else None,
+            int(bool(check)), ctypes.byref(stuck),
+            self._stream())
+        native.check(st, stuck.value)
+        if state is not None:
+            state._touch()
+        return state, stats
+
+    # -- observation --
+    def observe_device(self, state, player):
+        torch = _torch()
+        B = state.batch_size
+        planes = torch.empty((B, 3, self.num_cells), dtype=torch.uint8, device="cuda")
+        native.check(native.lib().lx_observe(self.handle, state.words.data_ptr(), B,
+                                             int(player), planes.data_ptr(), self._stream()))
+        return planes.view(torch.bool)
+
+    def observe(self, state, player):
+        """(B, 2T+1, C) relative-owner planes + legal mask (compiler.py:611-626)."""
+        return (self.observe_device(state, player).cpu().numpy(),
+                self.legal_mask(state))
+
+    # -- reference layout interchange --
+    def ref_arrays(self, B, device):
+        torch = _torch()
+        C, L = self.num_cells, self.layout
+        f = {"board_piece": ((B, C), torch.int8), "board_owner": ((B, C), torch.int8),
+             "current_player": ((B,), torch.int8), "move_count": ((B,), torch.int32),
+             "terminated": ((B,), torch.bool), "truncated": ((B,), torch.bool),
+             "outcome": ((B,), torch.int8), "seeds": ((B,), torch.int64)}
+        if L.scores:
+            f["scores"] = ((B, 2), torch.int32)
+        if L.passing:
+            f["pass_streak"] = ((B,), torch.int16)
+            f["pass_flags"] = ((B, 2), torch.bool)
+        if L.last_action:
+            f.update({"last_mover": ((B,), torch.int8), "last_kind": ((B,), torch.int8),
+                      "last_source": ((B,), torch.int16), "last_dest": ((B,), torch.int16),
+                      "last_dest_by_player": ((B, 2), torch.int16)})
+        if L.connectivity:
+            f["comp_labels"] = ((B, 1, C), torch.int16)
+        if L.phase:
+            f["phase"] = ((B,), torch.int8)
+        return {k: torch.empty(shape, dtype=dt, device=device) for k, (shape, dt) in f.items()}
+
+    def _ref_struct(self, tensors):
+        return native.RefState(**{k: (tensors[k].data_ptr() if k in tensors else None)
+                                  for k in native.REF_FIELDS})
+
+    def export_device(self, state):
+        """Device tensors in the reference GameState layout (lx_export)."""
+        t = self.ref_arrays(state.batch_size, "cuda")
+        ref = self._ref_struct(t)
+        native.check(native.lib().lx_export(self.handle, state.words.data_ptr(),
+                                            state.batch_size, ctypes.byref(ref), self._stream()))
+        return t
+
+    def _export(self, state):
+        t = self.export_device(state)
+        out = {}
+        for k, v in t.items():
+            a = v.cpu().numpy()
+            if k == "seeds":
+                a = a.view(np.uint64)
+            out[k] = a
+        return out
+
+    def from_reference(self, arrays):
+        """DeviceState from reference-layout numpy arrays (lx_import)."""
+        torch = _torch()
+        B = len(arrays["seeds"])
+        t = {}
+        for k, v in arrays.items():
+            if v is None or k not in native.REF_FIELDS:
+                continue
+            a = np.ascontiguousarray(v)
+            if a.dtype == np.uint64:
+                a = a.view(np.int64)
+            t[k] = torch.as_tensor(a).to("cuda")
+        st = self.empty_state(B)
+        ref = self._ref_struct(t)
+        native.check(native.lib().lx_import(self.handle, st.words.data_ptr(), B,
+                                            ctypes.byref(ref), self._stream()))
+        torch.cuda.current_stream().synchronize()
+        return st
+
+
+def _no_mover_override(mover, state):
+    if mover is not None:
+        raise NotImplementedError("legality for a non-current mover is not lowered yet")
+
+
+def _u64_tensor(seeds, B):
+    torch = _torch()
+    if isinstance(seeds, torch.Tensor):
+        return seeds.to(device="cuda", dtype=torch.int64).contiguous()
+    a = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(B)).view(np.int64)
+    return torch.as_tensor(a).to("cuda")
+
+
+def compile_game(spec):
+    return B200Game(spec)
+
+
+def load_game(text):
+    """Parse + lower (+ NVRTC on first device use); raises on any failure
+    (reference __init__.py:34-41 load_game)."""
+    spec = parse_game(text)
+    return B200Game(spec, text)
+
+
+def load_config_game(name):
+    with open(os.path.join(GAMES_DIR, f"{name}.ldx")) as f:
+        return load_game(f.read())
+
+
+def precompile(names=("tic_tac_toe", "connect_four", "hex", "reversi", "pente")):
+    """NVRTC-compile the config games' cubins into the in-tree cache (no GPU)."""
+    keys = {}
+    for name in names:
+        with open(os.path.join(GAMES_DIR, f"{name}.ldx")) as f:
+            low = lower_game(parse_game(f.read()))
+        keys[name] = native.compile_only(low.source, low.name)
+    return keys
+
+
+__all__ = ["B200Game", "DeviceState", "ActionCodec", "StateLayout", "load_game",
+           "load_config_game", "compile_game", "precompile", "CompileError", "EmptyMask"]

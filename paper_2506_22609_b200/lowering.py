@@ -1,0 +1,848 @@
+"""Lowering: parsed game AST -> one CUDA translation unit per game.
+
+The reference compiles each AST node into a numpy closure over (B, C)
+arrays (reference: pkg/src/boardlang/compiler.py:197-650, exprs.py,
+effects.py, mechanics.py:415-515).  Here every node becomes a fragment of a
+``struct Game`` whose device functions operate on one env's bitboards held
+in registers; ``csrc/device/lx_kernels.cuh`` then instantiates the kernels
+(init, legal, sample, step, fused rollout, export/import) around it and the
+native runtime compiles the unit with NVRTC for sm_100a.
+
+Supported subset (the five config games): placement
+mechanics on square / rectangle / hex_rectangle boards with one piece type;
+masks empty/occupied/edge/center/corners/row/column/region/adjacent/
+and/or/not and custodial (as placement result and as flip/capture effect);
+functions count/score/constant/line/connected/add/multiply/subtract;
+predicates and/or/not/exists/full_board/mover_is/>=/<=/=/passed/line;
+effects flip/capture/set_score/increment_score/if; phases repeat /
+once_through / force_pass; results win/lose/draw/by_score.  Anything else
+raises CompileError("lower", ...) -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import nodes as n
+from .errors import CompileError, UnsupportedConstruct
+from .geometry import OPPOSITE, Board, direction_pairs, resolve_direction
+
+ANCHOR_COST_THRESHOLD = 128          # reference compiler.py:28
+
+
+def _fail(msg):
+    raise CompileError("lower", msg)
+
+
+@dataclass
+class Lowered:
+    name: str
+    source: str
+    info: dict = field(default_factory=dict)
+
+    @property
+    def key(self):
+        return hashlib.sha256(self.source.encode()).hexdigest()[:24]
+
+
+class _Emitter:
+    """Collects constants and helper functions while expressions are built."""
+
+    def __init__(self, board, W):
+        self.board, self.W = board, W
+        self.consts = {}          # words tuple -> name
+        self.helpers = {}         # name -> code
+        self.counter = 0
+
+    def const(self, mask):
+        words = _words(mask, self.W)
+        if words not in self.consts:
+            self.consts[words] = f"K{len(self.consts)}"
+        return f"{self.consts[words]}()"
+
+    def fresh(self, base="t"):
+        self.counter += 1
+        return f"{base}{self.counter}"
+
+    def helper(self, name, code):
+        self.helpers.setdefault(name, code)
+        return name
+
+    def const_defs(self):
+        out = []
+        for words, name in self.consts.items():
+            lit = ", ".join(f"0x{w:08x}u" for w in words)
+            out.append(f"    static __device__ __forceinline__ BBW {name}() {{ return BBW{{{{{lit}}}}}; }}")
+        return "\n".join(out)
+
+
+def _words(mask, W):
+    m = np.zeros(W * 32, dtype=bool)
+    m[:len(mask)] = mask
+    return tuple(int(x) for x in np.packbits(m.reshape(W, 32)[:, ::-1], axis=1)
+                 .view(">u4").reshape(W))
+
+
+class GameLowering:
+    """Walks one validated GameSpec and produces its Lowered unit."""
+
+    def __init__(self, spec):
+        self.spec = spec
+        self.board = Board(spec.equipment.board)
+        B = self.board
+        if B.family == "hexagon":
+            _fail("hexagon boards are not lowered yet (rows are not shift-regular)")
+        self.C = B.num_cells
+        self.W = (self.C + 31) // 32
+        self.em = _Emitter(B, self.W)
+        self.piece_ids = {p.name: i for i, p in enumerate(spec.equipment.pieces)}
+        if len(self.piece_ids) != 1:
+            _fail("only single-piece-type games are lowered (board_piece is implied)")
+        self.forward = dict(spec.players.forward)
+        self.regions = {}
+        for r in spec.equipment.regions:
+            self.regions[r.name] = (B.mask_of(r.cells) if r.cells
+                                    else self._static_union(r.masks))
+        self.valid = np.ones(self.C, dtype=bool)
+        self._shift = {}
+        for d in B.directions:
+            self._shift[d] = self._check_shift(d)
+        self.conn_plans = []
+        self._scan()
+
+    # ------------------------------------------------------------ geometry
+
+    def _check_shift(self, d):
+        """Prove nbr_d(x) == x + S for every x with a d-neighbour."""
+        nt = self.board.neighbors[d]
+        deltas = {int(nt[x]) - x for x in range(self.C) if nt[x] != self.C}
+        if len(deltas) > 1:
+            _fail(f"direction {d} is not a constant cell shift on this board")
+        return deltas.pop() if deltas else 0
+
+    def _walk_ok(self, d, k):
+        nt = self.board.neighbors[d]
+        x = np.arange(self.C)
+        for _ in range(k):
+            x = nt[x]
+        return x != self.C
+
+    def walk(self, d, k, expr):
+        """Expression: bit x = expr bit (x + k*S_d), masked to valid walks."""
+        S = self._shift[d] * k
+        name = f"walk_{d}_{k}"
+        mask = self.em.const(self._walk_ok(d, k))
+        self.em.helper(name, f"    static __device__ __forceinline__ BBW {name}(const BBW& x) "
+                             f"{{ return lx::gather<W, {S}>(x) & {mask}; }}")
+        return f"{name}({expr})"
+
+    def nb(self, d, expr):
+        """neighbour gather: bit x = expr bit at nbr_d(x) (0 off-board)."""
+        return self.walk(d, 1, expr)
+
+    # ------------------------------------------------------------ scan / layout
+
+    def _scan(self):
+        """StateLayout + codec facts (reference compiler.py:98-152, 200-221)."""
+        spec = self.spec
+        allnodes = list(n.walk(spec))
+        types = {type(x) for x in allnodes}
+        for t in (n.MoveMechanic, n.HopMove, n.SlideMove, n.StepMove):
+            if t in types:
+                _fail("movement mechanics are not lowered yet (SURVEY 8f row 3)")
+        for t in (n.PromoteEffect, n.ExtraTurnEffect, n.CapturedMask, n.HoppedMask,
+                  n.PromotedMask, n.PrevMoveMask, n.LastMoveInPred, n.ActionWasPred,
+                  n.CanMoveAgainPred, n.NoLegalActionsPred, n.CornerCustodialMask,
+                  n.PatternFn):
+            if t in types:
+                _fail(f"{t.__name__} is not lowered yet")
+        self.has_flip = n.FlipEffect in types
+        scores = any(t in types for t in (n.ScoreFn, n.SetScoreEffect, n.IncrementScoreEffect))
+        scores |= any(isinstance(x, n.CaptureEffect) and x.increment_score for x in allnodes)
+        scores |= any(r.result.kind == "by_score" for r in spec.end_rules)
+        passing = any(p.force_pass for p in spec.phases) or n.PassedPred in types
+        last_action = any(t in types for t in (n.CustodialMask,))
+        for x in allnodes:
+            if isinstance(x, n.ConnectedFn):
+                self._conn_plan(x)
+        # anchored line candidates (reference compiler.py:122-135)
+        self.anchor_lines = set()
+        cands = []
+        if not self.has_flip:
+            for rule in spec.end_rules:
+                for x in n.walk(rule.condition):
+                    if isinstance(x, n.FunctionPred) and isinstance(x.fn, n.LineFn):
+                        line = x.fn
+                        if line.player != n.MOVER:
+                            continue
+                        T = len(self.board.line_windows(line.length, line.orientation))
+                        if T * line.length > ANCHOR_COST_THRESHOLD:
+                            cands.append(line)
+        self.phase_mult = len(spec.phases) > 1 or any(p.kind == "once_through"
+                                                      for p in spec.phases)
+        if any(len(p.order) != len(set(p.order)) for p in spec.phases):
+            _fail("repeated players in a mover order (turn_pos layout) are not lowered yet")
+        self.has_pass = passing
+        self.layout = {"scores": scores, "passing": passing, "must_move": False,
+                       "last_action": last_action or bool(cands),
+                       "transient_masks": False, "connectivity": len(self.conn_plans),
+                       "phase": self.phase_mult, "turn_pos": False}
+        self._anchor_candidates = cands
+        self._last_action_base = last_action
+        if len(self.conn_plans) > 1:
+            _fail("more than one connectivity direction plan is not lowered yet")
+        self.A = self.C + (1 if passing else 0)
+        self.PASS = self.C if passing else -1
+
+    def _conn_plan(self, node):
+        dirs = resolve_direction(node.directions or ("any",), n.P1, self.forward, self.board)
+        if dirs not in self.conn_plans:
+            self.conn_plans.append(dirs)
+        return self.conn_plans.index(dirs)
+
+    # ------------------------------------------------------------ static masks
+
+    def static_mask(self, node):
+        """(C,) bool for geometry-only masks, else None (reference exprs.py:42-88)."""
+        t = type(node)
+        B = self.board
+        if t is n.CenterMask:
+            return B.center_mask
+        if t is n.CornersMask:
+            return B.corners_mask
+        if t is n.RowMask:
+            return np.asarray(B.row_of == node.index)
+        if t is n.ColumnMask:
+            return np.asarray(B.col_of == node.index)
+        if t is n.EdgeMask and node.which not in ("forward", "backward"):
+            return B.edge_masks[node.which]
+        if t is n.RegionMask:
+            return self.regions[node.region]
+        if t is n.MultiMask:
+            out = np.zeros(self.C, dtype=bool)
+            for m in B.multi_mask(node.kind):
+                out |= m
+            return out
+        if t in (n.MaskAnd, n.MaskOr):
+            parts = [self.static_mask(i) for i in node.items]
+            if any(p is None for p in parts):
+                return None
+            out = parts[0].copy()
+            for p in parts[1:]:
+                out = (out & p) if t is n.MaskAnd else (out | p)
+            return out
+        if t is n.MaskNot:
+            inner = self.static_mask(node.item)
+            return None if inner is None else ~inner
+        return None
+
+    def _static_union(self, masks):
+        out = np.zeros(self.C, dtype=bool)
+        for m in masks:
+            s = self.static_mask(m)
+            if s is None:
+                _fail(f"{type(m).__name__} is not a static mask")
+            out |= s
+        return out
+
+    # ------------------------------------------------------------ expressions
+    # All expression code assumes locals: s (state), mover (int), me / op (BBW)
+
+    @staticmethod
+    def side(ref):
+        if ref in (n.MOVER, ""):
+            return "mover"
+        if ref == n.OPPONENT:
+            return "(1 - mover)"
+        if ref in ("P1", 0):
+            return "0"
+        if ref in ("P2", 1):
+            return "1"
+        _fail(f"cannot resolve side reference {ref!r}")
+
+    @staticmethod
+    def stones(side_expr):
+        if side_expr == "mover":
+            return "me"
+        if side_expr == "(1 - mover)":
+            return "op"
+        return "s.own0" if side_expr == "0" else "s.own1"
+
+    def mask(self, node):
+        st = self.static_mask(node)
+        if st is not None:
+            return self.em.const(st)
+        t = type(node)
+        if t is n.EmptyMask:
+            return f"lx::andnot({self.em.const(self.valid)}, s.own0 | s.own1)"
+        if t is n.OccupiedMask:
+            if not node.who:
+                return "(s.own0 | s.own1)"
+            return self.stones(self.side(node.who))
+        if t is n.EdgeMask:              # forward / backward edges per player
+            names = []
+            for pl in (n.P1, n.P2):
+                facing = self.forward.get(pl)
+                if facing is None:
+                    _fail("edge forward/backward needs set_forward")
+                if node.which == "backward":
+                    facing = OPPOSITE[facing]
+                names.append(self.em.const(self.board.edge_masks[
+                    {"up": "top", "down": "bottom", "left": "left", "right": "right"}[facing]]))
+            return f"lx::sel(mover != 0, {names[0]}, {names[1]})"
+        if t is n.AdjacentMask:
+            inner = self.mask(node.inner)
+            tmp = self.em.fresh("adj")
+            parts = []
+            for d1, d2 in direction_pairs(node.directions or ("any",), self.forward, self.board):
+                a = self.nb(OPPOSITE[d1], tmp)
+                if d1 == d2:
+                    parts.append(a)
+                else:
+                    parts.append(f"lx::sel(mover != 0, {a}, {self.nb(OPPOSITE[d2], tmp)})")
+            body = " | ".join(parts)
+            return f"([&]() {{ const BBW {tmp} = {inner}; return BBW({body}); }}())"
+        if t in (n.MaskAnd, n.MaskOr):
+            op = " & " if t is n.MaskAnd else " | "
+            return "(" + op.join(self.mask(i) for i in node.items) + ")"
+        if t is n.MaskNot:
+            return f"lx::andnot({self.em.const(self.valid)}, {self.mask(node.item)})"
+        if t is n.CustodialMask:
+            return self.custodial_anchored(node)
+        _fail(f"mask {t.__name__} is not lowered yet")
+
+    # -- custodial ------------------------------------------------------------
+
+    def custodial_dirs(self, node):
+        dirs = []
+        for d in self.board.orientation_dirs(node.orientation):
+            dirs += [d, OPPOSITE[d]]
+        return dirs
+
+    def custodial_anchored(self, node):
+        """Anchored custodial runs from last_dest (reference exprs.py:254-292).
+
+        For each walk direction, the run of target stones that starts next to
+        the anchor is kept when the next cell is a flanker; ``length`` fixes
+        the run length.  The reference bounds runs by the padded ray length
+        L (runlen < L), which any flanked run on the board satisfies.
+        """
+        side = self.side(node.mover)
+        name = f"custodial_{self.em.fresh('c')}"
+        lines = []
+        for d in self.custodial_dirs(node):
+            steps = self.board.ray_length(d) - 1 if node.length == "any" else node.length
+            steps = max(steps, 0)
+            if steps == 0:
+                continue
+            lines.append("        {")
+            lines.append("            BBW x = " + self.nb(OPPOSITE[d], "a") + " & tgt;")
+            lines.append("            BBW run = x;")
+            for _ in range(steps - 1):
+                lines.append("            x = " + self.nb(OPPOSITE[d], "x") + " & tgt;")
+                lines.append("            run = run | x;")
+            check = ""
+            if node.length != "any":
+                check = f" && lx::popc(run) == {node.length}"
+            lines.append("            const bool ok = lx::any(" + self.nb(OPPOSITE[d], "run")
+                         + f" & flank){check};")
+            lines.append("            out = lx::sel(ok, out, out | run);")
+            lines.append("        }")
+        body = "\n".join(lines)
+        code = f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
+        const int side = {side};
+        const BBW flank = side ? s.own1 : s.own0;
+        const BBW tgt = side ? s.own0 : s.own1;
+        BBW out = lx::bb_zero<W>();
+        if (!(s.last_dest >= 0 && s.last_mover == side)) return out;
+        const BBW a = lx::onehot<W>(s.last_dest);
+{body}
+        return out;
+    }}"""
+        self.em.helper(name, code)
+        return f"{name}(s, mover)"
+
+    def would_custodial(self, node):
+        """Placement-result fast path (reference exprs.py:334-378): cells whose
+        placement would flank a run, computed on the pre-placement board by
+        shift composition: z_k[x] = target on x..x+(k-1)d and flanker at x+kd."""
+        side = self.side(node.mover)
+        name = f"would_{self.em.fresh('w')}"
+        max_len = max(max(self.board.ray_length(d) for d in self.custodial_dirs(node)), 1)
+        lines = []
+        for d in self.custodial_dirs(node):
+            lines.append("        {")
+            lines.append("            BBW z = tgt & " + self.nb(d, "flank") + ";")
+            if node.length == "any":
+                lines.append("            BBW acc = z;")
+                for _ in range(max_len - 2):
+                    lines.append("            z = tgt & " + self.nb(d, "z") + ";")
+                    lines.append("            acc = acc | z;")
+            else:
+                for _ in range(node.length - 1):
+                    lines.append("            z = tgt & " + self.nb(d, "z") + ";")
+                lines.append("            const BBW acc = z;")
+            lines.append("            out = out | " + self.nb(d, "acc") + ";")
+            lines.append("        }")
+        body = "\n".join(lines)
+        code = f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
+        const int side = {side};
+        const BBW flank = side ? s.own1 : s.own0;
+        const BBW tgt = side ? s.own0 : s.own1;
+        BBW out = lx::bb_zero<W>();
+{body}
+        return out;
+    }}"""
+        self.em.helper(name, code)
+        return f"{name}(s, mover)"
+
+    # -- lines ------------------------------------------------------------
+
+    def line_runs(self, node, stones):
+        """Per-axis window-start bitmaps of ``length`` consecutive stones."""
+        if node.exact or node.exclude is not None:
+            _fail("exact / exclude lines are not lowered yet")
+        L = node.length
+        axes = self.board.orientation_dirs(node.orientation)
+        name = f"lines_{self.em.fresh('l')}"
+        lines = []
+        for ai, d in enumerate(axes):
+            # doubling: r(a+b) = r(a) & walk_a(r(b)); windows run along d
+            have = {1: "b"}
+            code = []
+            k = 1
+            while k * 2 <= L:
+                nm = f"r{ai}_{2 * k}"
+                code.append(f"        const BBW {nm} = {have[k]} & {self.walk(d, k, have[k])};")
+                have[2 * k] = nm
+                k *= 2
+            cur_len, cur = k, have[k]
+            rest = L - k
+            while rest > 0:
+                p = 1
+                while p * 2 <= rest:
+                    p *= 2
+                nm = f"r{ai}_{cur_len + p}"
+                code.append(f"        const BBW {nm} = {cur} & {self.walk(d, cur_len, have[p])};")
+                cur, cur_len, rest = nm, cur_len + p, rest - p
+            code.append(f"        z[{ai}] = {cur};")
+            lines += code
+        body = "\n".join(lines)
+        code = f"""    static __device__ __forceinline__ void {name}(const BBW& b, BBW (&z)[{len(axes)}]) {{
+{body}
+    }}"""
+        self.em.helper(name, code)
+        return name, len(axes)
+
+    def line_exists(self, node):
+        stones = self.stones(self.side(node.player))
+        name, nax = self.line_runs(node, stones)
+        fn = f"{name}_any"
+        self.em.helper(fn, f"""    static __device__ __forceinline__ bool {fn}(const BBW& b) {{
+        BBW z[{nax}];
+        {name}(b, z);
+        BBW o = z[0];
+#pragma unroll
+        for (int i = 1; i < {nax}; i++) o = o | z[i];
+        return lx::any(o);
+    }}""")
+        return f"{fn}({stones})"
+
+    def line_count(self, node):
+        stones = self.stones(self.side(node.player))
+        name, nax = self.line_runs(node, stones)
+        fn = f"{name}_count"
+        self.em.helper(fn, f"""    static __device__ __forceinline__ int {fn}(const BBW& b) {{
+        BBW z[{nax}];
+        {name}(b, z);
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < {nax}; i++) c += lx::popc(z[i]);
+        return c;
+    }}""")
+        return f"{fn}({stones})"
+
+    def line_anchored_exists(self, node):
+        """Exact anchored form: a satisfied window through last_dest
+        (reference exprs.py:484-535) <=> the run of the mover's stones through
+        the anchor along some axis has >= length cells."""
+        stones = self.stones(self.side(node.player))
+        L = node.length
+        name = f"line_anchor_{self.em.fresh('a')}"
+        lines = []
+        for d in self.board.orientation_dirs(node.orientation):
+            lines.append("        {")
+            lines.append("            BBW e = a;")
+            for _ in range(L - 1):
+                lines.append(f"            e = (e | {self.nb(d, 'e')} | {self.nb(OPPOSITE[d], 'e')}) & b;")
+            lines.append(f"            hit = hit || lx::popc(e | a) >= {L};")
+            lines.append("        }")
+        body = "\n".join(lines)
+        self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const St& s, int mover, const BBW& b) {{
+        if (!(s.last_dest >= 0 && s.last_mover == mover)) return false;
+        const BBW a = lx::onehot<W>(s.last_dest);
+        if (!lx::any(a & b)) return false;
+        bool hit = false;
+{body}
+        return hit;
+    }}""")
+        return f"{name}(s, mover, {stones})"
+
+    # -- connectivity ------------------------------------------------------
+
+    def connected(self, node):
+        """Some component of the side's stones touches every target mask
+        (reference exprs.py:629-652, labels from connectivity.py)."""
+        plan = self.conn_plans[self._conn_plan(node)]
+        if isinstance(node.masks, n.MultiMask):
+            targets = self.board.multi_mask(node.masks.kind)
+        else:
+            targets = [self.static_mask(m) for m in node.masks]
+            if any(t is None for t in targets):
+                _fail("connected targets must be static masks")
+        if len(targets) != 2:
+            _fail("connected with other than two targets is not lowered yet")
+        stones = self.stones(self.side(node.mover))
+        dil = " | ".join(self.nb(d, "f") for d in plan)
+        name = f"connected_{self.em.fresh('k')}"
+        t0, t1 = self.em.const(targets[0]), self.em.const(targets[1])
+        self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const BBW& mine) {{
+        // flood the stones reachable from target 0, then test target 1
+        BBW f = mine & {t0};
+        if (!lx::any(f) || !lx::any(mine & {t1})) return false;
+        while (true) {{
+            BBW g = (f | {dil}) & mine;
+            g = (g | {dil.replace('(f)', '(g)')}) & mine;
+            if (lx::equal(g, f)) break;
+            f = g;
+        }}
+        return lx::any(f & {t1});
+    }}""")
+        return f"{name}({stones})"
+
+    # -- functions / predicates -------------------------------------------
+
+    def function(self, node):
+        t = type(node)
+        if t is n.ConstantFn:
+            return str(int(node.value))
+        if t is n.CountFn:
+            return f"lx::popc({self.mask(node.mask)})"
+        if t is n.ScoreFn:
+            sd = self.side(node.who)
+            return f"(({sd}) ? s.sc1 : s.sc0)"
+        if t in (n.AddFn, n.MultiplyFn):
+            op = " + " if t is n.AddFn else " * "
+            return "(" + op.join(self.function(i) for i in node.items) + ")"
+        if t is n.SubtractFn:
+            return f"({self.function(node.a)} - {self.function(node.b)})"
+        if t is n.LineFn:
+            return self.line_count(node)
+        if t is n.ConnectedFn:
+            return f"(int){self.connected(node)}"
+        _fail(f"function {t.__name__} is not lowered yet")
+
+    def predicate(self, node, end_rule=False):
+        t = type(node)
+        if t in (n.PredAnd, n.PredOr):
+            op = " && " if t is n.PredAnd else " || "
+            return "(" + op.join(self.predicate(i, end_rule) for i in node.items) + ")"
+        if t is n.PredNot:
+            return f"(!{self.predicate(node.item, end_rule)})"
+        if t is n.FunctionPred:
+            if isinstance(node.fn, n.LineFn):
+                return self.line_predicate(node.fn, end_rule)
+            if isinstance(node.fn, n.ConnectedFn):
+                return self.connected(node.fn)
+            return f"({self.function(node.fn)} >= 1)"
+        if t is n.ExistsPred:
+            return f"lx::any({self.mask(node.mask)})"
+        if t is n.FullBoardPred:
+            return f"lx::equal(s.own0 | s.own1, {self.em.const(self.valid)})"
+        if t is n.MoverIsPred:
+            return f"(mover == {int(node.player)})"
+        if t is n.EqualsPred:
+            first = self.function(node.items[0])
+            return "(" + " && ".join(f"({first} == {self.function(i)})"
+                                     for i in node.items[1:]) + ")"
+        if t in (n.GreaterEqPred, n.LessEqPred):
+            op = ">=" if t is n.GreaterEqPred else "<="
+            return f"({self.function(node.a)} {op} {self.function(node.b)})"
+        if t is n.PassedPred:
+            if node.who == n.BOTH:
+                return "(s.pass_streak >= 2)"
+            sd = self.side(node.who)
+            return f"((({sd}) ? s.pf1 : s.pf0) != 0)"
+        _fail(f"predicate {t.__name__} is not lowered yet")
+
+    def line_predicate(self, line, end_rule):
+        """Global vs anchored line test, mirroring the reference's choice
+        (compiler.py:122-135, 271-281; exprs.py:799-804).
+
+        Where the reference anchors the test at last_dest, the global test is
+        used when it is provably identical on every reachable state: the rule
+        is a top-level `(if (line ...) <result>)`, stones are only added by
+        the mover's own placements (no flips/promotion/movement; placement
+        owner is the mover) and the start position holds no line -- then no
+        non-terminal state ever contains a line, so any line after a move
+        passes through the placed stone.  Otherwise the exact anchored form
+        is emitted."""
+        if end_rule and id(line) in self._anchored_lines:
+            if id(line) in self._global_ok:
+                return self.line_exists(line)
+            return self.line_anchored_exists(line)
+        return self.line_exists(line)
+
+    # ------------------------------------------------------------ rules
+
+    def _decide_anchoring(self):
+        self._anchored_lines = set()
+        self._global_ok = set()
+        start_has_line = self._start_boards()
+        owners_mover = all(isinstance(p.mechanic, n.PlaceMechanic)
+                           and p.mechanic.owner == n.MOVER for p in self.spec.phases)
+        for line in self._anchor_candidates:
+            own0, own1 = start_has_line
+            if self._np_line(own0, line) or self._np_line(own1, line):
+                continue      # reference keeps the global form (compiler.py:272-277)
+            self.anchor_lines.add(line)
+        if self._anchor_candidates and not self.anchor_lines and not self._last_action_base:
+            self.layout["last_action"] = False
+        for rule in self.spec.end_rules:
+            for x in n.walk(rule.condition):
+                if isinstance(x, n.FunctionPred) and isinstance(x.fn, n.LineFn) \
+                        and x.fn in self.anchor_lines:
+                    self._anchored_lines.add(id(x.fn))
+                    top = rule.condition is x
+                    if top and owners_mover and not self.has_flip:
+                        self._global_ok.add(id(x.fn))
+
+    def _np_line(self, owner_cells, line):
+        for _, cells in self.board.line_windows(line.length, line.orientation):
+            if all(owner_cells[c] for c in cells):
+                return True
+        return False
+
+    def _start_boards(self):
+        own = [np.zeros(self.C, dtype=bool), np.zeros(self.C, dtype=bool)]
+        for sp in self.spec.start:
+            cells = list(sp.cells) if sp.cells else \
+                np.nonzero(self._static_union(sp.masks))[0].tolist()
+            own[sp.player][cells] = True
+        return own
+
+    def lower(self):
+        self._decide_anchoring()
+        spec = self.spec
+        phases = spec.phases
+        em = self.em
+        # start position
+        own = self._start_boards()
+        start_scores = [0, 0]
+        for sp in spec.start:
+            cells = list(sp.cells) if sp.cells else \
+                np.nonzero(self._static_union(sp.masks))[0].tolist()
+            start_scores[sp.player] += len(cells)
+        start_code = [f"        s.own0 = {em.const(own[0])};", f"        s.own1 = {em.const(own[1])};"]
+        if self.layout["scores"]:
+            start_code.append(f"        s.sc0 = {start_scores[0]}; s.sc1 = {start_scores[1]};")
+
+        # per-phase legality, write, effects
+        legal_cases, fp_cases, eff_cases = [], [], []
+        for pi, ph in enumerate(phases):
+            mech = ph.mechanic
+            dest = self.mask(mech.destination)
+            legal = f"lx::andnot({em.const(self.valid)}, s.own0 | s.own1) & {dest}"
+            if mech.result is not None:
+                r = mech.result
+                if (isinstance(r, n.ExistsPred) and isinstance(r.mask, n.CustodialMask)
+                        and r.mask.mover == mech.owner):
+                    legal += f" & {self.would_custodial(r.mask)}"
+                else:
+                    _fail("placement result predicates other than (exists (custodial ...)) "
+                          "by the placing side are not lowered yet")
+            legal_cases.append(f"            case {pi}: return {legal};")
+            if ph.force_pass:
+                fp_cases.append(pi)
+            if mech.effects:
+                eff_cases.append(f"            case {pi}: {{\n{self.effects(mech.effects, mech)}\n"
+                                 f"                break;\n            }}")
+        owner_side = {pi: self.side(ph.mechanic.owner) for pi, ph in enumerate(phases)}
+        if len(set(owner_side.values())) != 1:
+            _fail("per-phase placement owners differ")
+        owner = owner_side[0]
+
+        # end rules
+        end_lines = []
+        for rule in spec.end_rules:
+            cond = self.predicate(rule.condition, end_rule=True)
+            end_lines.append(f"        if ({cond}) return {self.result(rule.result)};")
+
+        # advancement tables (reference compiler.py:251-267, 528-539)
+        nph = len(phases)
+        adv = []
+        for pi, ph in enumerate(phases):
+            order = list(ph.order)
+            for pl in (0, 1):
+                pos = order.index(pl) if pl in order else 0
+                nxt = pos + 1
+                wrap = nxt >= len(order)
+                nphase = pi + 1 if (wrap and ph.kind == "once_through") else pi
+                npos = 0 if wrap else nxt
+                nplayer = phases[nphase].order[npos] if nphase < nph else 0
+                adv.append(f"        if (phase == {pi} && mover == {pl}) {{ np = {nplayer}; "
+                           f"nphase = {nphase}; return; }}")
+        conn = ""
+        if self.conn_plans:
+            plan = self.conn_plans[0]
+            dil = " | ".join(self.nb(d, "f") for d in plan)
+            conn = f"""        const BBW occ[2] = {{s.own0, s.own1}};
+        BBW done = lx::bb_zero<W>();
+        for (int c = 0; c < C; c++) {{
+            const bool o0 = lx::test(s.own0, c), o1 = lx::test(s.own1, c);
+            if (!o0 && !o1) {{ out[c] = -1; continue; }}
+            if (lx::test(done, c)) continue;
+            const BBW mine = o0 ? occ[0] : occ[1];
+            BBW f = lx::onehot<W>(c);
+            while (true) {{
+                const BBW g = (f | {dil}) & mine;
+                if (lx::equal(g, f)) break;
+                f = g;
+            }}
+            done = done | f;
+#pragma unroll
+            for (int i = 0; i < W; i++) {{
+                u32 bits = f.w[i];
+                while (bits) {{ const int b = __ffs(bits) - 1; out[32 * i + b] = (short)c; bits &= bits - 1u; }}
+            }}
+        }}"""
+        fp = " || ".join(f"phase == {p}" for p in fp_cases) or "false"
+        L = self.layout
+        src = f"""// generated by paper_2506_22609_b200.lowering for game "{spec.name}"
+#include "lx_core.cuh"
+
+struct Game {{
+    static constexpr int C = {self.C}, W = {self.W}, NX = 0, A = {self.A}, PASS = {self.PASS};
+    static constexpr int FIRST_PLAYER = {phases[0].order[0]}, NPHASE = {nph};
+    static constexpr bool L_SCORES = {str(L['scores']).lower()}, L_PASSING = {str(L['passing']).lower()};
+    static constexpr bool L_LAST = {str(L['last_action']).lower()}, L_PHASE = {str(L['phase']).lower()};
+    typedef lx::BB<W> BBW;
+    typedef lx::State<W, NX> St;
+@@CONSTS@@
+@@HELPERS@@
+    static __device__ __forceinline__ void start(St& s) {{
+{chr(10).join(start_code)}
+    }}
+    static __device__ __forceinline__ BBW legal(const St& s) {{
+        const int mover = s.cur;
+        const BBW me = mover ? s.own1 : s.own0;
+        const BBW op = mover ? s.own0 : s.own1;
+        (void)me; (void)op;
+        switch (s.phase) {{
+{chr(10).join(legal_cases)}
+            default: return lx::bb_zero<W>();
+        }}
+    }}
+    static __device__ __forceinline__ bool force_pass(int phase) {{ return {fp}; }}
+    static __device__ __forceinline__ void write_place(St& s, int cell, int mover, int phase) {{
+        const int side = {owner};
+        if (side) lx::setbit(s.own1, cell); else lx::setbit(s.own0, cell);
+        s.last_kind = 0; s.last_dest = cell; s.last_mover = side;
+        if (side) s.ldbp1 = cell; else s.ldbp0 = cell;
+    }}
+    static __device__ __forceinline__ void effects(St& s, int cell, int mover, int phase) {{
+        switch (phase) {{
+{chr(10).join(eff_cases)}
+            default: break;
+        }}
+    }}
+    static __device__ __forceinline__ void advance(int phase, int mover, int& np, int& nphase) {{
+{chr(10).join(adv)}
+        np = 0; nphase = phase;
+    }}
+    static __device__ __forceinline__ int end_rules(const St& s, int mover) {{
+        const BBW me = mover ? s.own1 : s.own0;
+        const BBW op = mover ? s.own0 : s.own1;
+        (void)me; (void)op;
+{chr(10).join(end_lines)}
+        return -1;
+    }}
+    static __device__ __forceinline__ void labels(const St& s, short* out) {{
+{conn}
+    }}
+    static __device__ __forceinline__ void rebuild_ext(St& s) {{}}
+}};
+
+#include "lx_kernels.cuh"
+"""
+        src = src.replace("@@CONSTS@@", em.const_defs())
+        src = src.replace("@@HELPERS@@", "\n".join(em.helpers.values()))
+        info = {"name": spec.name, "C": self.C, "A": self.A, "W": self.W, "NX": 0,
+                "pass_index": self.PASS, "layout": dict(self.layout),
+                "nwords": 2 * self.W + 7, "nq": (2 * self.W + 7 + 3) // 4,
+                "first_player": int(phases[0].order[0]), "nphase": nph,
+                "observation_planes": 3}
+        return Lowered(name=spec.name, source=src, info=info)
+
+    def effects(self, effs, mech):
+        """Ordered effect list (reference effects.py:17-133)."""
+        out = []
+        for e in effs:
+            out.append(self.effect(e))
+        return "\n".join(out)
+
+    def effect(self, e):
+        t = type(e)
+        ind = "                "
+        if t is n.FlipEffect:
+            m = self.mask(e.mask)
+            sd = self.side(e.mover)
+            return (f"{ind}{{ const BBW cells = {m} & (s.own0 | s.own1); const int fs = {sd};\n"
+                    f"{ind}  if (fs) {{ s.own1 = s.own1 | cells; s.own0 = lx::andnot(s.own0, cells); }}\n"
+                    f"{ind}  else {{ s.own0 = s.own0 | cells; s.own1 = lx::andnot(s.own1, cells); }} }}")
+        if t is n.CaptureEffect:
+            m = self.mask(e.mask)
+            inc = ""
+            if e.increment_score:
+                inc = (f"\n{ind}  {{ const int g = lx::popc(cells); "
+                       f"if (mover) s.sc1 += g; else s.sc0 += g; }}")
+            return (f"{ind}{{ const BBW cells = {m} & (s.own0 | s.own1);\n"
+                    f"{ind}  s.own0 = lx::andnot(s.own0, cells); s.own1 = lx::andnot(s.own1, cells);{inc} }}")
+        if t in (n.SetScoreEffect, n.IncrementScoreEffect):
+            sd = self.side(e.who)
+            fn = self.function(e.fn)
+            op = "=" if t is n.SetScoreEffect else "+="
+            return (f"{ind}{{ const BBW me = mover ? s.own1 : s.own0; const BBW op = mover ? s.own0 : s.own1;\n"
+                    f"{ind}  (void)me; (void)op; const int v = {fn};\n"
+                    f"{ind}  if ({sd}) s.sc1 {op} v; else s.sc0 {op} v; }}")
+        if t is n.ConditionalEffect:
+            cond = self.predicate(e.condition)
+            then = self.effect(e.then_effect)
+            other = self.effect(e.else_effect) if e.else_effect is not None else ""
+            return (f"{ind}{{ const BBW me = mover ? s.own1 : s.own0; const BBW op = mover ? s.own0 : s.own1;\n"
+                    f"{ind}  (void)me; (void)op;\n"
+                    f"{ind}  if ({cond}) {{\n{then}\n{ind}  }} else {{\n{other}\n{ind}  }} }}")
+        _fail(f"effect {t.__name__} is not lowered yet")
+
+    def result(self, res):
+        """(reference compiler.py:582-597)"""
+        if res.kind == "draw":
+            return "0"
+        if res.kind == "by_score":
+            return "(s.sc0 > s.sc1 ? 1 : (s.sc1 > s.sc0 ? 2 : 0))"
+        if res.who == n.BOTH:
+            return "0"
+        sd = self.side(res.who)
+        if res.kind == "lose":
+            return f"(1 + (1 - ({sd})))"
+        return f"(1 + ({sd}))"
+
+
+def lower_game(spec):
+    try:
+        return GameLowering(spec).lower()
+    except (KeyError, UnsupportedConstruct) as exc:
+        raise CompileError("lower", str(exc)) from exc

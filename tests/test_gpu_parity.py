@@ -1,0 +1,225 @@
+"""Device path vs the CPU oracle and the reference's golden fixtures.
+
+Bit-exact comparisons on the reference GameState layout (digest = the
+reference's own blake2b over every field).  All tests call through the
+C-ABI (libludax_b200.so) via the package API.
+"""
+import numpy as np
+import pytest
+
+from conftest import GAMES, golden_arrays, golden_state
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2506_22609_b200 as lx  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+_GAMES = {}
+
+
+def game(name):
+    if name not in _GAMES:
+        _GAMES[name] = lx.load_config_game(name)
+    return _GAMES[name]
+
+
+ORACLE_B = {"tic_tac_toe": 65536, "connect_four": 16384, "hex": 2048, "reversi": 4096,
+            "pente": 512}
+
+
+@pytest.mark.parametrize("name", GAMES)
+def test_playout_matches_reference_fixtures(name, golden_meta):
+    g = game(name)
+    for k, p in enumerate(golden_meta["games"][name]["playouts"]):
+        final = lx.engine.playout_random(g, seed=p["seed"], batch_size=p["batch"]).final
+        want = golden_state(name, k)
+        host = final.host()
+        for f, v in want.items():
+            assert np.array_equal(host[f], v), (name, k, f)
+        assert final.digest() == p["digest"]
+
+
+@pytest.mark.parametrize("name", GAMES)
+def test_playout_matches_oracle_large(name):
+    B = ORACLE_B[name]
+    final = lx.engine.playout_random(game(name), seed=2024, batch_size=B).final
+    want, _ = O.OracleGame(name).playout(B, seed=2024, threads=8)
+    host = final.host()
+    for f, v in want.items():
+        assert np.array_equal(host[f], v), (name, f)
+
+
+@pytest.mark.parametrize("name", GAMES)
+def test_trajectory_masks_actions_digests(name, golden_meta):
+    g = game(name)
+    info = golden_meta["games"][name]
+    arr = golden_arrays(name)
+    width = info["traj_mask_width"]
+    masks = np.unpackbits(arr["traj_masks"], axis=-1)[..., :width].astype(bool)
+    st = g.init(batch_size=4, seed=3)
+    for t in range(len(arr["traj_actions"])):
+        assert np.array_equal(g.legal_mask(st), masks[t]), (name, t)
+        a = lx.engine.random_actions(g, st)
+        assert np.array_equal(a, arr["traj_actions"][t]), (name, t)
+        g.step_into(st, a, rows=~st.terminated, verify=False)
+        assert st.digest() == info["traj_digests"][t], (name, t)
+
+
+@pytest.mark.parametrize("name", GAMES)
+def test_replay_oracle_actions_stepwise(name):
+    """Recorded-trajectory replay: step both sides with the same actions and
+    compare every field after every ply, plus legal masks and counts."""
+    g, og = game(name), O.OracleGame(name)
+    B = 257
+    st = g.init(batch_size=B, seed=99)
+    ost = og.init(B, seed=99)
+    for ply in range(210):
+        m, cnt = og.legal_mask(ost)
+        assert np.array_equal(g.legal_mask(st), m), (name, ply)
+        assert np.array_equal(g.legal_counts(st), cnt), (name, ply)
+        if ost["terminated"].all():
+            break
+        a = og.sample_actions(ost)
+        live = ~ost["terminated"]
+        og.step_into(ost, a, rows=live, verify=False)
+        g.step_into(st, a, rows=live, verify=False)
+        assert st.digest() == O.digest(ost), (name, ply)
+
+
+@pytest.mark.parametrize("name", GAMES)
+def test_export_import_roundtrip(name):
+    og = O.OracleGame(name)
+    ost = og.init(300, seed=5)
+    for _ in range(9):
+        a = og.sample_actions(ost)
+        og.step_into(ost, a, rows=~ost["terminated"], verify=False)
+    st = game(name).from_reference(ost)
+    assert st.digest() == O.digest(ost)
+    # and it keeps playing identically from the imported position
+    lx.engine.playout_random(game(name), state=st)  # pure: st unchanged
+    fin = lx.engine.playout_random(game(name), state=st).final
+    want, _ = og.playout(state=ost)
+    assert fin.digest() == O.digest(want)
+
+
+def test_sample_with_host_uniforms():
+    g, og = game("reversi"), O.OracleGame("reversi")
+    st, ost = g.init(512, seed=1), og.init(512, seed=1)
+    u = np.random.default_rng(0).random(512)
+    assert np.array_equal(g.sample_actions(st, u), og.sample_actions(ost, u))
+
+
+def test_known_answers(golden_meta):
+    kat = golden_meta["kat"]
+    ttt = game("tic_tac_toe")
+    s = ttt.init(1)
+    for a in kat["ttt_diag"]["actions"]:
+        s = lx.engine.step(ttt, s, a)
+    assert s.digest() == kat["ttt_diag"]["digest"]
+    assert lx.engine.outcome_view(s) == {"p1": "win", "p2": "lose", "truncated": False}
+    c4 = game("connect_four")
+    assert np.nonzero(lx.engine.legal_actions(c4, c4.init(1))[0])[0].tolist() == \
+        kat["c4_initial_legal"]
+    rv = game("reversi")
+    assert np.nonzero(lx.engine.legal_actions(rv, rv.init(1))[0])[0].tolist() == \
+        kat["reversi_initial_legal"]
+    pe = game("pente")
+    for key in ("pente_capture", "pente_no_capture3"):
+        s = pe.init(1)
+        for a in kat[key]["actions"]:
+            s = pe.step(s, np.array([a]))
+        assert s.board_owner[0].tolist() == kat[key]["owner"]
+        assert s.digest() == kat[key]["digest"]
+
+
+def test_errors_map_to_reference_types():
+    ttt = game("tic_tac_toe")
+    s = lx.engine.step(ttt, ttt.init(1), 4)
+    with pytest.raises(lx.IllegalAction):
+        lx.engine.step(ttt, s, 4)
+    for a in (0, 1, 2, 8):
+        s = lx.engine.step(ttt, s, a) if not s.terminated[0] else s
+    s = ttt.init(1)
+    for a in [0, 1, 4, 2, 8]:
+        s = lx.engine.step(ttt, s, a)
+    with pytest.raises(lx.TerminalState):
+        lx.engine.step(ttt, s, 3)
+    with pytest.raises(lx.TerminalState):
+        lx.engine.legal_actions(ttt, s)
+    rv = game("reversi")
+    with pytest.raises(lx.IllegalAction):       # pass is illegal while moves exist
+        rv.step(rv.init(1), np.array([64]))
+
+
+def test_step_is_pure():
+    g = game("connect_four")
+    s = g.init(2, seed=1)
+    d0 = s.digest()
+    s1 = g.step(s, np.array([35, 41]))
+    s2 = g.step(s, np.array([35, 41]))
+    assert s1.digest() == s2.digest() and s.digest() == d0
+
+
+def test_batch_equals_sequential_and_partition():
+    for name in GAMES:
+        g = game(name)
+        seeds = lx.rng.spawn_seeds(1234, 8)
+        whole = lx.engine.playout_random(g, state=g.init(8, seeds=seeds)).final
+        singles = [lx.engine.playout_random(g, state=g.init(1, seeds=seeds[i:i + 1])).final
+                   for i in range(8)]
+        assert whole.digest() == lx.DeviceState.concat(singles).digest(), name
+        # shard by first_index: two halves == one batch (multi-GPU partition)
+        left, _ = g.rollout(batch_size=512, seed=77)
+        right, _ = g.rollout(batch_size=512, seed=77, first_index=512)
+        full, _ = g.rollout(batch_size=1024, seed=77)
+        assert lx.DeviceState.concat([left, right]).digest() == full.digest(), name
+
+
+def test_record_mode_matches_fused(golden_meta):
+    for name in GAMES:
+        g = game(name)
+        a = lx.engine.playout_random(g, seed=3, batch_size=16, record=True)
+        b = lx.engine.playout_random(g, seed=3, batch_size=16)
+        assert a.final.digest() == b.final.digest(), name
+        rows = a.trajectory(0)
+        assert rows[0]["move_count"] == 0 and rows[-1]["terminated"]
+
+
+def test_truncation_marks_draw():
+    g = game("pente")
+    f = lx.engine.playout_random(g, seed=5, batch_size=64, max_turns=40).final
+    tr = f.truncated
+    assert tr.any() and (f.outcome[tr] == 0).all() and (f.move_count[tr] == 40).all()
+    want, _ = O.OracleGame("pente").playout(64, seed=5, max_turns=40)
+    assert f.digest() == O.digest(want)
+
+
+def test_hex_no_draws_10000():
+    f = lx.engine.playout_random(game("hex"), seed=404, batch_size=10_000).final
+    assert f.terminated.all() and not f.truncated.any() and (f.outcome != 0).all()
+
+
+def test_reversi_integrity_1000():
+    f = lx.engine.playout_random(game("reversi"), seed=777, batch_size=1000).final
+    p1 = (f.board_owner == 0).sum(axis=1)
+    p2 = (f.board_owner == 1).sum(axis=1)
+    assert (f.scores.sum(axis=1) == p1 + p2).all()
+    assert (f.outcome == np.where(p1 > p2, 1, np.where(p2 > p1, 2, 0))).all()
+
+
+def test_c4_opening_distribution(golden_meta):
+    g = game("connect_four")
+    st = g.init(batch_size=100_000, seed=77)
+    a = lx.engine.random_actions(g, st)
+    vals, cnt = np.unique(a, return_counts=True)
+    assert dict(zip(map(str, vals.tolist()), cnt.tolist())) == golden_meta["kat"]["c4_opening_counts"]
+
+
+def test_ttt_outcome_counts(golden_meta):
+    want = golden_meta["kat"]["ttt_10000_seed11"]
+    f = lx.engine.playout_random(game("tic_tac_toe"), seed=11, batch_size=10_000).final
+    assert f.digest() == want["digest"]
