@@ -305,38 +305,79 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
 // stats (u64[8], zeroed by the caller): steps, p1 wins, p2 wins, draws,
 // truncated, envs finished.  *counter must be zero.  *stuck = min row that
 // had no legal action (init ~0).
-extern "C" __global__ void __launch_bounds__(256) lx_rollout(u32* st, i64 B, int max_turns,
+extern "C" __global__ void __launch_bounds__(256, 2) lx_rollout(u32* st, i64 B, int max_turns,
                                                              int mode, u64 seed_base,
                                                              const u64* seeds, i64 first,
                                                              u64* stats, u64* counter,
                                                              u64* stuck, signed char* outcomes,
                                                              int* turns) {
+    constexpr unsigned FULL = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31u;
+    const unsigned lanes_below = (1u << lane) - 1u;
+    const u64 base_mix = lx::seed_mix(seed_base);
     u64 n_steps = 0, n_p1 = 0, n_p2 = 0, n_draw = 0, n_trunc = 0, n_done = 0;
+    // Env indices are handed out in warp-private chunks of 32.  The next
+    // chunk is claimed one chunk ahead, so the atomic's latency is hidden
+    // behind ~32 games; each lane precomputes the seed (and its first mix)
+    // of env cur+lane at full warp width, and a lane starting a new game
+    // fetches its seed with a shuffle.
+    auto prep = [&](u64 base, u64& ps, u64& pm) {
+        const i64 j = (i64)(base + lane);
+        ps = 0;
+        pm = 0;
+        if ((mode & 1) && j < B) {
+            ps = seeds ? seeds[j] : lx::mix64(base_mix ^ (u64)(first + j));
+            pm = lx::seed_mix(ps);
+        }
+    };
+    u64 cur = 0, nxt = 0;
+    if (lane == 0) {
+        cur = atomicAdd(counter, 32ull);
+        nxt = atomicAdd(counter, 32ull);
+    }
+    cur = __shfl_sync(FULL, cur, 0);
+    int used = 0;
+    u64 pre_seed, pre_mix;
+    prep(cur, pre_seed, pre_mix);
     Game::St s;
     u64 smix = 0;
     i64 idx = -1;
     bool need = true, active = true;
     while (true) {
-        const unsigned want = __ballot_sync(0xffffffffu, need && active);
-        if (want) {
-            u64 base = 0;
-            const unsigned leader = __ffs(want) - 1;
-            if (lane == leader) base = atomicAdd(counter, (u64)__popc(want));
-            base = __shfl_sync(0xffffffffu, base, leader);
+        const unsigned want = __ballot_sync(FULL, need && active);
+        if (want) {                                     // warp-uniform
+            const int n = __popc(want);
+            const int pos = used + __popc(want & lanes_below);
+            u64 sd = __shfl_sync(FULL, pre_seed, pos & 31);
+            u64 sm = __shfl_sync(FULL, pre_mix, pos & 31);
+            u64 my_base = cur;
+            if (used + n > 32) {                        // switch to the prefetched chunk
+                const u64 nb = __shfl_sync(FULL, nxt, 0);
+                u64 ps2, pm2;
+                prep(nb, ps2, pm2);
+                const u64 sd2 = __shfl_sync(FULL, ps2, pos & 31);
+                const u64 sm2 = __shfl_sync(FULL, pm2, pos & 31);
+                if (pos >= 32) { sd = sd2; sm = sm2; my_base = nb; }
+                cur = nb;
+                used = used + n - 32;
+                pre_seed = ps2;
+                pre_mix = pm2;
+                if (lane == 0) nxt = atomicAdd(counter, 32ull);
+            } else {
+                used += n;
+            }
             if (need && active) {
-                idx = (i64)(base + __popc(want & ((1u << lane) - 1u)));
+                idx = (i64)(my_base + (u64)(pos & 31));
                 if (idx >= B) {
                     active = false;
                 } else {
                     if (mode & 1) {
-                        const u64 seed = seeds ? seeds[idx]
-                                               : lx::mix64(lx::seed_mix(seed_base) ^ (u64)(first + idx));
-                        lx::init_state<Game>(s, seed);
+                        lx::init_state<Game>(s, sd);
+                        smix = sm;
                     } else {
                         lx::load_state<Game>(s, st, B, idx);
+                        smix = lx::seed_mix(s.seed);
                     }
-                    smix = lx::seed_mix(s.seed);
                     need = false;
                 }
             }

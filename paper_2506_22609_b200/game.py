@@ -478,13 +478,18 @@ def load_config_game(name):
         return load_game(f.read())
 
 
-def precompile(names=("tic_tac_toe", "connect_four", "hex", "reversi", "pente")):
+def precompile(names=("tic_tac_toe", "connect_four", "hex", "reversi", "pente"), prune=True):
     """NVRTC-compile the config games' cubins into the in-tree cache (no GPU)."""
     keys = {}
     for name in names:
         with open(os.path.join(GAMES_DIR, f"{name}.ldx")) as f:
             low = lower_game(parse_game(f.read()))
         keys[name] = native.compile_only(low.source, low.name)
+    if prune:
+        live = {f"{k}.cubin" for k in keys.values()}
+        for fn in os.listdir(native.CACHE_DIR):
+            if fn.endswith(".cubin") and fn not in live:
+                os.remove(os.path.join(native.CACHE_DIR, fn))
     return keys
 
 

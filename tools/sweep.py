@@ -1,0 +1,55 @@
+"""Batch-size sweep of the fused rollout for every config game (1 GPU).
+
+    python tools/sweep.py [--games a,b] [--min-log2 10] [--max-log2 22]
+
+Each point: 3 warm-up episodes, then episodes (seed hash_key(0, B, 10000+e))
+timed with CUDA events until >= 0.25 s; prints one JSON line per point.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2506_22609_b200 as lx  # noqa: E402
+from paper_2506_22609_b200 import rng  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--games", default="tic_tac_toe,connect_four,hex,reversi,pente")
+p.add_argument("--min-log2", type=int, default=10)
+p.add_argument("--max-log2", type=int, default=22)
+p.add_argument("--seconds", type=float, default=0.25)
+a = p.parse_args()
+
+for name in a.games.split(","):
+    g = lx.load_config_game(name)
+    for k in range(a.min_log2, a.max_log2 + 1):
+        B = 1 << k
+        out = g.empty_state(B)
+        stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+        work = torch.zeros(4, dtype=torch.int64, device="cuda")
+        acc = torch.zeros(8, dtype=torch.int64, device="cuda")
+        for e in range(3):
+            g.rollout(seed=rng.episode_seed(0, B, e), out=out, batch_size=B, truncate=False,
+                      check=False, stats=stats, work=work)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n, ms = 0, 0.0
+        while ms < a.seconds * 1000:
+            reps = max(1, n)
+            ev0.record()
+            for e in range(reps):
+                g.rollout(seed=rng.episode_seed(0, B, 10000 + n + e), out=out, batch_size=B,
+                          truncate=False, check=False, stats=stats, work=work)
+                acc.add_(stats)
+            ev1.record()
+            torch.cuda.synchronize()
+            ms += ev0.elapsed_time(ev1)
+            n += reps
+        tot = acc.cpu().tolist()
+        print(json.dumps({"game": name, "batch": B, "episodes": n, "ms_per_episode": ms / n,
+                          "env_steps_per_s": tot[0] / (ms / 1000), "mean_plies": tot[0] / tot[5]}),
+              flush=True)
