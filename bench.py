@@ -181,7 +181,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2506_22609_b200 as lx
-    from paper_2506_22609_b200 import rng
+    from paper_2506_22609_b200 import rng, shard
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -189,7 +189,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     game = lx.load_config_game(args.game)
     B, B_total = args.batch, args.batch * ws
-    first = rank * B
+    first, _ = shard.shard_range(rank, ws, B)
     state = game.empty_state(B)
     stats = torch.zeros(8, dtype=torch.int64, device="cuda")
     work = torch.zeros(4, dtype=torch.int64, device="cuda")
@@ -219,9 +219,9 @@ def main():
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     tot = acc.clone()
+    shard.max_over_ranks(t)
+    shard.reduce_stats(tot)
     if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot)
         dist.barrier()
     ms_max = float(t.item())
     tot = tot.cpu().tolist()

@@ -124,6 +124,17 @@ int lx_rollout(const lx_game *g, void *state, int64_t B, int max_turns, int mode
                const uint64_t *seeds, int64_t first_index, uint64_t *stats, void *work,
                int8_t *outcomes, int32_t *turns, int check, int64_t *stuck_row, void *stream);
 
+/* PGX-style environment step (LudaxEnvironment.step; BASELINE north star),
+   one launch: apply actions (B,) int64 to live rows (NULL = refresh outputs
+   only), rewards (B, 2) float32 for the terminating ply from the outcome
+   (engine.py:79-87), truncate at max_turns (> 0), auto_reset finished rows
+   with seeds hash_key(seed, 0xE9) (engine.py:58-65), then write the next
+   state's legal mask (B, A) uint8, terminated / truncated (B,) uint8 and
+   current player (B,) int32.  Any output may be NULL. */
+int lx_env_step(const lx_game *g, void *state, int64_t B, const int64_t *actions, int max_turns,
+                int auto_reset, uint8_t *mask, float *rewards, uint8_t *terminated,
+                uint8_t *truncated, int32_t *player, void *stream);
+
 /* device state <-> reference GameState arrays (device pointers) */
 int lx_export(const lx_game *g, const void *state, int64_t B, const lx_ref_state *ref,
               void *stream);

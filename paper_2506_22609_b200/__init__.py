@@ -14,6 +14,7 @@ from .errors import (BoardLangError, CompileError, EmptyMask, IllegalAction,  # 
                      ParseError, TerminalState)
 from .game import (B200Game, DeviceState, compile_game, load_config_game,  # noqa: F401
                    load_game, precompile)
+from .env import EnvState, LudaxEnvironment  # noqa: F401
 from .syntax import parse_game  # noqa: F401
 
 __version__ = "0.1.0"

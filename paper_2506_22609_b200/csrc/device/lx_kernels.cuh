@@ -430,6 +430,60 @@ extern "C" __global__ void __launch_bounds__(256, 2) lx_rollout(u32* st, i64 B, 
     }
 }
 
+// PGX-style environment step (env.LudaxEnvironment.step), one launch per ply:
+// apply actions[i] to live rows (actions == null: no move, just refresh the
+// outputs), reward the terminating ply from the outcome (reference
+// engine.py:79-87: P1 win [+1,-1], P2 win [-1,+1], draw [0,0]), truncate at
+// max_turns (> 0), optionally auto-reset finished rows with seed
+// hash_key(seed, 0xE9) (engine.reset_rows, engine.py:58-65), and write the
+// legal mask / flags / player of the resulting state.
+extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, const i64* actions,
+                                                              int max_turns, int auto_reset,
+                                                              unsigned char* mask, float* rewards,
+                                                              unsigned char* terminated,
+                                                              unsigned char* truncated,
+                                                              int* player) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    const bool was = s.term;
+    float r0 = 0.f, r1 = 0.f;
+    if (!was && actions) {
+        lx::apply_step<Game>(s, (int)actions[i]);
+        if (s.term) {
+            r0 = s.outcome == 1 ? 1.f : (s.outcome == 2 ? -1.f : 0.f);
+            r1 = -r0;
+        } else if (max_turns > 0 && (int)s.mc >= max_turns) {
+            s.term = 1; s.trunc = 1; s.outcome = 0;
+        }
+    }
+    if (auto_reset && s.term && actions) {
+        const u64 seed = lx::mix64(lx::seed_mix(s.seed) ^ 0xE9ull);
+        lx::init_state<Game>(s, seed);
+    }
+    if (actions) lx::store_state<Game>(s, st, B, i);
+    if (rewards) { rewards[2 * i] = r0; rewards[2 * i + 1] = r1; }
+    if (terminated) terminated[i] = (unsigned char)s.term;
+    if (truncated) truncated[i] = (unsigned char)s.trunc;
+    if (player) player[i] = s.cur;
+    if (mask) {
+        lx::BB<Game::W> legal = Game::legal(s);
+        if (s.term) legal = lx::bb_zero<Game::W>();
+        const bool pass_only = !s.term && !lx::any(legal) && Game::force_pass(s.phase);
+        unsigned char* row = mask + i * (i64)Game::A;
+#pragma unroll
+        for (int wd = 0; wd < Game::W; wd++) {
+            const u32 v = legal.w[wd];
+            for (int b = 0; b < 32; b++) {
+                const int c = wd * 32 + b;
+                if (c < Game::C) row[c] = (v >> b) & 1u;
+            }
+        }
+        if (Game::PASS >= 0) row[Game::C] = pass_only;
+    }
+}
+
 // device state -> reference GameState SoA (state.py:78-130)
 extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B, LxRefPtrs p) {
     const i64 i = lx::gtid();

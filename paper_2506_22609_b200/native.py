@@ -39,7 +39,8 @@ class RefState(ctypes.Structure):
 
 EXPORTS = ("lx_version", "lx_last_error", "lx_game_create", "lx_compile_only",
            "lx_game_info_get", "lx_game_destroy", "lx_init", "lx_legal", "lx_sample",
-           "lx_step", "lx_random_step", "lx_rollout", "lx_export", "lx_import", "lx_observe")
+           "lx_step", "lx_random_step", "lx_rollout", "lx_export", "lx_import", "lx_observe",
+           "lx_env_step")
 
 
 def build_native():
@@ -76,6 +77,7 @@ def lib():
     L.lx_export.argtypes = [vp, vp, i64, ctypes.POINTER(RefState), vp]
     L.lx_import.argtypes = [vp, vp, i64, ctypes.POINTER(RefState), vp]
     L.lx_observe.argtypes = [vp, vp, i64, i32, vp, vp]
+    L.lx_env_step.argtypes = [vp, vp, i64, vp, i32, i32, vp, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("lx_version", "lx_last_error"):
             getattr(L, name).restype = i32
