@@ -78,6 +78,9 @@ int lx_game_create(const char *source, const char *name, const char *include_dir
    cache key (>= 65 bytes). */
 int lx_compile_only(const char *source, const char *name, const char *include_dir,
                     const char *cache_dir, char *key_out);
+/* Cache key of (source, headers in include_dir, NVRTC options) without
+   compiling (>= 65 bytes). */
+int lx_cache_key(const char *source, const char *include_dir, char *key_out);
 int lx_game_info_get(const lx_game *g, lx_game_info *out);
 int lx_game_destroy(lx_game *g);
 

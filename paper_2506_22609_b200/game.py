@@ -184,8 +184,9 @@ class B200Game:
         return self.native.h
 
     def lowered_key(self):
-        """Content hash of the generated translation unit (profiles are keyed on it)."""
-        return self.lowered.key
+        """NVRTC cache key: generated unit + device headers + options (profiles
+        under profiles/ are keyed on it)."""
+        return native.cache_key(self.lowered.source)
 
     @staticmethod
     def _stream():

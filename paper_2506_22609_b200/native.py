@@ -37,7 +37,7 @@ class RefState(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in REF_FIELDS]
 
 
-EXPORTS = ("lx_version", "lx_last_error", "lx_game_create", "lx_compile_only",
+EXPORTS = ("lx_version", "lx_last_error", "lx_game_create", "lx_compile_only", "lx_cache_key",
            "lx_game_info_get", "lx_game_destroy", "lx_init", "lx_legal", "lx_sample",
            "lx_step", "lx_random_step", "lx_rollout", "lx_export", "lx_import", "lx_observe",
            "lx_env_step")
@@ -66,6 +66,7 @@ def lib():
     L.lx_game_create.argtypes = [cs, cs, cs, cs, ctypes.POINTER(vp)]
     L.lx_compile_only.argtypes = [cs, cs, cs, cs, ctypes.c_char_p]
     L.lx_game_info_get.argtypes = [vp, ctypes.POINTER(GameInfo)]
+    L.lx_cache_key.argtypes = [cs, cs, ctypes.c_char_p]
     L.lx_game_destroy.argtypes = [vp]
     L.lx_init.argtypes = [vp, vp, i64, vp, u64, i64, vp]
     L.lx_legal.argtypes = [vp, vp, i64, vp, vp, vp]
@@ -95,6 +96,12 @@ def compile_only(source, name):
     os.makedirs(CACHE_DIR, exist_ok=True)
     check(lib().lx_compile_only(source.encode(), name.encode(), INCLUDE_DIR.encode(),
                                 CACHE_DIR.encode(), key))
+    return key.value.decode()
+
+
+def cache_key(source):
+    key = ctypes.create_string_buffer(80)
+    check(lib().lx_cache_key(source.encode(), INCLUDE_DIR.encode(), key))
     return key.value.decode()
 
 

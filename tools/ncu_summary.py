@@ -1,0 +1,95 @@
+"""Summarise ncu reports of lx_rollout into profiles/ (run locally, no GPU).
+
+    python tools/ncu_summary.py gpurun_out --tag r1 [--out profiles]
+
+Reads gpurun_out/prof_<game>.ncu-rep (+ plain_<game>.json written by
+tools/ncu_rollout.py for the env-step count of the profiled launch) and
+writes profiles/<tag>_rollout_<game>.json plus profiles/rollout_<Game>.json
+(the file bench.py reads for the per-env-step instruction count).
+"""
+import argparse
+import csv
+import io
+import json
+import os
+import subprocess
+
+METRICS = {
+    "gpu__time_duration.sum": "duration_ns",
+    "smsp__inst_executed.sum": "warp_inst",
+    "smsp__thread_inst_executed.sum": "thread_inst",
+    "sm__inst_executed_pipe_alu.sum": "alu_warp_inst",
+    "sm__inst_executed_pipe_fma.sum": "fma_warp_inst",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pipe_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "achieved_occupancy_pct",
+    "smsp__thread_inst_executed_per_inst_executed.ratio": "active_lanes_per_inst",
+    "launch__registers_per_thread": "registers",
+    "launch__grid_size": "grid",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio": "stall_long_sb",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio": "stall_wait",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio": "stall_math",
+    "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio": "stall_branch",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio": "stall_short_sb",
+}
+UNITS = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "us": 1e3, "ms": 1e6,
+         "ns": 1.0, "Ghz": 1e9, "Mhz": 1e6, "hz": 1.0}
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    head, units, vals = rows[0], rows[1], rows[2]
+    res = {}
+    for k, name in METRICS.items():
+        if k in head:
+            i = head.index(k)
+            v = float(vals[i].replace(",", ""))
+            res[name] = v * UNITS.get(units[i], 1.0)
+    return res
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("src")
+    p.add_argument("--tag", default="r1")
+    p.add_argument("--out", default="profiles")
+    a = p.parse_args()
+    os.makedirs(a.out, exist_ok=True)
+    names = {"tic_tac_toe": "Tic-Tac-Toe", "connect_four": "Connect_Four", "hex": "Hex",
+             "reversi": "Reversi", "pente": "Pente"}
+    for game, gname in names.items():
+        rep = os.path.join(a.src, f"prof_{game}.ncu-rep")
+        plain = os.path.join(a.src, f"plain_{game}.json")
+        if not (os.path.exists(rep) and os.path.exists(plain)):
+            continue
+        with open(plain) as f:
+            info = json.loads(f.read().strip().splitlines()[-1])
+        m = raw(rep)
+        steps = info["env_steps"]
+        s = {"game": game, "batch": info["batch"], "cubin_key": info["cubin_key"],
+             "env_steps_in_launch": steps, **m,
+             "warp_inst_per_env_step": m["warp_inst"] / steps,
+             "thread_inst_per_env_step": m.get("thread_inst", 0) / steps,
+             "alu_warp_inst_per_env_step": m.get("alu_warp_inst", 0) / steps,
+             "dram_bytes_per_launch": m.get("dram_read", 0) + m.get("dram_write", 0),
+             "env_steps_per_s_under_ncu": steps / (m["duration_ns"] / 1e9),
+             "source": f"ncu --set full, {os.path.basename(rep)} (serialised, cold cache)"}
+        with open(os.path.join(a.out, f"{a.tag}_rollout_{game}.json"), "w") as f:
+            json.dump(s, f, indent=1, sort_keys=True)
+        with open(os.path.join(a.out, f"rollout_{gname}.json"), "w") as f:
+            json.dump(s, f, indent=1, sort_keys=True)
+        print(game, f"{s['warp_inst_per_env_step']:.2f} warp-inst/step",
+              f"lanes {m.get('active_lanes_per_inst', 0):.1f}",
+              f"alu {m.get('alu_pipe_pct', 0):.1f}%", f"issue {m.get('issue_active_pct', 0):.1f}%",
+              f"{s['env_steps_per_s_under_ncu'] / 1e9:.1f} G/s")
+
+
+if __name__ == "__main__":
+    main()
