@@ -305,7 +305,13 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
 // stats (u64[8], zeroed by the caller): steps, p1 wins, p2 wins, draws,
 // truncated, envs finished.  *counter must be zero.  *stuck = min row that
 // had no legal action (init ~0).
-extern "C" __global__ void __launch_bounds__(256, 2) lx_rollout(u32* st, i64 B, int max_turns,
+#ifndef LX_ROLLOUT_THREADS
+#define LX_ROLLOUT_THREADS 256
+#endif
+#ifndef LX_ROLLOUT_MINB
+#define LX_ROLLOUT_MINB 2
+#endif
+extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB) lx_rollout(u32* st, i64 B, int max_turns,
                                                              int mode, u64 seed_base,
                                                              const u64* seeds, i64 first,
                                                              u64* stats, u64* counter,
@@ -331,12 +337,10 @@ extern "C" __global__ void __launch_bounds__(256, 2) lx_rollout(u32* st, i64 B, 
         }
     };
     u64 cur = 0, nxt = 0;
-    if (lane == 0) {
-        cur = atomicAdd(counter, 32ull);
-        nxt = atomicAdd(counter, 32ull);
-    }
+    if (lane == 0) cur = atomicAdd(counter, 32ull);
     cur = __shfl_sync(FULL, cur, 0);
     int used = 0;
+    bool requested = false;       // next chunk claimed (warp-uniform)
     u64 pre_seed, pre_mix;
     prep(cur, pre_seed, pre_mix);
     Game::St s;
@@ -352,6 +356,8 @@ extern "C" __global__ void __launch_bounds__(256, 2) lx_rollout(u32* st, i64 B, 
             u64 sm = __shfl_sync(FULL, pre_mix, pos & 31);
             u64 my_base = cur;
             if (used + n > 32) {                        // switch to the prefetched chunk
+                if (!requested && lane == 0) nxt = atomicAdd(counter, 32ull);
+                requested = false;
                 const u64 nb = __shfl_sync(FULL, nxt, 0);
                 u64 ps2, pm2;
                 prep(nb, ps2, pm2);
@@ -362,9 +368,15 @@ extern "C" __global__ void __launch_bounds__(256, 2) lx_rollout(u32* st, i64 B, 
                 used = used + n - 32;
                 pre_seed = ps2;
                 pre_mix = pm2;
-                if (lane == 0) nxt = atomicAdd(counter, 32ull);
             } else {
                 used += n;
+            }
+            // claim the next chunk once this one is half used: its latency is
+            // then hidden behind ~16 games, and small batches still spread
+            // one chunk per warp before any warp takes a second
+            if (!requested && used >= 16) {
+                if (lane == 0) nxt = atomicAdd(counter, 32ull);
+                requested = true;
             }
             if (need && active) {
                 idx = (i64)(my_base + (u64)(pos & 31));

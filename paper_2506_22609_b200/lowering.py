@@ -401,69 +401,61 @@ class GameLowering:
 
     # -- lines ------------------------------------------------------------
 
-    def line_runs(self, node, stones):
-        """Per-axis window-start bitmaps of ``length`` consecutive stones."""
+    def _line_axis(self, L, d):
+        """Code computing r = window-start bitmap of L stones of ``b`` along d,
+        by doubling r(a+b) = r(a) & walk_a(r(b)) (reference _LineTables.satisfied,
+        exprs.py:433-450, as bit-parallel shifts)."""
+        have = {1: "b"}
+        code = []
+        k = 1
+        while k * 2 <= L:
+            nm = f"r{2 * k}"
+            code.append(f"            const BBW {nm} = {have[k]} & {self.walk(d, k, have[k])};")
+            have[2 * k] = nm
+            k *= 2
+        cur_len, cur = k, have[k]
+        rest = L - k
+        while rest > 0:
+            p = 1
+            while p * 2 <= rest:
+                p *= 2
+            nm = f"r{cur_len + p}"
+            code.append(f"            const BBW {nm} = {cur} & {self.walk(d, cur_len, have[p])};")
+            cur, cur_len, rest = nm, cur_len + p, rest - p
+        return code, cur
+
+    def _line_fn(self, node, kind):
         if node.exact or node.exclude is not None:
             _fail("exact / exclude lines are not lowered yet")
-        L = node.length
         axes = self.board.orientation_dirs(node.orientation)
-        name = f"lines_{self.em.fresh('l')}"
-        lines = []
-        for ai, d in enumerate(axes):
-            # doubling: r(a+b) = r(a) & walk_a(r(b)); windows run along d
-            have = {1: "b"}
-            code = []
-            k = 1
-            while k * 2 <= L:
-                nm = f"r{ai}_{2 * k}"
-                code.append(f"        const BBW {nm} = {have[k]} & {self.walk(d, k, have[k])};")
-                have[2 * k] = nm
-                k *= 2
-            cur_len, cur = k, have[k]
-            rest = L - k
-            while rest > 0:
-                p = 1
-                while p * 2 <= rest:
-                    p *= 2
-                nm = f"r{ai}_{cur_len + p}"
-                code.append(f"        const BBW {nm} = {cur} & {self.walk(d, cur_len, have[p])};")
-                cur, cur_len, rest = nm, cur_len + p, rest - p
-            code.append(f"        z[{ai}] = {cur};")
-            lines += code
-        body = "\n".join(lines)
-        code = f"""    static __device__ __forceinline__ void {name}(const BBW& b, BBW (&z)[{len(axes)}]) {{
-{body}
-    }}"""
-        self.em.helper(name, code)
-        return name, len(axes)
+        name = f"line_{kind}_{self.em.fresh('l')}"
+        body = []
+        for d in axes:
+            code, r = self._line_axis(node.length, d)
+            body.append("        {")
+            body += code
+            body.append(f"            acc = acc | {r};" if kind == "any"
+                        else f"            acc += lx::popc({r});")
+            body.append("        }")
+        init = "BBW acc = lx::bb_zero<W>();" if kind == "any" else "int acc = 0;"
+        ret = "lx::any(acc)" if kind == "any" else "acc"
+        rtype = "bool" if kind == "any" else "int"
+        self.em.helper(name, f"""    static __device__ __forceinline__ {rtype} {name}(const BBW& b) {{
+        {init}
+{chr(10).join(body)}
+        return {ret};
+    }}""")
+        return name
 
     def line_exists(self, node):
+        """Any window of `length` stones of the player (one axis live at a time)."""
         stones = self.stones(self.side(node.player))
-        name, nax = self.line_runs(node, stones)
-        fn = f"{name}_any"
-        self.em.helper(fn, f"""    static __device__ __forceinline__ bool {fn}(const BBW& b) {{
-        BBW z[{nax}];
-        {name}(b, z);
-        BBW o = z[0];
-#pragma unroll
-        for (int i = 1; i < {nax}; i++) o = o | z[i];
-        return lx::any(o);
-    }}""")
-        return f"{fn}({stones})"
+        return f"{self._line_fn(node, 'any')}({stones})"
 
     def line_count(self, node):
+        """Number of satisfied windows (LineFn as a function, exprs.py:454-459)."""
         stones = self.stones(self.side(node.player))
-        name, nax = self.line_runs(node, stones)
-        fn = f"{name}_count"
-        self.em.helper(fn, f"""    static __device__ __forceinline__ int {fn}(const BBW& b) {{
-        BBW z[{nax}];
-        {name}(b, z);
-        int c = 0;
-#pragma unroll
-        for (int i = 0; i < {nax}; i++) c += lx::popc(z[i]);
-        return c;
-    }}""")
-        return f"{fn}({stones})"
+        return f"{self._line_fn(node, 'count')}({stones})"
 
     def line_anchored_exists(self, node):
         """Exact anchored form: a satisfied window through last_dest
@@ -493,10 +485,7 @@ class GameLowering:
 
     # -- connectivity ------------------------------------------------------
 
-    def connected(self, node):
-        """Some component of the side's stones touches every target mask
-        (reference exprs.py:629-652, labels from connectivity.py)."""
-        plan = self.conn_plans[self._conn_plan(node)]
+    def _conn_targets(self, node):
         if isinstance(node.masks, n.MultiMask):
             targets = self.board.multi_mask(node.masks.kind)
         else:
@@ -505,23 +494,174 @@ class GameLowering:
                 _fail("connected targets must be static masks")
         if len(targets) != 2:
             _fail("connected with other than two targets is not lowered yet")
-        stones = self.stones(self.side(node.mover))
-        dil = " | ".join(self.nb(d, "f") for d in plan)
-        name = f"connected_{self.em.fresh('k')}"
+        return targets
+
+    def _dilate(self, plan, var):
+        return " | ".join(self.nb(d, var) for d in plan)
+
+    def _conn_tracking(self):
+        """Decide which (connected node, side) pairs get an incrementally
+        maintained reach set R = the side's stones connected to target 0.
+
+        Valid when stones are only ever added (placement, no capture/flip):
+        components then only grow and merge, so R changes only when a placed
+        stone touches target 0 or R, and then grows by exactly the stones
+        reachable from it outside R.  Sides are narrowed by (mover_is P)
+        conjunctions around the connected test (Hex: P1 top-bottom, P2
+        left-right), so Hex keeps 2 sets of 4 words."""
+        self.conn_slots = {}
+        self.slot_info = []
+        types = {type(x) for x in n.walk(self.spec)}
+        if n.CaptureEffect in types or n.FlipEffect in types or not self.conn_plans:
+            return
+
+        def register(node, gate):
+            who = node.mover
+            if who in (n.MOVER, ""):
+                sides = [gate] if gate is not None else [0, 1]
+            elif who == n.OPPONENT:
+                sides = [1 - gate] if gate is not None else [0, 1]
+            elif who in ("P1", 0):
+                sides = [0]
+            elif who in ("P2", 1):
+                sides = [1]
+            else:
+                sides = [0, 1]
+            for sd in sides:
+                key = (id(node), sd)
+                if key not in self.conn_slots:
+                    self.conn_slots[key] = len(self.slot_info)
+                    plan = self.conn_plans[self._conn_plan(node)]
+                    self.slot_info.append((sd, self._conn_targets(node), plan))
+
+        def visit(node, gate):
+            if isinstance(node, n.PredAnd):
+                g = gate
+                for it in node.items:
+                    if isinstance(it, n.MoverIsPred):
+                        g = int(it.player)
+                for it in node.items:
+                    visit(it, g)
+            elif isinstance(node, n.FunctionPred) and isinstance(node.fn, n.ConnectedFn):
+                register(node.fn, gate)
+            else:
+                for ch in node.children():
+                    visit(ch, None)
+
+        for rule in self.spec.end_rules:
+            visit(rule.condition, None)
+        for x in n.walk(self.spec):
+            if isinstance(x, n.ConnectedFn) and not any(k[0] == id(x) for k in self.conn_slots):
+                register(x, None)
+
+    def _slot_get(self, k):
+        W = self.W
+        words = ", ".join(f"s.ext[{k * W + i}]" for i in range(W))
+        return f"BBW{{{{{words}}}}}"
+
+    def _slot_set(self, k, var):
+        W = self.W
+        return " ".join(f"s.ext[{k * W + i}] = {var}.w[{i}];" for i in range(W))
+
+    def connected(self, node):
+        """Some component of the side's stones touches every target mask
+        (reference exprs.py:629-652, labels from connectivity.py)."""
+        plan = self.conn_plans[self._conn_plan(node)]
+        targets = self._conn_targets(node)
         t0, t1 = self.em.const(targets[0]), self.em.const(targets[1])
+        slots = {sd: k for (nid, sd), k in self.conn_slots.items() if nid == id(node)}
+        if slots:
+            # incremental reach sets: O(1) test
+            sd = self.side(node.mover)
+            parts = {p: f"lx::any({self._slot_get(k)} & {t1})" for p, k in slots.items()}
+            if len(parts) == 1:
+                return next(iter(parts.values()))
+            return f"(({sd}) ? {parts[1]} : {parts[0]})"
+        stones = self.stones(self.side(node.mover))
+        dil_f, dil_g = self._dilate(plan, "f"), self._dilate(plan, "g")
+        name = f"connected_{self.em.fresh('k')}"
         self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const BBW& mine) {{
         // flood the stones reachable from target 0, then test target 1
         BBW f = mine & {t0};
         if (!lx::any(f) || !lx::any(mine & {t1})) return false;
         while (true) {{
-            BBW g = (f | {dil}) & mine;
-            g = (g | {dil.replace('(f)', '(g)')}) & mine;
+            BBW g = (f | {dil_f}) & mine;
+            g = (g | {dil_g}) & mine;
             if (lx::equal(g, f)) break;
             f = g;
         }}
         return lx::any(f & {t1});
     }}""")
         return f"{name}({stones})"
+
+    def _conn_update_code(self):
+        """write_place tail: grow the placing side's reach sets.  One P1 slot
+        and one P2 slot with the same direction plan share a single update
+        on side-selected operands, so lanes of a warp with different movers
+        do not diverge."""
+        out = []
+        by_side = {}
+        for k, (sd, targets, plan) in enumerate(self.slot_info):
+            by_side.setdefault(sd, []).append(k)
+        merged = (len(self.slot_info) == 2 and sorted(by_side) == [0, 1]
+                  and self.slot_info[0][2] == self.slot_info[1][2])
+        groups = [(by_side[0][0], by_side[1][0])] if merged else [(k,) for k in
+                                                                    range(len(self.slot_info))]
+        for grp in groups:
+            plan = self.slot_info[grp[0]][2]
+            dil_f, dil_g = self._dilate(plan, "f"), self._dilate(plan, "g")
+            dil_a = self._dilate(plan, "a")
+            if len(grp) == 2:
+                k0, k1 = grp
+                c0 = self.em.const(self.slot_info[k0][1][0])
+                c1 = self.em.const(self.slot_info[k1][1][0])
+                head = (f"        {{\n            const bool s1 = side != 0;\n"
+                        f"            BBW R = lx::sel(s1, {self._slot_get(k0)}, {self._slot_get(k1)});\n"
+                        f"            const BBW t0 = lx::sel(s1, {c0}, {c1});")
+                store = (f"if (s1) {{ {self._slot_set(k1, 'R')} }} else {{ {self._slot_set(k0, 'R')} }}")
+                cond = "true"
+            else:
+                k = grp[0]
+                sd = self.slot_info[k][0]
+                head = (f"        {{\n            BBW R = {self._slot_get(k)};\n"
+                        f"            const BBW t0 = {self.em.const(self.slot_info[k][1][0])};")
+                store = self._slot_set(k, "R")
+                cond = f"side == {sd}"
+            out.append(f"""{head}
+            const BBW a = lx::onehot<W>(cell);
+            if (({cond}) && lx::any((a & t0) | (({dil_a}) & R))) {{
+                const BBW mine = side ? s.own1 : s.own0;
+                const BBW free_ = lx::andnot(mine, R);
+                BBW f = a;
+                while (true) {{
+                    BBW g = (f | {dil_f}) & free_;
+                    g = (g | {dil_g}) & free_;
+                    if (lx::equal(g, f)) break;
+                    f = g;
+                }}
+                R = R | f;
+                {store}
+            }}
+        }}""")
+        return "\n".join(out)
+
+    def _conn_rebuild_code(self):
+        """Reach sets from scratch (start position, lx_import)."""
+        out = []
+        for k, (sd, targets, plan) in enumerate(self.slot_info):
+            t0 = self.em.const(targets[0])
+            dil_f = self._dilate(plan, "f")
+            out.append(f"""        {{
+            const BBW mine = {"s.own1" if sd else "s.own0"};
+            BBW f = mine & {t0};
+            while (true) {{
+                const BBW g = (f | {dil_f}) & mine;
+                if (lx::equal(g, f)) break;
+                f = g;
+            }}
+            {self._slot_set(k, "f")}
+        }}""")
+        return "\n".join(out)
 
     # -- functions / predicates -------------------------------------------
 
@@ -636,6 +776,8 @@ class GameLowering:
 
     def lower(self):
         self._decide_anchoring()
+        self._conn_tracking()
+        NX = len(self.slot_info) * self.W
         spec = self.spec
         phases = spec.phases
         em = self.em
@@ -720,12 +862,19 @@ class GameLowering:
             }}
         }}"""
         fp = " || ".join(f"phase == {p}" for p in fp_cases) or "false"
+        conn_update = self._conn_update_code()
+        conn_rebuild = self._conn_rebuild_code()
         L = self.layout
+        # rollout block shape: big boards (>= 8 words per side) need ~170
+        # registers to stay spill-free; smaller games run 2 x 256 per SM
+        r_threads, r_minb = (128, 3) if self.W >= 8 else (256, 2)
         src = f"""// generated by paper_2506_22609_b200.lowering for game "{spec.name}"
+#define LX_ROLLOUT_THREADS {r_threads}
+#define LX_ROLLOUT_MINB {r_minb}
 #include "lx_core.cuh"
 
 struct Game {{
-    static constexpr int C = {self.C}, W = {self.W}, NX = 0, A = {self.A}, PASS = {self.PASS};
+    static constexpr int C = {self.C}, W = {self.W}, NX = {NX}, A = {self.A}, PASS = {self.PASS};
     static constexpr int FIRST_PLAYER = {phases[0].order[0]}, NPHASE = {nph};
     static constexpr bool L_SCORES = {str(L['scores']).lower()}, L_PASSING = {str(L['passing']).lower()};
     static constexpr bool L_LAST = {str(L['last_action']).lower()}, L_PHASE = {str(L['phase']).lower()};
@@ -735,6 +884,7 @@ struct Game {{
 @@HELPERS@@
     static __device__ __forceinline__ void start(St& s) {{
 {chr(10).join(start_code)}
+        rebuild_ext(s);
     }}
     static __device__ __forceinline__ BBW legal(const St& s) {{
         const int mover = s.cur;
@@ -752,6 +902,7 @@ struct Game {{
         if (side) lx::setbit(s.own1, cell); else lx::setbit(s.own0, cell);
         s.last_kind = 0; s.last_dest = cell; s.last_mover = side;
         if (side) s.ldbp1 = cell; else s.ldbp0 = cell;
+{conn_update}
     }}
     static __device__ __forceinline__ void effects(St& s, int cell, int mover, int phase) {{
         switch (phase) {{
@@ -773,16 +924,18 @@ struct Game {{
     static __device__ __forceinline__ void labels(const St& s, short* out) {{
 {conn}
     }}
-    static __device__ __forceinline__ void rebuild_ext(St& s) {{}}
+    static __device__ __forceinline__ void rebuild_ext(St& s) {{
+{conn_rebuild}
+    }}
 }};
 
 #include "lx_kernels.cuh"
 """
         src = src.replace("@@CONSTS@@", em.const_defs())
         src = src.replace("@@HELPERS@@", "\n".join(em.helpers.values()))
-        info = {"name": spec.name, "C": self.C, "A": self.A, "W": self.W, "NX": 0,
+        info = {"name": spec.name, "C": self.C, "A": self.A, "W": self.W, "NX": NX,
                 "pass_index": self.PASS, "layout": dict(self.layout),
-                "nwords": 2 * self.W + 7, "nq": (2 * self.W + 7 + 3) // 4,
+                "nwords": 2 * self.W + NX + 7, "nq": (2 * self.W + NX + 7 + 3) // 4,
                 "first_player": int(phases[0].order[0]), "nphase": nph,
                 "observation_planes": 3}
         return Lowered(name=spec.name, source=src, info=info)
