@@ -1,0 +1,140 @@
+// lx_rules.cuh -- per-env rule templates shared by every kernel: the HBM
+// word layout (pack/unpack), start position, sampling and the ply itself.
+// Host-compilable on purpose (no CUDA builtins beyond lx_core.cuh), so the
+// CPU test suite can run the generated rules through tests/hostsim.
+#pragma once
+
+namespace lx {
+
+
+template <class G>
+struct Layout {
+    static constexpr int W = G::W, NX = G::NX;
+    static constexpr int META = 2 * W + NX;
+    static constexpr int NWORDS = META + 7;
+    static constexpr int NQ = (NWORDS + 3) / 4;
+};
+
+template <class G>
+__device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<G>::NQ * 4]) {
+    constexpr int W = G::W, M = Layout<G>::META;
+#pragma unroll
+    for (int i = 0; i < W; i++) { s.own0.w[i] = w[i]; s.own1.w[i] = w[W + i]; }
+#pragma unroll
+    for (int i = 0; i < G::NX; i++) s.ext[i] = w[2 * W + i];
+    s.mc = w[M];
+    const u32 f = w[M + 1];
+    s.cur = f & 1u;
+    s.term = (f >> 1) & 1u;
+    s.trunc = (f >> 2) & 1u;
+    s.outcome = (int)((f >> 3) & 3u) - 1;
+    s.phase = (f >> 5) & 7u;
+    s.last_mover = (int)((f >> 8) & 3u) - 1;
+    s.pf0 = (f >> 10) & 1u;
+    s.pf1 = (f >> 11) & 1u;
+    s.last_kind = (int)((f >> 12) & 7u) - 1;
+    s.last_dest = (short)(w[M + 2] & 0xffffu);
+    s.pass_streak = (short)(w[M + 2] >> 16);
+    s.ldbp0 = (short)(w[M + 3] & 0xffffu);
+    s.ldbp1 = (short)(w[M + 3] >> 16);
+    s.sc0 = (short)(w[M + 4] & 0xffffu);
+    s.sc1 = (short)(w[M + 4] >> 16);
+    s.seed = (u64)w[M + 5] | ((u64)w[M + 6] << 32);
+}
+
+template <class G>
+__device__ __forceinline__ void pack(const typename G::St& s, u32 (&w)[Layout<G>::NQ * 4]) {
+    constexpr int W = G::W, M = Layout<G>::META;
+#pragma unroll
+    for (int i = 0; i < W; i++) { w[i] = s.own0.w[i]; w[W + i] = s.own1.w[i]; }
+#pragma unroll
+    for (int i = 0; i < G::NX; i++) w[2 * W + i] = s.ext[i];
+    w[M] = s.mc;
+    w[M + 1] = (u32)s.cur | ((u32)s.term << 1) | ((u32)s.trunc << 2) |
+               ((u32)(s.outcome + 1) << 3) | ((u32)s.phase << 5) |
+               ((u32)(s.last_mover + 1) << 8) | ((u32)s.pf0 << 10) | ((u32)s.pf1 << 11) |
+               ((u32)(s.last_kind + 1) << 12);
+    w[M + 2] = ((u32)s.last_dest & 0xffffu) | ((u32)s.pass_streak << 16);
+    w[M + 3] = ((u32)s.ldbp0 & 0xffffu) | ((u32)s.ldbp1 << 16);
+    w[M + 4] = ((u32)s.sc0 & 0xffffu) | ((u32)s.sc1 << 16);
+    w[M + 5] = (u32)s.seed;
+    w[M + 6] = (u32)(s.seed >> 32);
+#pragma unroll
+    for (int i = Layout<G>::NWORDS; i < Layout<G>::NQ * 4; i++) w[i] = 0u;
+}
+
+// start position (reference compiler.py:329-345 _build_template + init)
+template <class G>
+__device__ __forceinline__ void init_state(typename G::St& s, u64 seed) {
+    s.own0 = bb_zero<G::W>();
+    s.own1 = bb_zero<G::W>();
+#pragma unroll
+    for (int i = 0; i < (G::NX > 0 ? G::NX : 1); i++) s.ext[i] = 0u;
+    s.mc = 0u;
+    s.cur = G::FIRST_PLAYER;
+    s.term = 0; s.trunc = 0; s.outcome = -1; s.phase = 0;
+    s.last_mover = -1; s.last_kind = -1; s.last_dest = -1;
+    s.pass_streak = 0; s.pf0 = 0; s.pf1 = 0; s.ldbp0 = -1; s.ldbp1 = -1;
+    s.sc0 = 0; s.sc1 = 0;
+    s.seed = seed;
+    G::start(s);
+}
+
+// uniform legal action for the current mover; -1 when stuck
+// (reference compiler.py:430-446, mechanics.py:488-492)
+template <class G>
+__device__ __forceinline__ int sample_action(const typename G::St& s, u64 smix) {
+    const BB<G::W> legal = G::legal(s);
+    const int n = popc(legal);
+    if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
+    const int r = draw_index(mix64(smix ^ (u64)s.mc), n);
+    return select_bit(legal, r);
+}
+
+// one ply for a live row (reference compiler.py:456-580, order preserved:
+// mechanic write, pass bookkeeping, effects, score clamp, advancement,
+// ordered end rules evaluated for the mover, counters)
+template <class G>
+__device__ __forceinline__ void apply_step(typename G::St& s, int action) {
+    const int mover = s.cur;
+    const int phase = s.phase;
+    const bool is_pass = (G::PASS >= 0) && action == G::PASS;
+    if (is_pass) {
+        s.last_kind = 4; s.last_dest = -1; s.last_mover = mover;
+    } else {
+        G::write_place(s, action, mover, phase);
+    }
+    if (G::L_PASSING) {
+        if (is_pass) {
+            s.pass_streak += 1;
+            if (mover) s.pf1 = 1; else s.pf0 = 1;
+        } else {
+            s.pass_streak = 0;
+            if (mover) s.pf1 = 0; else s.pf0 = 0;
+        }
+    }
+    if (!is_pass) G::effects(s, action, mover, phase);
+    if (G::L_SCORES) {
+        s.sc0 = s.sc0 < 0 ? 0 : s.sc0;
+        s.sc1 = s.sc1 < 0 ? 0 : s.sc1;
+    }
+    int next_player, next_phase;
+    G::advance(phase, mover, next_player, next_phase);
+    const int out = G::end_rules(s, mover);
+    if (out >= 0) { s.term = 1; s.outcome = out; }
+    s.mc += 1u;
+    s.cur = next_player;
+    s.phase = next_phase;
+}
+
+// legality of one action (reference mechanics.py:499-512, compiler.py:484-494)
+template <class G>
+__device__ __forceinline__ bool action_legal(const typename G::St& s, i64 a) {
+    const BB<G::W> legal = G::legal(s);
+    if (G::PASS >= 0 && a == G::PASS) return !any(legal) && G::force_pass(s.phase);
+    if (a < 0 || a >= G::C) return false;
+    return test(legal, (int)a);
+}
+
+
+}  // namespace lx

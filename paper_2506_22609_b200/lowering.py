@@ -322,6 +322,21 @@ class GameLowering:
             dirs += [d, OPPOSITE[d]]
         return dirs
 
+    def _ks_fill(self, e, gen, pro, max_run, ind="            "):
+        """Kogge-Stone occluded fill along e: g = gen plus every cell y of a
+        run y, y+e, .., y+(j-1)e of `pro` cells with y+je in gen, j <= 2^m - 1
+        >= max_run.  Log-steps walk(e, 1), walk(e, 2), walk(e, 4) ... with
+        exact k-step validity masks (no wrap).  Declares BBW g."""
+        code = [f"{ind}BBW g = {gen};", f"{ind}BBW p = {pro};"]
+        k, covered = 1, 0
+        while covered < max_run:
+            code.append(f"{ind}g = g | (p & {self.walk(e, k, 'g')});")
+            covered += k
+            if covered < max_run:
+                code.append(f"{ind}p = p & {self.walk(e, k, 'p')};")
+            k *= 2
+        return code
+
     def custodial_anchored(self, node):
         """Anchored custodial runs from last_dest (reference exprs.py:254-292).
 
@@ -339,11 +354,16 @@ class GameLowering:
             if steps == 0:
                 continue
             lines.append("        {")
-            lines.append("            BBW x = " + self.nb(OPPOSITE[d], "a") + " & tgt;")
-            lines.append("            BBW run = x;")
-            for _ in range(steps - 1):
-                lines.append("            x = " + self.nb(OPPOSITE[d], "x") + " & tgt;")
-                lines.append("            run = run | x;")
+            if node.length == "any":
+                # run of targets from the anchor along d (fill moves forward: opposite gather)
+                lines += self._ks_fill(OPPOSITE[d], "a", "tgt", steps)
+                lines.append("            const BBW run = g & tgt;")
+            else:
+                lines.append("            BBW x = " + self.nb(OPPOSITE[d], "a") + " & tgt;")
+                lines.append("            BBW run = x;")
+                for _ in range(steps - 1):
+                    lines.append("            x = " + self.nb(OPPOSITE[d], "x") + " & tgt;")
+                    lines.append("            run = run | x;")
             check = ""
             if node.length != "any":
                 check = f" && lx::popc(run) == {node.length}"
@@ -375,13 +395,12 @@ class GameLowering:
         lines = []
         for d in self.custodial_dirs(node):
             lines.append("        {")
-            lines.append("            BBW z = tgt & " + self.nb(d, "flank") + ";")
             if node.length == "any":
-                lines.append("            BBW acc = z;")
-                for _ in range(max_len - 2):
-                    lines.append("            z = tgt & " + self.nb(d, "z") + ";")
-                    lines.append("            acc = acc | z;")
+                # cells y of target runs that reach a flanker along d
+                lines += self._ks_fill(d, "flank", "tgt", max_len - 1)
+                lines.append("            const BBW acc = g & tgt;")
             else:
+                lines.append("            BBW z = tgt & " + self.nb(d, "flank") + ";")
                 for _ in range(node.length - 1):
                     lines.append("            z = tgt & " + self.nb(d, "z") + ";")
                 lines.append("            const BBW acc = z;")

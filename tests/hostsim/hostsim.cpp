@@ -1,0 +1,103 @@
+// hostsim.cpp -- TEST INFRASTRUCTURE.  Runs a lowered game's rules on the CPU
+// (same templates as the kernels: lx_core.cuh, lx_rules.cuh, generated
+// struct Game) and exports the reference GameState layout, so the CPU test
+// suite can compare the lowering against the oracle without a GPU.
+// Built per game by tests/hostsim/hostsim.py with -DGAME_SOURCE="<file>".
+#include "host_compat.h"
+#include "lx_core.cuh"
+#include GAME_SOURCE
+#include "lx_rules.cuh"
+
+#include <cstring>
+#include <vector>
+
+typedef Game::St St;
+
+struct RefOut {
+    int8_t *board_piece, *board_owner, *current_player;
+    int32_t *move_count;
+    uint8_t *terminated, *truncated;
+    int8_t *outcome;
+    uint64_t *seeds;
+    int32_t *scores;
+    int16_t *pass_streak;
+    uint8_t *pass_flags;
+    int8_t *last_mover, *last_kind;
+    int16_t *last_source, *last_dest, *last_dest_by_player, *comp_labels;
+    int8_t *phase;
+};
+
+static void export_one(const St& s, int64_t i, const RefOut* p) {
+    for (int c = 0; c < Game::C; c++) {
+        const bool a = lx::test(s.own0, c), b = lx::test(s.own1, c);
+        p->board_owner[i * Game::C + c] = a ? 0 : (b ? 1 : -1);
+        p->board_piece[i * Game::C + c] = (a || b) ? 0 : -1;
+    }
+    p->current_player[i] = (int8_t)s.cur;
+    p->move_count[i] = (int32_t)s.mc;
+    p->terminated[i] = (uint8_t)s.term;
+    p->truncated[i] = (uint8_t)s.trunc;
+    p->outcome[i] = (int8_t)s.outcome;
+    p->seeds[i] = s.seed;
+    if (p->scores) { p->scores[2 * i] = s.sc0; p->scores[2 * i + 1] = s.sc1; }
+    if (p->pass_streak) {
+        p->pass_streak[i] = (int16_t)s.pass_streak;
+        p->pass_flags[2 * i] = (uint8_t)s.pf0;
+        p->pass_flags[2 * i + 1] = (uint8_t)s.pf1;
+    }
+    if (p->last_mover) {
+        p->last_mover[i] = (int8_t)s.last_mover;
+        p->last_kind[i] = (int8_t)s.last_kind;
+        p->last_source[i] = -1;
+        p->last_dest[i] = (int16_t)s.last_dest;
+        p->last_dest_by_player[2 * i] = (int16_t)s.ldbp0;
+        p->last_dest_by_player[2 * i + 1] = (int16_t)s.ldbp1;
+    }
+    if (p->comp_labels) Game::labels(s, (short*)(p->comp_labels + i * Game::C));
+    if (p->phase) p->phase[i] = (int8_t)s.phase;
+}
+
+extern "C" {
+
+// engine.playout_random from given seeds; also round-trips every state
+// through pack/unpack each ply (checks the HBM word layout).
+int64_t sim_playout(int64_t B, const uint64_t* seeds, int max_turns, const RefOut* out) {
+    int64_t steps = 0;
+    for (int64_t i = 0; i < B; i++) {
+        St s;
+        lx::init_state<Game>(s, seeds[i]);
+        const uint64_t smix = lx::seed_mix(s.seed);
+        while (!s.term && (int)s.mc < max_turns) {
+            const int a = lx::sample_action<Game>(s, smix);
+            if (a < 0) break;
+            lx::apply_step<Game>(s, a);
+            u32 w[lx::Layout<Game>::NQ * 4];
+            lx::pack<Game>(s, w);
+            lx::unpack<Game>(s, w);
+            steps++;
+        }
+        if (!s.term) { s.term = 1; s.trunc = 1; s.outcome = 0; }
+        export_one(s, i, out);
+    }
+    return steps;
+}
+
+// per-ply legal masks of env `seed` (A bytes per ply, up to max_plies)
+int sim_masks(uint64_t seed, int max_plies, uint8_t* masks, int64_t* actions) {
+    St s;
+    lx::init_state<Game>(s, seed);
+    const uint64_t smix = lx::seed_mix(s.seed);
+    int t = 0;
+    for (; t < max_plies && !s.term; t++) {
+        lx::BB<Game::W> legal = Game::legal(s);
+        for (int c = 0; c < Game::C; c++) masks[t * Game::A + c] = lx::test(legal, c);
+        if (Game::PASS >= 0) masks[t * Game::A + Game::C] = !lx::any(legal) && Game::force_pass(s.phase);
+        const int a = lx::sample_action<Game>(s, smix);
+        actions[t] = a;
+        if (a < 0) break;
+        lx::apply_step<Game>(s, a);
+    }
+    return t;
+}
+
+}
