@@ -167,9 +167,9 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
     lx::store_state<Game>(s, st, B, i);
 }
 
-// Fused rollout.  Persistent threads: each thread plays one env to the end
-// with the whole state in registers, then claims the next env index with a
-// warp-aggregated atomic, so no lane idles while a long game finishes.
+// Fused rollout.  Persistent threads: each thread plays one env at a time to
+// the end with the whole state in registers, then starts another, so no lane
+// idles while a long game finishes.
 //   mode & 1: start each env from its seed (seeds[i] or spawn(seed_base, first+i))
 //             else load it from st
 //   mode & 2: store the final state to st
@@ -177,28 +177,37 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
 // stats (u64[8], zeroed by the caller): steps, p1 wins, p2 wins, draws,
 // truncated, envs finished.  *counter must be zero.  *stuck = min row that
 // had no legal action (init ~0).
+//
+// Game-over handling is batched per warp: a lane whose game ends keeps its
+// final state in registers and waits until LX_REFILL_LANES lanes are waiting
+// (or LX_REFILL_WAIT plies passed, or nothing else is running); then every
+// waiting lane flushes (stats, final-state store) and starts its next env in
+// one pass, instead of one or two lanes running that code every ply.
 #ifndef LX_ROLLOUT_THREADS
 #define LX_ROLLOUT_THREADS 256
 #endif
 #ifndef LX_ROLLOUT_MINB
 #define LX_ROLLOUT_MINB 2
 #endif
-extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB) lx_rollout(u32* st, i64 B, int max_turns,
-                                                             int mode, u64 seed_base,
-                                                             const u64* seeds, i64 first,
-                                                             u64* stats, u64* counter,
-                                                             u64* stuck, signed char* outcomes,
-                                                             int* turns) {
+#ifndef LX_REFILL_LANES
+#define LX_REFILL_LANES 6
+#endif
+#ifndef LX_REFILL_WAIT
+#define LX_REFILL_WAIT 6
+#endif
+extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB)
+lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* seeds, i64 first,
+           u64* stats, u64* counter, u64* stuck, signed char* outcomes, int* turns) {
     constexpr unsigned FULL = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned lanes_below = (1u << lane) - 1u;
     const u64 base_mix = lx::seed_mix(seed_base);
-    u64 n_steps = 0, n_p1 = 0, n_p2 = 0, n_draw = 0, n_trunc = 0, n_done = 0;
-    // Env indices are handed out in warp-private chunks of 32.  The next
-    // chunk is claimed one chunk ahead, so the atomic's latency is hidden
-    // behind ~32 games; each lane precomputes the seed (and its first mix)
-    // of env cur+lane at full warp width, and a lane starting a new game
-    // fetches its seed with a shuffle.
+    u32 n_steps = 0, n_p1 = 0, n_p2 = 0, n_draw = 0, n_trunc = 0, n_done = 0;
+    // Env indices are handed out in warp-private chunks of 32, the next chunk
+    // claimed once the current one is half used (its atomic's latency hides
+    // behind ~16 games); each lane precomputes the seed (and its first mix)
+    // of env chunk+lane at full warp width and a lane starting a game fetches
+    // its seed with a shuffle.
     auto prep = [&](u64 base, u64& ps, u64& pm) {
         const i64 j = (i64)(base + lane);
         ps = 0;
@@ -218,16 +227,32 @@ extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB
     Game::St s;
     u64 smix = 0;
     i64 idx = -1;
-    bool need = true, active = true;
+    bool playing = false, pending = false, active = true;
+    int waited = 0;               // plies since a lane started waiting (warp-uniform)
     while (true) {
-        const unsigned want = __ballot_sync(FULL, need && active);
-        if (want) {                                     // warp-uniform
-            const int n = __popc(want);
-            const int pos = used + __popc(want & lanes_below);
+        const unsigned idle = __ballot_sync(FULL, active && !playing);
+        const unsigned busy = __ballot_sync(FULL, playing);
+        if (idle && (__popc(idle) >= LX_REFILL_LANES || waited >= LX_REFILL_WAIT || !busy)) {
+            waited = 0;
+            const bool me = (idle >> lane) & 1u;
+            if (me && pending) {                        // flush the finished game
+                if ((mode & 4) && !s.term) { s.term = 1; s.trunc = 1; s.outcome = 0; }
+                n_p1 += s.outcome == 1;
+                n_p2 += s.outcome == 2;
+                n_draw += s.outcome == 0;
+                n_trunc += s.trunc;
+                n_done += 1;
+                if (mode & 2) lx::store_state<Game>(s, st, B, idx);
+                if (outcomes) outcomes[idx] = (signed char)s.outcome;
+                if (turns) turns[idx] = (int)s.mc;
+                pending = false;
+            }
+            const int n = __popc(idle);
+            const int pos = used + __popc(idle & lanes_below);
             u64 sd = __shfl_sync(FULL, pre_seed, pos & 31);
             u64 sm = __shfl_sync(FULL, pre_mix, pos & 31);
             u64 my_base = cur;
-            if (used + n > 32) {                        // switch to the prefetched chunk
+            if (used + n > 32) {                        // switch to the next chunk
                 if (!requested && lane == 0) nxt = atomicAdd(counter, 32ull);
                 requested = false;
                 const u64 nb = __shfl_sync(FULL, nxt, 0);
@@ -243,14 +268,11 @@ extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB
             } else {
                 used += n;
             }
-            // claim the next chunk once this one is half used: its latency is
-            // then hidden behind ~16 games, and small batches still spread
-            // one chunk per warp before any warp takes a second
             if (!requested && used >= 16) {
                 if (lane == 0) nxt = atomicAdd(counter, 32ull);
                 requested = true;
             }
-            if (need && active) {
+            if (me) {
                 idx = (i64)(my_base + (u64)(pos & 31));
                 if (idx >= B) {
                     active = false;
@@ -262,35 +284,27 @@ extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB
                         lx::load_state<Game>(s, st, B, idx);
                         smix = lx::seed_mix(s.seed);
                     }
-                    need = false;
+                    playing = !(s.term || (int)s.mc >= max_turns);
+                    pending = !playing;
                 }
             }
+        } else if (idle) {
+            waited++;
         }
-        if (!__any_sync(0xffffffffu, active)) break;
-        if (active) {
-            bool done = s.term || (int)s.mc >= max_turns;
-            if (!done) {
-                const int a = lx::sample_action<Game>(s, smix);
-                if (a < 0) {
-                    atomicMin(stuck, (u64)idx);
-                    done = true;
-                } else {
-                    lx::apply_step<Game>(s, a);
-                    n_steps++;
-                    done = s.term || (int)s.mc >= max_turns;
+        if (!__any_sync(FULL, active)) break;
+        if (playing) {
+            const int a = lx::sample_action<Game>(s, smix);
+            if (a < 0) {
+                atomicMin(stuck, (u64)idx);
+                playing = false;
+                pending = true;
+            } else {
+                lx::apply_step<Game>(s, a);
+                n_steps++;
+                if (s.term || (int)s.mc >= max_turns) {
+                    playing = false;
+                    pending = true;
                 }
-            }
-            if (done) {
-                if ((mode & 4) && !s.term) { s.term = 1; s.trunc = 1; s.outcome = 0; }
-                n_p1 += s.outcome == 1;
-                n_p2 += s.outcome == 2;
-                n_draw += s.outcome == 0;
-                n_trunc += s.trunc;
-                n_done += 1;
-                if (mode & 2) lx::store_state<Game>(s, st, B, idx);
-                if (outcomes) outcomes[idx] = (signed char)s.outcome;
-                if (turns) turns[idx] = (int)s.mc;
-                need = true;
             }
         }
     }
@@ -305,12 +319,12 @@ extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB
         n_done += __shfl_xor_sync(0xffffffffu, n_done, o);
     }
     if (lane == 0) {
-        atomicAdd(stats + 0, n_steps);
-        atomicAdd(stats + 1, n_p1);
-        atomicAdd(stats + 2, n_p2);
-        atomicAdd(stats + 3, n_draw);
-        atomicAdd(stats + 4, n_trunc);
-        atomicAdd(stats + 5, n_done);
+        atomicAdd(stats + 0, (u64)n_steps);
+        atomicAdd(stats + 1, (u64)n_p1);
+        atomicAdd(stats + 2, (u64)n_p2);
+        atomicAdd(stats + 3, (u64)n_draw);
+        atomicAdd(stats + 4, (u64)n_trunc);
+        atomicAdd(stats + 5, (u64)n_done);
     }
 }
 

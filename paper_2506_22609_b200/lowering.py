@@ -22,6 +22,7 @@ raises CompileError("lower", ...) -- there is no CPU fallback.
 from __future__ import annotations
 
 import hashlib
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -887,9 +888,14 @@ class GameLowering:
         # rollout block shape: big boards (>= 8 words per side) need ~170
         # registers to stay spill-free; smaller games run 2 x 256 per SM
         r_threads, r_minb = (128, 3) if self.W >= 8 else (256, 2)
+        # batched game-over handling (lx_kernels.cuh); env overrides for tuning
+        r_lanes = int(os.environ.get("LX_REFILL_LANES", "6"))
+        r_wait = int(os.environ.get("LX_REFILL_WAIT", "6"))
         src = f"""// generated by paper_2506_22609_b200.lowering for game "{spec.name}"
 #define LX_ROLLOUT_THREADS {r_threads}
 #define LX_ROLLOUT_MINB {r_minb}
+#define LX_REFILL_LANES {r_lanes}
+#define LX_REFILL_WAIT {r_wait}
 #include "lx_core.cuh"
 
 struct Game {{
@@ -918,9 +924,12 @@ struct Game {{
     static __device__ __forceinline__ bool force_pass(int phase) {{ return {fp}; }}
     static __device__ __forceinline__ void write_place(St& s, int cell, int mover, int phase) {{
         const int side = {owner};
-        if (side) lx::setbit(s.own1, cell); else lx::setbit(s.own0, cell);
+        const BBW oh = lx::onehot<W>(cell);          // branchless: no warp split on the mover
+        s.own0 = lx::sel(side != 0, s.own0 | oh, s.own0);
+        s.own1 = lx::sel(side != 0, s.own1, s.own1 | oh);
         s.last_kind = 0; s.last_dest = cell; s.last_mover = side;
-        if (side) s.ldbp1 = cell; else s.ldbp0 = cell;
+        s.ldbp0 = side ? s.ldbp0 : cell;
+        s.ldbp1 = side ? cell : s.ldbp1;
 {conn_update}
     }}
     static __device__ __forceinline__ void effects(St& s, int cell, int mover, int phase) {{
@@ -972,9 +981,10 @@ struct Game {{
         if t is n.FlipEffect:
             m = self.mask(e.mask)
             sd = self.side(e.mover)
-            return (f"{ind}{{ const BBW cells = {m} & (s.own0 | s.own1); const int fs = {sd};\n"
-                    f"{ind}  if (fs) {{ s.own1 = s.own1 | cells; s.own0 = lx::andnot(s.own0, cells); }}\n"
-                    f"{ind}  else {{ s.own0 = s.own0 | cells; s.own1 = lx::andnot(s.own1, cells); }} }}")
+            # branchless (lanes of a warp hold different movers)
+            return (f"{ind}{{ const BBW cells = {m} & (s.own0 | s.own1); const bool fs = ({sd}) != 0;\n"
+                    f"{ind}  s.own0 = lx::sel(fs, s.own0 | cells, lx::andnot(s.own0, cells));\n"
+                    f"{ind}  s.own1 = lx::sel(fs, lx::andnot(s.own1, cells), s.own1 | cells); }}")
         if t is n.CaptureEffect:
             m = self.mask(e.mask)
             inc = ""
