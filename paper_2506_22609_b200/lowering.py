@@ -888,9 +888,13 @@ class GameLowering:
         # rollout block shape: big boards (>= 8 words per side) need ~170
         # registers to stay spill-free; smaller games run 2 x 256 per SM
         r_threads, r_minb = (128, 3) if self.W >= 8 else (256, 2)
-        # batched game-over handling (lx_kernels.cuh); env overrides for tuning
-        r_lanes = int(os.environ.get("LX_REFILL_LANES", "6"))
-        r_wait = int(os.environ.get("LX_REFILL_WAIT", "6"))
+        # batched game-over handling (lx_kernels.cuh): worth it for short games
+        # only (measured on B200 at 2^22 envs, profiles/r1_tune_refill.jsonl:
+        # TTT best 8-12, C4 best 6, Hex/Reversi/Pente best 1); board size bounds
+        # the game length.  Env overrides for tuning.
+        k_def = 8 if self.C <= 16 else (6 if self.C <= 48 else 1)
+        r_lanes = int(os.environ.get("LX_REFILL_LANES", str(k_def)))
+        r_wait = int(os.environ.get("LX_REFILL_WAIT", str(k_def)))
         src = f"""// generated by paper_2506_22609_b200.lowering for game "{spec.name}"
 #define LX_ROLLOUT_THREADS {r_threads}
 #define LX_ROLLOUT_MINB {r_minb}
