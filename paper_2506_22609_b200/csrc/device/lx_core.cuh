@@ -205,6 +205,37 @@ __device__ __forceinline__ double key_uniform(u64 key) {
     return __dmul_rn((double)(key >> 11), 0x1p-53);
 }
 
+__device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
+
+// Per-thread shared-memory mirror of both boards, for rules that probe a few
+// cells at run-time positions (anchored captures / lines on big boards): a
+// probe is one LDS instead of a W-way register select, and it runs on the
+// LSU pipe while the bitboard work saturates the ALU pipe.  Layout
+// [word][thread] keeps every access bank-conflict free.
+#ifndef LX_MIRROR_STRIDE
+#define LX_MIRROR_STRIDE 256
+#endif
+template <int W>
+struct Mirror {
+    static __device__ __forceinline__ u32* slot() {
+        __shared__ u32 buf[2 * W * LX_MIRROR_STRIDE];
+        return buf + threadIdx.x;
+    }
+    static __device__ __forceinline__ void store(const BB<W>& p0, const BB<W>& p1) {
+        u32* m = slot();
+#pragma unroll
+        for (int i = 0; i < W; i++) {
+            m[i * LX_MIRROR_STRIDE] = p0.w[i];
+            m[(W + i) * LX_MIRROR_STRIDE] = p1.w[i];
+        }
+    }
+    // is `cell` occupied by `player` (0/1)?
+    static __device__ __forceinline__ bool probe(int player, int cell) {
+        const u32 w = slot()[(player * W + (cell >> 5)) * LX_MIRROR_STRIDE];
+        return (w >> (cell & 31)) & 1u;
+    }
+};
+
 // register-resident state of one env (unpacked from the HBM state words)
 template <int W, int NX>
 struct State {

@@ -338,6 +338,102 @@ class GameLowering:
             k *= 2
         return code
 
+    # -- cell probes (big boards) --------------------------------------------
+
+    @property
+    def use_probe(self):
+        """Anchored rules on boards of >= 6 words per side use cell probes
+        through the shared-memory mirror instead of whole-board shifts."""
+        return self.W >= 6
+
+    def _max_steps(self, d):
+        """Expression: how many steps along d stay on the board from (r, col)."""
+        dr, dc = self.board.delta(d)
+        terms = []
+        if dr > 0:
+            terms.append(f"({self.board.rows - 1} - r) / {dr}")
+        elif dr < 0:
+            terms.append(f"r / {-dr}")
+        if dc > 0:
+            terms.append(f"({self.board.cols - 1} - col) / {dc}")
+        elif dc < 0:
+            terms.append(f"col / {-dc}")
+        if not terms:
+            return "0"
+        out = terms[0]
+        for t in terms[1:]:
+            out = f"lx::imin({out}, {t})"
+        return out
+
+    def custodial_anchored_probe(self, node):
+        """Fixed-length anchored custodial run by probing cells from last_dest:
+        anchor+kd (k=1..n) target stones and anchor+(n+1)d a flanker
+        (reference exprs.py:254-292 with length n)."""
+        side = self.side(node.mover)
+        n_len = node.length
+        name = f"custodial_probe_{self.em.fresh('c')}"
+        lines = []
+        for d in self.custodial_dirs(node):
+            S = self._shift[d]
+            conds = [f"M::probe(tg, c + {k * S})" for k in range(1, n_len + 1)]
+            conds.append(f"M::probe(side, c + {(n_len + 1) * S})")
+            lines.append(f"        if ({self._max_steps(d)} >= {n_len + 1} && "
+                         + " && ".join(conds) + ") {")
+            for k in range(1, n_len + 1):
+                lines.append(f"            lx::setbit(out, c + {k * S});")
+            lines.append("        }")
+        body = "\n".join(lines)
+        self.em.helper(name, f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
+        typedef lx::Mirror<W> M;
+        const int side = {side};
+        const int tg = 1 - side;
+        BBW out = lx::bb_zero<W>();
+        if (!(s.last_dest >= 0 && s.last_mover == side)) return out;
+        M::store(s.own0, s.own1);
+        const int c = s.last_dest;
+        const int r = c / {self.board.cols};
+        const int col = c - r * {self.board.cols};
+{body}
+        return out;
+    }}""")
+        return f"{name}(s, mover)"
+
+    def line_anchored_probe(self, node):
+        """Anchored line test (reference exprs.py:484-535) by probing: the run
+        of the player's stones through last_dest along some axis has at least
+        `length` cells."""
+        if node.exact or node.exclude is not None:
+            _fail("exact / exclude lines are not lowered yet")
+        side = self.side(node.player)
+        L = node.length
+        name = f"line_probe_{self.em.fresh('a')}"
+        lines = []
+        for d in self.board.orientation_dirs(node.orientation):
+            for sgn, dd in ((1, d), (-1, OPPOSITE[d])):
+                S = self._shift[dd]
+                lines.append(f"        {{ const int mk = {self._max_steps(dd)}; bool on = true;")
+                for k in range(1, L):
+                    lines.append(f"          on = on && mk >= {k} && M::probe(side, c + {k * S}); "
+                                 f"run += on;")
+                lines.append("        }")
+            lines.append(f"        if (run >= {L - 1}) return true;")
+            lines.append("        run = 0;")
+        body = "\n".join(lines)
+        self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const St& s, int mover) {{
+        typedef lx::Mirror<W> M;
+        const int side = {side};
+        if (!(s.last_dest >= 0 && s.last_mover == mover)) return false;
+        const int c = s.last_dest;
+        M::store(s.own0, s.own1);
+        if (!M::probe(side, c)) return false;
+        const int r = c / {self.board.cols};
+        const int col = c - r * {self.board.cols};
+        int run = 0;
+{body}
+        return false;
+    }}""")
+        return f"{name}(s, mover)"
+
     def custodial_anchored(self, node):
         """Anchored custodial runs from last_dest (reference exprs.py:254-292).
 
@@ -346,6 +442,8 @@ class GameLowering:
         the run length.  The reference bounds runs by the padded ray length
         L (runlen < L), which any flanked run on the board satisfies.
         """
+        if self.use_probe and node.length != "any":
+            return self.custodial_anchored_probe(node)
         side = self.side(node.mover)
         name = f"custodial_{self.em.fresh('c')}"
         lines = []
@@ -751,6 +849,8 @@ class GameLowering:
         passes through the placed stone.  Otherwise the exact anchored form
         is emitted."""
         if end_rule and id(line) in self._anchored_lines:
+            if self.use_probe:                 # exact anchored semantics, cheap on big boards
+                return self.line_anchored_probe(line)
             if id(line) in self._global_ok:
                 return self.line_exists(line)
             return self.line_anchored_exists(line)

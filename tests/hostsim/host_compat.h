@@ -8,6 +8,9 @@
 #define __device__
 #define __forceinline__ inline
 #define __host__
+#define __shared__ static
+struct HostThreadIdx { unsigned x = 0, y = 0, z = 0; };
+static const HostThreadIdx threadIdx;
 
 static inline int __popc(unsigned x) { return __builtin_popcount(x); }
 static inline int __ffs(int x) { return __builtin_ffs(x); }
