@@ -141,7 +141,7 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     B_total = args.batch * max(ws, args.gpus)
     rates = []
-    per = max(args.cpu_seconds / max(args.steps, 1), 0.5)
+    per = max(args.cpu_seconds / max(args.steps, 1), 0.02)
     for w in range(args.warmup):
         cpu_rate(args.game, B_total, min(per, 1.0), threads, args.max_turns)
     sample = None
@@ -159,7 +159,40 @@ def run_reference(args):
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    ref = numpy_reference_rate(args.game, seconds=3.0, max_turns=args.max_turns)
+    if ref:
+        line["reference_numpy"] = ref
     print(json.dumps(line), flush=True)
+
+
+def numpy_reference_rate(game, seconds, max_turns, batch=1024):
+    """For context only: the unmodified reference (pip-installed into
+    baseline/_ref) timed through its own _run_episode (evaluation.py:197-211),
+    one process, B=1024, on the same game program."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "boardlang")):
+        return None
+    try:
+        sys.path.insert(0, ref_dir)
+        import numpy as np
+        import boardlang
+        from boardlang import evaluation, rng as rrng
+        with open(os.path.join(ROOT, "paper_2506_22609_b200", "games", f"{game}.ldx")) as f:
+            g = boardlang.load_game(f.read())
+        steps, t, e = 0, 0.0, 0
+        while t < seconds:
+            seed = rrng.hash_key(np.uint64(0), np.uint64(batch), np.uint64(10_000 + e))
+            s, dt = evaluation._run_episode(g, batch, seed, max_turns)
+            steps += s
+            t += dt
+            e += 1
+        return {"value": steps / t, "unit": UNIT, "cores": 1, "episodes": e,
+                "sample": f"{e} episodes x {batch} envs via boardlang.evaluation._run_episode"}
+    except Exception as exc:              # context only; never fail the bench
+        return {"error": repr(exc)[:200]}
+    finally:
+        if ref_dir in sys.path:
+            sys.path.remove(ref_dir)
 
 
 def config(args, ws):
@@ -229,7 +262,8 @@ def main():
 
     extras = {}
     if rank == 0 and not args.no_extras:
-        extras = measure_extras(args, game, lx, rng, B, B_total, value, ms_max / args.steps)
+        extras = measure_extras(args, game, lx, rng, B, B_total, value, ms_max / args.steps,
+                                clk.summary().get("sm_mhz"), tot)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup,
@@ -258,7 +292,7 @@ def native_rollout(game, state, B, max_turns, seed, first, stats, work):
         game._stream()))
 
 
-def measure_extras(args, game, lx, rng, B, B_total, value, ms_step):
+def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, totals):
     """e2e through the public API, the HBM-bound step kernel, roofline data,
     and the CPU baseline (rank 0, N=1 sizes)."""
     import torch
@@ -290,18 +324,32 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step):
                   "d2h_bytes_per_step": B + 64,
                   "path": "B200Game.rollout(seeds=host->device) + outcomes device->host"}
 
-    # ---- roofline of the fused rollout kernel: integer issue bound
+    # ---- roofline of the fused rollout kernel: integer ALU pipe bound.
+    # Per-env-step instruction counts come from the ncu capture of this exact
+    # cubin (profiles/rollout_<Game>.json, keyed by the NVRTC cache key);
+    # achieved = count x live env steps/s; peak = pipe rate x SMs x clock.
     prof = load_profile(game)
-    clk_mhz = 1965.0
-    peak_warp_inst = 148 * 4 * clk_mhz * 1e6          # 1 warp-inst/clk/SMSP
-    rl = {"bound": "int_issue", "unit": "Gwarp-inst/s", "peak": peak_warp_inst / 1e9,
-          "peak_source": "148 SMs x 4 SMSP x 1 warp-inst/clk x 1965 MHz (B200_PROFILING.md)",
-          "kernel": "lx_rollout", "traffic": None, "achieved": None, "frac": None}
+    clk_mhz = float(clock_mhz or 1965.0)
+    sms = 148
+    peak_alu = sms * 4 * 0.5 * clk_mhz * 1e6          # ALU pipe: 0.5 warp-inst/clk/SMSP
+    peak_issue = sms * 4 * 1.0 * clk_mhz * 1e6        # issue: 1 warp-inst/clk/SMSP
+    mean_plies = totals[0] / max(totals[5], 1)
+    rl = {"bound": "int_alu", "unit": "Gwarp-inst/s", "kernel": "lx_rollout",
+          "peak": peak_alu / 1e9,
+          "peak_source": f"{sms} SMs x 4 SMSP x 0.5 ALU warp-inst/clk (B300_MICROARCH.md pipe "
+                         f"rates) x {clk_mhz:.0f} MHz measured SM clock",
+          "achieved": None, "frac": None, "traffic": None,
+          "algorithmic_bytes_per_env_step": game.info["nq"] * 16 / mean_plies}
     if prof:
-        ach = prof["warp_inst_per_env_step"] * value
-        rl.update({"achieved": ach / 1e9, "frac": ach / peak_warp_inst,
-                   "traffic": prof.get("dram_bytes_per_launch"),
-                   "inst_source": prof.get("source")})
+        ach = prof["alu_warp_inst_per_env_step"] * value
+        iss = prof["warp_inst_per_env_step"] * value
+        rl.update({"achieved": ach / 1e9, "frac": ach / peak_alu,
+                   "traffic": prof["dram_bytes_per_launch"] / prof["env_steps_in_launch"],
+                   "traffic_unit": "DRAM bytes per env step (ncu)",
+                   "issue": {"achieved": iss / 1e9, "peak": peak_issue / 1e9,
+                             "frac": iss / peak_issue},
+                   "ncu_alu_pipe_pct": prof.get("alu_pipe_elapsed_pct"),
+                   "inst_source": prof.get("source"), "cubin_key": prof.get("cubin_key")})
     out["roofline"] = rl
 
     # ---- HBM-bound per-ply step kernel (PGX-style API path)

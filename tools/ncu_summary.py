@@ -17,8 +17,9 @@ import subprocess
 METRICS = {
     "gpu__time_duration.sum": "duration_ns",
     "smsp__inst_executed.sum": "warp_inst",
-    "smsp__thread_inst_executed.sum": "thread_inst",
-    "sm__inst_executed_pipe_alu.sum": "alu_warp_inst",
+    "thread_inst_executed": "thread_inst",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed": "alu_pipe_elapsed_pct",
+    "device__attribute_multiprocessor_count": "sms",
     "sm__inst_executed_pipe_fma.sum": "fma_warp_inst",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
@@ -73,6 +74,10 @@ def main():
             info = json.loads(f.read().strip().splitlines()[-1])
         m = raw(rep)
         steps = info["env_steps"]
+        # ALU pipe: 0.5 warp-inst/clk per SMSP, 4 SMSPs per SM (B300_MICROARCH.md)
+        sms = m.get("sms", 148)
+        m["alu_warp_inst"] = (m.get("alu_pipe_elapsed_pct", 0) / 100.0 * 0.5 * 4 * sms
+                              * m["sm_clock_hz"] * m["duration_ns"] / 1e9)
         s = {"game": game, "batch": info["batch"], "cubin_key": info["cubin_key"],
              "env_steps_in_launch": steps, **m,
              "warp_inst_per_env_step": m["warp_inst"] / steps,
