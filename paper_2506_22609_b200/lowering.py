@@ -615,7 +615,40 @@ class GameLowering:
         return targets
 
     def _dilate(self, plan, var):
-        return " | ".join(self.nb(d, var) for d in plan)
+        """Expression: cells with a plan-direction neighbour in `var`.
+
+        Directions that are the composition of two others (nbr_d = nbr_b
+        after nbr_a, on every cell, validity included) share a shift:
+        x(nbr_d(y)) = nb_a(nb_b(x))(y), so nb_a(x) | nb_a(nb_b(x)) = nb_a(x | nb_b(x)).
+        Hex's 6-neighbourhood then costs 4 shifts, the square 8-neighbourhood 4."""
+        B = self.board
+        C = self.C
+        comp = {}
+        plan = list(plan)
+        for d in plan:
+            for a in plan:
+                for b in plan:
+                    if len({a, b, d}) < 3 or d in comp:
+                        continue
+                    na, nb_, nd = B.neighbors[a], B.neighbors[b], B.neighbors[d]
+                    ok = all((nb_[nd_a] if (nd_a := na[y]) != C else C) == nd[y]
+                             for y in range(C))
+                    if ok:
+                        comp[d] = (a, b)
+        base = [d for d in plan if d not in comp or comp[d][0] in comp or comp[d][1] in comp]
+        comp = {d: ab for d, ab in comp.items() if d not in base}
+        if not comp:
+            return " | ".join(self.nb(d, var) for d in plan)
+        tmp = {d: f"{var}_{d}" for d in base}
+        decl = " ".join(f"const BBW {tmp[d]} = {self.nb(d, var)};" for d in base)
+        terms = []
+        for a in base:
+            inner = [tmp[b] for d, (a2, b) in comp.items() if a2 == a]
+            if inner:
+                terms.append(self.nb(a, f"({var} | {' | '.join(sorted(set(inner)))})"))
+            else:
+                terms.append(tmp[a])
+        return f"([&]() {{ {decl} return BBW({' | '.join(terms)}); }}())"
 
     def _conn_tracking(self):
         """Decide which (connected node, side) pairs get an incrementally
@@ -750,12 +783,11 @@ class GameLowering:
             if (({cond}) && lx::any((a & t0) | (({dil_a}) & R))) {{
                 const BBW mine = side ? s.own1 : s.own0;
                 const BBW free_ = lx::andnot(mine, R);
-                BBW f = a;
-                while (true) {{
-                    BBW g = (f | {dil_f}) & free_;
-                    g = (g | {dil_g}) & free_;
-                    if (lx::equal(g, f)) break;
+                BBW f = a;                               // grow inside the side's stones outside R
+                BBW g = (f | {dil_f}) & free_;
+                while (!lx::equal(g, f)) {{
                     f = g;
+                    g = (f | {dil_f}) & free_;
                 }}
                 R = R | f;
                 {store}
