@@ -45,6 +45,60 @@ __device__ __forceinline__ void store_state(const typename G::St& s, u32* __rest
 
 __device__ __forceinline__ i64 gtid() { return (i64)blockIdx.x * blockDim.x + threadIdx.x; }
 
+// 4 mask bits -> 4 bytes of 0/1
+__device__ __forceinline__ u32 spread4(u32 x) { return ((x & 0xfu) * 0x00204081u) & 0x01010101u; }
+
+// Warp-cooperative write of the (B, A) uint8 legal mask for the warp's 32
+// consecutive envs: each lane stages its row as a bit vector (cells, then the
+// pass column) in shared memory; the warp's rows form one contiguous block of
+// 32*A bytes in global memory, written with coalesced 16-byte stores.  Every
+// lane of the warp must call it (rows >= B pass valid = false).
+template <class G>
+__device__ __forceinline__ void write_mask_rows(unsigned char* __restrict__ mask, i64 B, i64 i,
+                                                bool valid, const BB<G::W>& legal,
+                                                bool pass_bit) {
+    constexpr int A = G::A, NW = (G::A + 31) / 32, STRIDE = NW + 1;
+    __shared__ u32 stage[(256 / 32) * 32 * STRIDE];
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    u32* mine = stage + (warp * 32 + lane) * STRIDE;
+#pragma unroll
+    for (int j = 0; j < NW; j++) {
+        u32 v = j < G::W ? legal.w[j] : 0u;
+        if (G::PASS >= 0 && j == (G::C >> 5) && pass_bit) v |= 1u << (G::C & 31);
+        mine[j] = valid ? v : 0u;
+    }
+    mine[NW] = 0u;
+    __syncwarp();
+    const i64 i0 = i - lane;
+    const i64 left = B - i0;
+    const int nrows = left < 32 ? (int)left : 32;
+    const int bytes = nrows * A;
+    unsigned char* base = mask + i0 * (i64)A;
+    const u32* rows = stage + warp * 32 * STRIDE;
+    for (int p0 = (int)lane * 16; p0 < bytes; p0 += 32 * 16) {
+        const int nb = bytes - p0 < 16 ? bytes - p0 : 16;
+        u32 v = 0u;
+        int got = 0, r = p0 / A, c = p0 - r * A;
+        while (got < nb) {
+            const int take = (nb - got) < (A - c) ? (nb - got) : (A - c);
+            const u32* rw = rows + r * STRIDE;
+            const u32 lo = rw[c >> 5], hi = rw[(c >> 5) + 1];
+            const u32 bits = __funnelshift_r(lo, hi, (unsigned)(c & 31)) & ((1u << take) - 1u);
+            v |= bits << got;
+            got += take;
+            r++;
+            c = 0;
+        }
+        if (nb == 16) {
+            *reinterpret_cast<uint4*>(base + p0) =
+                make_uint4(spread4(v), spread4(v >> 4), spread4(v >> 8), spread4(v >> 12));
+        } else {
+            for (int j = 0; j < nb; j++) base[p0 + j] = (v >> j) & 1u;
+        }
+    }
+    __syncwarp();
+}
+
 }  // namespace lx
 
 
@@ -86,26 +140,19 @@ extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const 
 extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
                                                            unsigned char* mask, i64* counts) {
     const i64 i = lx::gtid();
-    if (i >= B) return;
-    Game::St s;
-    lx::load_state<Game>(s, st, B, i);
-    lx::BB<Game::W> legal = Game::legal(s);
-    if (s.term) legal = lx::bb_zero<Game::W>();
-    const int n = lx::popc(legal);
-    const bool pass_only = !s.term && n == 0 && Game::force_pass(s.phase);
-    if (counts) counts[i] = s.term ? 0 : (pass_only ? 1 : n);
-    if (mask) {
-        unsigned char* row = mask + i * (i64)Game::A;
-#pragma unroll
-        for (int wd = 0; wd < Game::W; wd++) {
-            const u32 v = legal.w[wd];
-            for (int b = 0; b < 32; b++) {
-                const int c = wd * 32 + b;
-                if (c < Game::C) row[c] = (v >> b) & 1u;
-            }
-        }
-        if (Game::PASS >= 0) row[Game::C] = pass_only;
+    if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
+    const bool valid = i < B;
+    lx::BB<Game::W> legal = lx::bb_zero<Game::W>();
+    bool pass_only = false;
+    if (valid) {
+        Game::St s;
+        lx::load_state<Game>(s, st, B, i);
+        if (!s.term) legal = Game::legal(s);
+        const int n = lx::popc(legal);
+        pass_only = !s.term && n == 0 && Game::force_pass(s.phase);
+        if (counts) counts[i] = s.term ? 0 : (pass_only ? 1 : n);
     }
+    if (mask) lx::write_mask_rows<Game>(mask, B, i, valid, legal, pass_only);
 }
 
 // sampled action per row from u (when given) or from the row's own stream
@@ -342,44 +389,37 @@ extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, co
                                                               unsigned char* truncated,
                                                               int* player) {
     const i64 i = lx::gtid();
-    if (i >= B) return;
-    Game::St s;
-    lx::load_state<Game>(s, st, B, i);
-    const bool was = s.term;
-    float r0 = 0.f, r1 = 0.f;
-    if (!was && actions) {
-        lx::apply_step<Game>(s, (int)actions[i]);
-        if (s.term) {
-            r0 = s.outcome == 1 ? 1.f : (s.outcome == 2 ? -1.f : 0.f);
-            r1 = -r0;
-        } else if (max_turns > 0 && (int)s.mc >= max_turns) {
-            s.term = 1; s.trunc = 1; s.outcome = 0;
-        }
-    }
-    if (auto_reset && s.term && actions) {
-        const u64 seed = lx::mix64(lx::seed_mix(s.seed) ^ 0xE9ull);
-        lx::init_state<Game>(s, seed);
-    }
-    if (actions) lx::store_state<Game>(s, st, B, i);
-    if (rewards) { rewards[2 * i] = r0; rewards[2 * i + 1] = r1; }
-    if (terminated) terminated[i] = (unsigned char)s.term;
-    if (truncated) truncated[i] = (unsigned char)s.trunc;
-    if (player) player[i] = s.cur;
-    if (mask) {
-        lx::BB<Game::W> legal = Game::legal(s);
-        if (s.term) legal = lx::bb_zero<Game::W>();
-        const bool pass_only = !s.term && !lx::any(legal) && Game::force_pass(s.phase);
-        unsigned char* row = mask + i * (i64)Game::A;
-#pragma unroll
-        for (int wd = 0; wd < Game::W; wd++) {
-            const u32 v = legal.w[wd];
-            for (int b = 0; b < 32; b++) {
-                const int c = wd * 32 + b;
-                if (c < Game::C) row[c] = (v >> b) & 1u;
+    if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
+    const bool valid = i < B;
+    lx::BB<Game::W> legal = lx::bb_zero<Game::W>();
+    bool pass_only = false;
+    if (valid) {
+        Game::St s;
+        lx::load_state<Game>(s, st, B, i);
+        const bool was = s.term;
+        float r0 = 0.f, r1 = 0.f;
+        if (!was && actions) {
+            lx::apply_step<Game>(s, (int)actions[i]);
+            if (s.term) {
+                r0 = s.outcome == 1 ? 1.f : (s.outcome == 2 ? -1.f : 0.f);
+                r1 = -r0;
+            } else if (max_turns > 0 && (int)s.mc >= max_turns) {
+                s.term = 1; s.trunc = 1; s.outcome = 0;
             }
         }
-        if (Game::PASS >= 0) row[Game::C] = pass_only;
+        if (auto_reset && s.term && actions) {
+            const u64 seed = lx::mix64(lx::seed_mix(s.seed) ^ 0xE9ull);
+            lx::init_state<Game>(s, seed);
+        }
+        if (actions) lx::store_state<Game>(s, st, B, i);
+        if (rewards) reinterpret_cast<float2*>(rewards)[i] = make_float2(r0, r1);
+        if (terminated) terminated[i] = (unsigned char)s.term;
+        if (truncated) truncated[i] = (unsigned char)s.trunc;
+        if (player) player[i] = s.cur;
+        if (mask && !s.term) legal = Game::legal(s);
+        pass_only = !s.term && !lx::any(legal) && Game::force_pass(s.phase);
     }
+    if (mask) lx::write_mask_rows<Game>(mask, B, i, valid, legal, pass_only);
 }
 
 // device state -> reference GameState SoA (state.py:78-130)
