@@ -373,6 +373,34 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
                                        "traffic": None,
                                        "bytes_per_env_ply": 2 * game.info["nq"] * 16}}
 
+    # ---- PGX-style API path (LudaxEnvironment): lx_sample + lx_env_step per ply
+    env = lx.LudaxEnvironment(game, auto_reset=True)
+    est = env.init(seed=2, batch_size=B)
+    for _ in range(3):
+        est = env.step_(est, env.random_actions(est))
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_s = t_e = 0.0
+    plies = 16
+    for _ in range(plies):
+        ev[0].record()
+        acts = env.random_actions(est)
+        ev[1].record()
+        est = env.step_(est, acts)
+        ev[2].record()
+        torch.cuda.synchronize()
+        t_s += ev[0].elapsed_time(ev[1])
+        t_e += ev[1].elapsed_time(ev[2])
+    nq, A = game.info["nq"], game.action_space_size
+    b_env = 2 * nq * 16 + 8 + A + 8 + 6      # state r/w, action, mask, rewards, flags
+    gbs = b_env * B / (t_e / plies / 1e3) / 1e9
+    out["env_step_api"] = {
+        "path": "LudaxEnvironment.random_actions + step_ (auto_reset), device tensors",
+        "env_steps_per_s": B / ((t_s + t_e) / plies / 1e3), "plies_timed": plies,
+        "kernel": "lx_env_step",
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak_hbm, "unit": "GB/s",
+                     "frac": gbs / peak_hbm, "traffic": None, "bytes_per_env_step": b_env}}
+
     # ---- CPU baseline (oracle port, all host threads, bounded sample)
     threads = os.cpu_count() or 1
     r, steps, dt, n = cpu_rate(args.game, B_total, args.cpu_seconds, threads, args.max_turns)
