@@ -234,6 +234,13 @@ struct Mirror {
         const u32 w = slot()[(player * W + (cell >> 5)) * LX_MIRROR_STRIDE];
         return (w >> (cell & 31)) & 1u;
     }
+    // branch-free probe: `ok` gates a possibly off-board cell (clamped, so the
+    // load stays inside the mirror)
+    static __device__ __forceinline__ u32 probe_if(bool ok, int player, int cell) {
+        const int c = ok ? cell : 0;
+        const u32 w = slot()[(player * W + (c >> 5)) * LX_MIRROR_STRIDE];
+        return ok ? ((w >> (c & 31)) & 1u) : 0u;
+    }
 };
 
 // register-resident state of one env (unpacked from the HBM state words)

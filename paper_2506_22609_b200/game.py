@@ -371,6 +371,21 @@ class B200Game:
             state._touch()
         return state, stats
 
+    def with_seeds(self, state, seeds):
+        """Copy of ``state`` whose rows draw from new RNG streams (the MCTS
+        rollout re-keying, reference agents.py:229-233)."""
+        torch = _torch()
+        out = state.copy()
+        s = _u64_tensor(seeds, state.batch_size)
+        m = 2 * self.info["W"] + self.info["NX"] + 5          # seed lo word (lx_kernels.cuh)
+        lo = (s & 0xFFFFFFFF).to(torch.int64)
+        hi = ((s >> 32) & 0xFFFFFFFF).to(torch.int64)
+        lo = torch.where(lo >= 2 ** 31, lo - 2 ** 32, lo).to(torch.int32)
+        hi = torch.where(hi >= 2 ** 31, hi - 2 ** 32, hi).to(torch.int32)
+        out.words[m // 4, :, m % 4] = lo
+        out.words[(m + 1) // 4, :, (m + 1) % 4] = hi
+        return out
+
     # -- observation --
     def observe_device(self, state, player):
         torch = _torch()

@@ -375,13 +375,14 @@ class GameLowering:
         lines = []
         for d in self.custodial_dirs(node):
             S = self._shift[d]
-            conds = [f"M::probe(tg, c + {k * S})" for k in range(1, n_len + 1)]
-            conds.append(f"M::probe(side, c + {(n_len + 1) * S})")
-            lines.append(f"        if ({self._max_steps(d)} >= {n_len + 1} && "
-                         + " && ".join(conds) + ") {")
+            # branch-free: all probes issue (clamped when off-board), one rare branch
+            lines.append(f"        {{ const bool ok = {self._max_steps(d)} >= {n_len + 1};")
+            conds = [f"M::probe_if(ok, tg, c + {k * S})" for k in range(1, n_len + 1)]
+            conds.append(f"M::probe_if(ok, side, c + {(n_len + 1) * S})")
+            lines.append("        if (" + " & ".join(conds) + ") {")
             for k in range(1, n_len + 1):
                 lines.append(f"            lx::setbit(out, c + {k * S});")
-            lines.append("        }")
+            lines.append("        } }")
         body = "\n".join(lines)
         self.em.helper(name, f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
         typedef lx::Mirror<W> M;
@@ -411,9 +412,9 @@ class GameLowering:
         for d in self.board.orientation_dirs(node.orientation):
             for sgn, dd in ((1, d), (-1, OPPOSITE[d])):
                 S = self._shift[dd]
-                lines.append(f"        {{ const int mk = {self._max_steps(dd)}; bool on = true;")
+                lines.append(f"        {{ const int mk = {self._max_steps(dd)}; u32 on = 1u;")
                 for k in range(1, L):
-                    lines.append(f"          on = on && mk >= {k} && M::probe(side, c + {k * S}); "
+                    lines.append(f"          on &= M::probe_if(mk >= {k}, side, c + {k * S}); "
                                  f"run += on;")
                 lines.append("        }")
             lines.append(f"        if (run >= {L - 1}) return true;")
@@ -1020,6 +1021,8 @@ class GameLowering:
         # rollout block shape: big boards (>= 8 words per side) need ~170
         # registers to stay spill-free; smaller games run 2 x 256 per SM
         r_threads, r_minb = (128, 3) if self.W >= 8 else (256, 2)
+        r_threads = int(os.environ.get("LX_ROLLOUT_THREADS", r_threads))     # tuning overrides
+        r_minb = int(os.environ.get("LX_ROLLOUT_MINB", r_minb))
         # batched game-over handling (lx_kernels.cuh): worth it for short games
         # only (measured on B200 at 2^22 envs, profiles/r1_tune_refill.jsonl:
         # TTT best 8-12, C4 best 6, Hex/Reversi/Pente best 1); board size bounds

@@ -173,3 +173,23 @@ def test_full_size_hex_no_draws_and_reversi_conservation():
     p2 = (h["board_owner"] == 1).sum(axis=1)
     assert (h["scores"][:, 0] == p1).all() and (h["scores"][:, 1] == p2).all()
     assert (h["outcome"] == np.where(p1 > p2, 1, np.where(p2 > p1, 2, 0))).all()
+
+
+@pytest.mark.parametrize("name", GAMES)
+def test_mcts_rollout_primitive(name):
+    """engine.rollout_outcomes == reference agents._rollout semantics: continue
+    from mid-game states with re-keyed seeds (agents.py:229-233), draws at the cap."""
+    g, og = game(name), O.OracleGame(name)
+    B = 200
+    st, ost = g.init(B, seed=21), og.init(B, seed=21)
+    for _ in range(5):
+        a = og.sample_actions(ost)
+        og.step_into(ost, a, verify=False)
+        g.step_into(st, a, verify=False)
+    keys = lx.rng.hash_key(np.uint64(777), np.uint64(0x5011), np.arange(B, dtype=np.uint64))
+    got = lx.engine.rollout_outcomes(g, st, max_turns=60, seeds=keys).cpu().numpy()
+    ost["seeds"][:] = keys
+    fin, _ = og.playout(state=ost, max_turns=60)
+    want = np.where(fin["terminated"] & ~fin["truncated"], fin["outcome"], 0)
+    assert np.array_equal(got, want)
+    assert st.digest() != O.digest(fin)        # input state untouched (still mid-game)
