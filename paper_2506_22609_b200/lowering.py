@@ -1018,9 +1018,9 @@ class GameLowering:
         conn_update = self._conn_update_code()
         conn_rebuild = self._conn_rebuild_code()
         L = self.layout
-        # rollout block shape: big boards (>= 8 words per side) need ~170
-        # registers to stay spill-free; smaller games run 2 x 256 per SM
-        r_threads, r_minb = (128, 3) if self.W >= 8 else (256, 2)
+        # rollout block shape: 2 x 256 threads per SM (<= 128 registers) won a
+        # B200 sweep for every config game incl. Pente (128x3..5 and 256x2 tried)
+        r_threads, r_minb = 256, 2
         r_threads = int(os.environ.get("LX_ROLLOUT_THREADS", r_threads))     # tuning overrides
         r_minb = int(os.environ.get("LX_ROLLOUT_MINB", r_minb))
         # batched game-over handling (lx_kernels.cuh): worth it for short games
