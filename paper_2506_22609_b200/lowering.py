@@ -399,6 +399,63 @@ class GameLowering:
     }}""")
         return f"{name}(s, mover)"
 
+    def custodial_anchored_rays(self, node):
+        """Anchored custodial runs of any length on boards of <= 64 cells with
+        per-cell ray masks (reference exprs.py:254-292): along each direction
+        the first non-target cell on the ray from the anchor is found with a
+        lowest/highest-set-bit trick; the run is flanked iff that cell is a
+        flanker, and the run is every ray cell before it."""
+        side = self.side(node.mover)
+        name = f"custodial_rays_{self.em.fresh('c')}"
+        dirs = self.custodial_dirs(node)
+        C = self.C
+        rows = []
+        for d in dirs:
+            nt = self.board.neighbors[d]
+            vals = []
+            for c in range(C):
+                m, x = 0, int(nt[c])
+                while x != C:
+                    m |= 1 << x
+                    x = int(nt[x])
+                vals.append(m)
+            rows.append("{" + ", ".join(f"0x{v:016x}ull" for v in vals) + "}")
+        table = f"RAYS_{name}"
+        self.em.helper(table, f"    static __device__ __forceinline__ u64 {table}(int d, int c) {{\n"
+                              f"        static __device__ const u64 t[{len(dirs)}][{C}] = {{\n            "
+                              + ",\n            ".join(rows) + "};\n        return t[d][c];\n    }")
+        lines = []
+        for k, d in enumerate(dirs):
+            S = self._shift[d]
+            lines.append("        {")
+            lines.append(f"            const u64 r = {table}({k}, c);")
+            lines.append("            const u64 blk = r & ~tgt;            // first of these ends the run")
+            if S > 0:
+                lines.append("            const u64 first = blk & (0ull - blk);")
+                lines.append("            if (first & flank) run |= r & (first - 1ull);")
+            else:
+                lines.append("            const u64 first = blk ? (1ull << (63 - __clzll((long long)blk))) : 0ull;")
+                lines.append("            if (first & flank) run |= r & ~((first << 1) - 1ull);")
+            lines.append("        }")
+        body = "\n".join(lines)
+        W = self.W
+        to64 = "(u64)b.w[0]" + (" | ((u64)b.w[1] << 32)" if W == 2 else "")
+        self.em.helper(name, f"""    static __device__ __forceinline__ u64 {name}_u64(const BBW& b) {{ return {to64}; }}
+    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
+        const int side = {side};
+        BBW out = lx::bb_zero<W>();
+        if (!(s.last_dest >= 0 && s.last_mover == side)) return out;
+        const u64 flank = {name}_u64(side ? s.own1 : s.own0);
+        const u64 tgt = {name}_u64(side ? s.own0 : s.own1);
+        const int c = s.last_dest;
+        u64 run = 0ull;
+{body}
+        out.w[0] = (u32)run;
+        {"out.w[1] = (u32)(run >> 32);" if W == 2 else ""}
+        return out;
+    }}""")
+        return f"{name}(s, mover)"
+
     def line_anchored_probe(self, node):
         """Anchored line test (reference exprs.py:484-535) by probing: the run
         of the player's stones through last_dest along some axis has at least
@@ -445,6 +502,8 @@ class GameLowering:
         """
         if self.use_probe and node.length != "any":
             return self.custodial_anchored_probe(node)
+        if node.length == "any" and self.W <= 2:
+            return self.custodial_anchored_rays(node)
         side = self.side(node.mover)
         name = f"custodial_{self.em.fresh('c')}"
         lines = []
