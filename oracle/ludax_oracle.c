@@ -61,8 +61,9 @@ typedef struct {
     int nend;
     int end_kind[4], end_arg[4], end_gate[4], end_ea[4], end_eb[4], end_res[4], end_anch[4];
     /* line windows for "any" orientation (topology.py:319-359) */
-    int line_len, nwin;
+    int line_len, nwin, line_exact;
     int16_t win[MAXW][5];
+    int16_t win_before[MAXW], win_after[MAXW];   /* extension cells (topology.py:348-352) */
     /* custodial walk directions: each axis then its inverse (exprs.py:244-251) */
     int ncust;
     int cust_dir[8];
@@ -135,6 +136,7 @@ static void build_lines(orc_game *g, int len) {
     /* orientation "any" on grids: right, down, down_right, down_left
        (topology.py:96-103); windows enumerated per axis, per start cell */
     static const char *axes[4] = {"right", "down", "down_right", "down_left"};
+    static const char *inv_axes[4] = {"left", "up", "up_left", "up_right"};
     g->line_len = len; g->nwin = 0;
     for (int a = 0; a < 4; a++) {
         int d = dir_index_grid(axes[a]);
@@ -143,6 +145,8 @@ static void build_lines(orc_game *g, int len) {
             while (k < len && g->nbr[d][cells[k - 1]] != g->C) { cells[k] = g->nbr[d][cells[k - 1]]; k++; }
             if (k == len) {
                 for (int j = 0; j < len; j++) g->win[g->nwin][j] = (int16_t)cells[j];
+                g->win_before[g->nwin] = g->nbr[dir_index_grid(inv_axes[a])][s];
+                g->win_after[g->nwin] = g->nbr[d][cells[len - 1]];
                 g->nwin++;
             }
         }
@@ -202,6 +206,12 @@ orc_game *orc_game_new(const char *name) {
         g->end_kind[0] = END_LINE; g->end_arg[0] = 5; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
         g->end_kind[1] = END_SCORE_GE; g->end_arg[1] = 10; g->end_res[1] = RES_MOVER_WIN;
         g->end_kind[2] = END_FULL; g->end_res[2] = RES_DRAW;
+    } else if (!strcmp(name, "gomoku")) {              /* corpus: games/gomoku.ldx */
+        g->game = 5; build_topology(g, FAM_GRID, 15, 15); build_lines(g, 5);
+        g->line_exact = 1; g->L_last = 1;
+        g->nend = 2;
+        g->end_kind[0] = END_LINE; g->end_arg[0] = 5; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
+        g->end_kind[1] = END_FULL; g->end_res[1] = RES_DRAW;
     } else {
         free(g);
         return NULL;
@@ -345,6 +355,11 @@ static int line_sat(const env_t *e, int side, int anchored) {
         for (int j = 0; j < g->line_len && ok; j++) {
             int c = g->win[w][j];
             ok = e->own[c] == side && e->pc[c] == 0;
+        }
+        if (ok && g->line_exact) {        /* exprs.py:444-448: extensions not the side's */
+            int b = g->win_before[w], a = g->win_after[w];
+            if (b != g->C && e->own[b] == side && e->pc[b] == 0) ok = 0;
+            if (a != g->C && e->own[a] == side && e->pc[a] == 0) ok = 0;
         }
         if (ok) return 1;
     }

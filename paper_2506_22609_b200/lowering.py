@@ -460,21 +460,22 @@ class GameLowering:
         """Anchored line test (reference exprs.py:484-535) by probing: the run
         of the player's stones through last_dest along some axis has at least
         `length` cells."""
-        if node.exact or node.exclude is not None:
-            _fail("exact / exclude lines are not lowered yet")
+        if node.exclude is not None:
+            _fail("line exclude: is not lowered yet")
         side = self.side(node.player)
         L = node.length
         name = f"line_probe_{self.em.fresh('a')}"
         lines = []
+        steps = L if node.exact else L - 1          # exact: detect overlines too
         for d in self.board.orientation_dirs(node.orientation):
             for sgn, dd in ((1, d), (-1, OPPOSITE[d])):
                 S = self._shift[dd]
                 lines.append(f"        {{ const int mk = {self._max_steps(dd)}; u32 on = 1u;")
-                for k in range(1, L):
+                for k in range(1, steps + 1):
                     lines.append(f"          on &= M::probe_if(mk >= {k}, side, c + {k * S}); "
                                  f"run += on;")
                 lines.append("        }")
-            lines.append(f"        if (run >= {L - 1}) return true;")
+            lines.append(f"        if (run {'==' if node.exact else '>='} {L - 1}) return true;")
             lines.append("        run = 0;")
         body = "\n".join(lines)
         self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const St& s, int mover) {{
@@ -603,8 +604,8 @@ class GameLowering:
         return code, cur
 
     def _line_fn(self, node, kind):
-        if node.exact or node.exclude is not None:
-            _fail("exact / exclude lines are not lowered yet")
+        if node.exclude is not None:
+            _fail("line exclude: is not lowered yet")
         axes = self.board.orientation_dirs(node.orientation)
         name = f"line_{kind}_{self.em.fresh('l')}"
         body = []
@@ -612,6 +613,13 @@ class GameLowering:
             code, r = self._line_axis(node.length, d)
             body.append("        {")
             body += code
+            if node.exact:
+                # exact: the cells just before and after the window are not the
+                # player's (reference exprs.py:444-448; off-board counts as not)
+                code.append("")
+                body.append(f"            const BBW rx = lx::andnot(lx::andnot({r}, "
+                            f"{self.nb(OPPOSITE[d], 'b')}), {self.walk(d, node.length, 'b')});")
+                r = "rx"
             body.append(f"            acc = acc | {r};" if kind == "any"
                         else f"            acc += lx::popc({r});")
             body.append("        }")
@@ -642,13 +650,19 @@ class GameLowering:
         stones = self.stones(self.side(node.player))
         L = node.length
         name = f"line_anchor_{self.em.fresh('a')}"
+        if node.exclude is not None:
+            _fail("line exclude: is not lowered yet")
         lines = []
+        # exact lines need the maximal run through the anchor to be exactly L:
+        # grow L steps each way and compare (reference exprs.py:525-533)
+        steps = L if node.exact else L - 1
+        test = f"== {L}" if node.exact else f">= {L}"
         for d in self.board.orientation_dirs(node.orientation):
             lines.append("        {")
             lines.append("            BBW e = a;")
-            for _ in range(L - 1):
+            for _ in range(steps):
                 lines.append(f"            e = (e | {self.nb(d, 'e')} | {self.nb(OPPOSITE[d], 'e')}) & b;")
-            lines.append(f"            hit = hit || lx::popc(e | a) >= {L};")
+            lines.append(f"            hit = hit || lx::popc(e | a) {test};")
             lines.append("        }")
         body = "\n".join(lines)
         self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const St& s, int mover, const BBW& b) {{

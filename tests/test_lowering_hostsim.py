@@ -8,7 +8,8 @@ from hostsim.hostsim import HostGame
 from oracle import oracle as O
 from paper_2506_22609_b200 import lowering, rng, syntax
 
-B = {"tic_tac_toe": 4096, "connect_four": 2048, "hex": 512, "reversi": 1024, "pente": 128}
+B = {"tic_tac_toe": 4096, "connect_four": 2048, "hex": 512, "reversi": 1024, "pente": 128,
+     "gomoku": 256}
 
 
 @pytest.fixture(scope="module", params=GAMES)
