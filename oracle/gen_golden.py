@@ -31,10 +31,11 @@ from boardlang.parser import parse_game  # noqa: E402
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
 GAMES_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                          "paper_2506_22609_b200", "games")
-GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku")
+GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath")
 PLAYOUT = {"tic_tac_toe": [(1024, 0), (512, 99)], "connect_four": [(256, 0), (256, 5)],
            "hex": [(64, 0), (48, 21)], "reversi": [(64, 0), (64, 12)],
-           "pente": [(32, 0), (24, 3)], "gomoku": [(32, 0), (24, 5)]}
+           "pente": [(32, 0), (24, 3)], "gomoku": [(32, 0), (24, 5)],
+           "yavalath": [(128, 0), (96, 9)]}
 
 
 def state_arrays(st, prefix):

@@ -23,11 +23,11 @@
 #define MAXC 384
 #define MAXW 1100
 
-enum { FAM_GRID = 0, FAM_HEXRECT = 1 };
+enum { FAM_GRID = 0, FAM_HEXRECT = 1, FAM_HEXAGON = 2 };
 enum { DEST_EMPTY = 0, DEST_C4 = 1, DEST_CENTER = 2 };
 enum { EFF_NONE = 0, EFF_REVERSI = 1, EFF_PENTE = 2 };
-enum { END_LINE = 0, END_FULL = 1, END_CONN = 2, END_PASSED_BOTH = 3, END_SCORE_GE = 4 };
-enum { RES_MOVER_WIN = 0, RES_DRAW = 1, RES_BY_SCORE = 2 };
+enum { END_LINE = 0, END_FULL = 1, END_CONN = 2, END_PASSED_BOTH = 3, END_SCORE_GE = 4, END_LINE_LOSE = 5 };
+enum { RES_MOVER_WIN = 0, RES_DRAW = 1, RES_BY_SCORE = 2, RES_MOVER_LOSE = 3 };
 enum { ST_OK = 0, ST_ILLEGAL = 1, ST_TERMINAL = 2, ST_EMPTY_MASK = 3 };
 
 /* --- rng.py:12-42 --------------------------------------------------------- */
@@ -61,9 +61,12 @@ typedef struct {
     int nend;
     int end_kind[4], end_arg[4], end_gate[4], end_ea[4], end_eb[4], end_res[4], end_anch[4];
     /* line windows for "any" orientation (topology.py:319-359) */
-    int line_len, nwin, line_exact;
-    int16_t win[MAXW][5];
-    int16_t win_before[MAXW], win_after[MAXW];   /* extension cells (topology.py:348-352) */
+    struct {
+        int len, nwin, exact;
+        int16_t win[MAXW][5];
+        int16_t before[MAXW], after[MAXW];       /* extension cells (topology.py:348-352) */
+    } lt[2];                                      /* one table per line end rule */
+    int nlt;
     /* custodial walk directions: each axis then its inverse (exprs.py:244-251) */
     int ncust;
     int cust_dir[8];
@@ -132,25 +135,52 @@ static int ray_len(const orc_game *g, int d) {
     return best;
 }
 
-static void build_lines(orc_game *g, int len) {
-    /* orientation "any" on grids: right, down, down_right, down_left
-       (topology.py:96-103); windows enumerated per axis, per start cell */
+/* hexagon boards (topology.py:134-150): axial (q, r), rows r = -R..R, cells
+   row-major; directions left, right, up_left, up_right, down_left, down_right */
+static const int HEXA_D[6][2] = {{-1, 0}, {1, 0}, {0, -1}, {1, -1}, {-1, 1}, {0, 1}};
+
+static void build_hexagon(orc_game *g, int diameter) {
+    int R = (diameter - 1) / 2, n = 0;
+    static int qs[MAXC], rs[MAXC];
+    g->family = FAM_HEXAGON; g->rows = g->cols = diameter; g->ndirs = 6;
+    for (int r = -R; r <= R; r++) {
+        int lo = -R > -R - r ? -R : -R - r, hi = R < R - r ? R : R - r;
+        for (int q = lo; q <= hi; q++) { qs[n] = q; rs[n] = r; n++; }
+    }
+    g->C = n;
+    for (int d = 0; d < 6; d++) {
+        for (int i = 0; i <= n; i++) g->nbr[d][i] = (int16_t)n;
+        for (int i = 0; i < n; i++)
+            for (int j = 0; j < n; j++)
+                if (qs[j] == qs[i] + HEXA_D[d][0] && rs[j] == rs[i] + HEXA_D[d][1]) g->nbr[d][i] = (int16_t)j;
+    }
+}
+
+/* windows of `len` cells along each axis of orientation "any", per start
+   cell (topology.py:319-359): grids right, down, down_right, down_left;
+   hexagons right, down_left, down_right.  Returns the table index. */
+static int build_lines(orc_game *g, int len, int exact) {
     static const char *axes[4] = {"right", "down", "down_right", "down_left"};
     static const char *inv_axes[4] = {"left", "up", "up_left", "up_right"};
-    g->line_len = len; g->nwin = 0;
-    for (int a = 0; a < 4; a++) {
-        int d = dir_index_grid(axes[a]);
+    static const int hex_axes[3] = {1, 4, 5}, hex_inv[3] = {0, 3, 2};
+    int t = g->nlt++;
+    g->lt[t].len = len; g->lt[t].nwin = 0; g->lt[t].exact = exact;
+    int naxes = g->family == FAM_HEXAGON ? 3 : 4;
+    for (int a = 0; a < naxes; a++) {
+        int d = g->family == FAM_HEXAGON ? hex_axes[a] : dir_index_grid(axes[a]);
+        int di = g->family == FAM_HEXAGON ? hex_inv[a] : dir_index_grid(inv_axes[a]);
         for (int s = 0; s < g->C; s++) {
             int cells[8], k = 1; cells[0] = s;
             while (k < len && g->nbr[d][cells[k - 1]] != g->C) { cells[k] = g->nbr[d][cells[k - 1]]; k++; }
             if (k == len) {
-                for (int j = 0; j < len; j++) g->win[g->nwin][j] = (int16_t)cells[j];
-                g->win_before[g->nwin] = g->nbr[dir_index_grid(inv_axes[a])][s];
-                g->win_after[g->nwin] = g->nbr[d][cells[len - 1]];
-                g->nwin++;
+                int w = g->lt[t].nwin++;
+                for (int j = 0; j < len; j++) g->lt[t].win[w][j] = (int16_t)cells[j];
+                g->lt[t].before[w] = g->nbr[di][s];
+                g->lt[t].after[w] = g->nbr[d][cells[len - 1]];
             }
         }
     }
+    return t;
 }
 
 static void build_custodial(orc_game *g) {
@@ -172,16 +202,16 @@ orc_game *orc_game_new(const char *name) {
     orc_game *g = (orc_game *)calloc(1, sizeof(orc_game));
     g->nphase = 1; g->olen[0] = 2; g->order[0][0] = 0; g->order[0][1] = 1;
     if (!strcmp(name, "tic_tac_toe")) {                 /* games/tic_tac_toe.ldx */
-        g->game = 0; build_topology(g, FAM_GRID, 3, 3); build_lines(g, 3);
+        g->game = 0; build_topology(g, FAM_GRID, 3, 3); build_lines(g, 3, 0);
         g->nend = 2;
-        g->end_kind[0] = END_LINE; g->end_arg[0] = 3; g->end_anch[0] = 0; g->end_res[0] = RES_MOVER_WIN;
+        g->end_kind[0] = END_LINE; g->end_arg[0] = 0; g->end_anch[0] = 0; g->end_res[0] = RES_MOVER_WIN;
         g->end_kind[1] = END_FULL; g->end_res[1] = RES_DRAW;
     } else if (!strcmp(name, "connect_four")) {         /* games/connect_four.ldx */
-        g->game = 1; build_topology(g, FAM_GRID, 6, 7); build_lines(g, 4);
+        g->game = 1; build_topology(g, FAM_GRID, 6, 7); build_lines(g, 4, 0);
         g->dest[0] = DEST_C4; g->L_last = 1;
         g->nend = 2;
         /* 69 windows * 4 > 128: anchored at last_dest (compiler.py:28,122-135) */
-        g->end_kind[0] = END_LINE; g->end_arg[0] = 4; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
+        g->end_kind[0] = END_LINE; g->end_arg[0] = 0; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
         g->end_kind[1] = END_FULL; g->end_res[1] = RES_DRAW;
     } else if (!strcmp(name, "hex")) {                  /* games/hex.ldx */
         g->game = 2; build_topology(g, FAM_HEXRECT, 11, 11);
@@ -196,22 +226,29 @@ orc_game *orc_game_new(const char *name) {
         g->nend = 1;
         g->end_kind[0] = END_PASSED_BOTH; g->end_res[0] = RES_BY_SCORE;
     } else if (!strcmp(name, "pente")) {                /* games/pente.ldx */
-        g->game = 4; build_topology(g, FAM_GRID, 19, 19); build_lines(g, 5); build_custodial(g);
+        g->game = 4; build_topology(g, FAM_GRID, 19, 19); build_lines(g, 5, 0); build_custodial(g);
         g->nphase = 2;
         g->once[0] = 1; g->olen[0] = 1; g->order[0][0] = 0; g->dest[0] = DEST_CENTER;
         g->once[1] = 0; g->olen[1] = 2; g->order[1][0] = 1; g->order[1][1] = 0; g->dest[1] = DEST_EMPTY;
         g->effect[1] = EFF_PENTE;
         g->L_scores = 1; g->L_last = 1; g->L_phase = 1;
         g->nend = 3;
-        g->end_kind[0] = END_LINE; g->end_arg[0] = 5; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
+        g->end_kind[0] = END_LINE; g->end_arg[0] = 0; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
         g->end_kind[1] = END_SCORE_GE; g->end_arg[1] = 10; g->end_res[1] = RES_MOVER_WIN;
         g->end_kind[2] = END_FULL; g->end_res[2] = RES_DRAW;
     } else if (!strcmp(name, "gomoku")) {              /* corpus: games/gomoku.ldx */
-        g->game = 5; build_topology(g, FAM_GRID, 15, 15); build_lines(g, 5);
-        g->line_exact = 1; g->L_last = 1;
+        g->game = 5; build_topology(g, FAM_GRID, 15, 15); build_lines(g, 5, 1);
+        g->L_last = 1;
         g->nend = 2;
-        g->end_kind[0] = END_LINE; g->end_arg[0] = 5; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
+        g->end_kind[0] = END_LINE; g->end_arg[0] = 0; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
         g->end_kind[1] = END_FULL; g->end_res[1] = RES_DRAW;
+    } else if (!strcmp(name, "yavalath")) {            /* corpus: games/yavalath.ldx */
+        g->game = 6; build_hexagon(g, 9); build_lines(g, 4, 0); build_lines(g, 3, 0);
+        g->L_last = 1;
+        g->nend = 3;
+        g->end_kind[0] = END_LINE; g->end_arg[0] = 0; g->end_anch[0] = 1; g->end_res[0] = RES_MOVER_WIN;
+        g->end_kind[1] = END_LINE_LOSE; g->end_arg[1] = 1; g->end_anch[1] = 1; g->end_res[1] = RES_MOVER_LOSE;
+        g->end_kind[2] = END_FULL; g->end_res[2] = RES_DRAW;
     } else {
         free(g);
         return NULL;
@@ -341,23 +378,23 @@ static int connected2(const env_t *e, int side, int ea, int eb) {
 }
 
 /* _LineTables.satisfied / compile_line_anchored_exists (exprs.py:433-535) */
-static int line_sat(const env_t *e, int side, int anchored) {
+static int line_sat(const env_t *e, int side, int anchored, int t) {
     const orc_game *g = e->g;
-    int dest = g->C;
+    int dest = g->C, len = g->lt[t].len;
     if (anchored) {
         int ld = e->s->last_dest[e->i];
         if (ld >= 0 && e->s->last_mover[e->i] == side) dest = ld; else return 0;
     }
-    for (int w = 0; w < g->nwin; w++) {
+    for (int w = 0; w < g->lt[t].nwin; w++) {
         int through = !anchored, ok = 1;
-        for (int j = 0; j < g->line_len; j++) through |= g->win[w][j] == dest;
+        for (int j = 0; j < len; j++) through |= g->lt[t].win[w][j] == dest;
         if (!through) continue;
-        for (int j = 0; j < g->line_len && ok; j++) {
-            int c = g->win[w][j];
+        for (int j = 0; j < len && ok; j++) {
+            int c = g->lt[t].win[w][j];
             ok = e->own[c] == side && e->pc[c] == 0;
         }
-        if (ok && g->line_exact) {        /* exprs.py:444-448: extensions not the side's */
-            int b = g->win_before[w], a = g->win_after[w];
+        if (ok && g->lt[t].exact) {       /* exprs.py:444-448: extensions not the side's */
+            int b = g->lt[t].before[w], a = g->lt[t].after[w];
             if (b != g->C && e->own[b] == side && e->pc[b] == 0) ok = 0;
             if (a != g->C && e->own[a] == side && e->pc[a] == 0) ok = 0;
         }
@@ -452,7 +489,8 @@ static int step_one(env_t *e, int64_t action, int verify, uint8_t *scratch) {
     for (int r = 0; r < g->nend; r++) {
         int fired = 0;
         switch (g->end_kind[r]) {
-        case END_LINE: fired = line_sat(e, mover, g->end_anch[r]); break;
+        case END_LINE: fired = line_sat(e, mover, g->end_anch[r], g->end_arg[r]); break;
+        case END_LINE_LOSE: fired = line_sat(e, mover, g->end_anch[r], g->end_arg[r]); break;
         case END_FULL: { fired = 1; for (int c = 0; c < g->C; c++) if (e->own[c] < 0) { fired = 0; break; } } break;
         case END_CONN: fired = mover == g->end_gate[r] && connected2(e, mover, g->end_ea[r], g->end_eb[r]); break;
         case END_PASSED_BOTH: fired = s->pass_streak[i] >= 2; break;
@@ -461,6 +499,7 @@ static int step_one(env_t *e, int64_t action, int verify, uint8_t *scratch) {
         if (fired) {
             int8_t out = 0;
             if (g->end_res[r] == RES_MOVER_WIN) out = (int8_t)(1 + mover);
+            else if (g->end_res[r] == RES_MOVER_LOSE) out = (int8_t)(2 - mover);
             else if (g->end_res[r] == RES_BY_SCORE) {      /* compiler.py:586-591 */
                 int a = s->scores[i * 2], b = s->scores[i * 2 + 1];
                 out = a > b ? 1 : (b > a ? 2 : 0);

@@ -25,7 +25,7 @@ FIELDS = ("board_piece", "board_owner", "current_player", "move_count",
           "last_dest", "last_dest_by_player", "hopped_mask", "captured_mask",
           "promoted_mask", "comp_labels", "phase", "turn_pos")
 
-GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku")
+GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath")
 
 
 class _SoA(ctypes.Structure):

@@ -61,11 +61,20 @@ __device__ __forceinline__ void write_mask_rows(unsigned char* __restrict__ mask
     __shared__ u32 stage[(256 / 32) * 32 * STRIDE];
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     u32* mine = stage + (warp * 32 + lane) * STRIDE;
+    if (G::IDENT) {
 #pragma unroll
-    for (int j = 0; j < NW; j++) {
-        u32 v = j < G::W ? legal.w[j] : 0u;
-        if (G::PASS >= 0 && j == (G::C >> 5) && pass_bit) v |= 1u << (G::C & 31);
-        mine[j] = valid ? v : 0u;
+        for (int j = 0; j < NW; j++) {
+            u32 v = j < G::W ? legal.w[j] : 0u;
+            if (G::PASS >= 0 && j == (G::C >> 5) && pass_bit) v |= 1u << (G::C & 31);
+            mine[j] = valid ? v : 0u;
+        }
+    } else {                                   // embedded layout: compact bits to cell order
+        for (int j = 0; j < NW; j++) mine[j] = 0u;
+        if (valid) {
+            for (int c = 0; c < G::C; c++)
+                if (test(legal, G::cell_bit(c))) mine[c >> 5] |= 1u << (c & 31);
+            if (G::PASS >= 0 && pass_bit) mine[G::C >> 5] |= 1u << (G::C & 31);
+        }
     }
     mine[NW] = 0u;
     __syncwarp();
@@ -169,7 +178,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_sample(const u32* st, i64 B
     if (n == 0) { actions[i] = Game::force_pass(s.phase) ? Game::PASS : -1; return; }
     i64 r = __double2ll_rz(__dmul_rn(u[i], (double)n));
     r = r < (i64)(n - 1) ? r : (i64)(n - 1);
-    actions[i] = lx::select_bit(legal, (int)r);
+    actions[i] = Game::bit_cell(lx::select_bit(legal, (int)r));
 }
 
 // verification pass: *bad = min illegal live row (init to ~0 by the caller)
@@ -431,7 +440,8 @@ extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B
     signed char* own = p.board_owner + i * Game::C;
     signed char* pc = p.board_piece + i * Game::C;
     for (int c = 0; c < Game::C; c++) {
-        const bool a = lx::test(s.own0, c), b = lx::test(s.own1, c);
+        const int cb = Game::cell_bit(c);
+        const bool a = lx::test(s.own0, cb), b = lx::test(s.own1, cb);
         own[c] = a ? 0 : (b ? 1 : -1);
         pc[c] = (a || b) ? 0 : -1;
     }
@@ -469,8 +479,8 @@ extern "C" __global__ void __launch_bounds__(128) lx_import(u32* st, i64 B, LxRe
     s.own1 = lx::bb_zero<Game::W>();
     const signed char* own = p.board_owner + i * Game::C;
     for (int c = 0; c < Game::C; c++) {
-        if (own[c] == 0) lx::setbit(s.own0, c);
-        else if (own[c] == 1) lx::setbit(s.own1, c);
+        if (own[c] == 0) lx::setbit(s.own0, Game::cell_bit(c));
+        else if (own[c] == 1) lx::setbit(s.own1, Game::cell_bit(c));
     }
     s.cur = p.current_player[i];
     s.mc = (u32)p.move_count[i];
@@ -509,8 +519,8 @@ extern "C" __global__ void __launch_bounds__(128) lx_observe(const u32* st, i64 
     unsigned char* out = planes + i * (i64)(3 * Game::C);
     const unsigned char mv = s.cur == player;
     for (int c = 0; c < Game::C; c++) {
-        out[c] = lx::test(me, c);
-        out[Game::C + c] = lx::test(op, c);
+        out[c] = lx::test(me, Game::cell_bit(c));
+        out[Game::C + c] = lx::test(op, Game::cell_bit(c));
         out[2 * Game::C + c] = mv;
     }
 }

@@ -88,7 +88,7 @@ __device__ __forceinline__ int sample_action(const typename G::St& s, u64 smix) 
     const int n = popc(legal);
     if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
     const int r = draw_index(mix64(smix ^ (u64)s.mc), n);
-    return select_bit(legal, r);
+    return G::bit_cell(select_bit(legal, r));
 }
 
 // one ply for a live row (reference compiler.py:456-580, order preserved:
@@ -133,7 +133,7 @@ __device__ __forceinline__ bool action_legal(const typename G::St& s, i64 a) {
     const BB<G::W> legal = G::legal(s);
     if (G::PASS >= 0 && a == G::PASS) return !any(legal) && G::force_pass(s.phase);
     if (a < 0 || a >= G::C) return false;
-    return test(legal, (int)a);
+    return test(legal, G::cell_bit((int)a));
 }
 
 

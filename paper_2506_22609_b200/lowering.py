@@ -52,14 +52,18 @@ class Lowered:
 class _Emitter:
     """Collects constants and helper functions while expressions are built."""
 
-    def __init__(self, board, W):
+    def __init__(self, board, W, bit_of):
         self.board, self.W = board, W
+        self.bit_of = bit_of      # cell id -> bit position
         self.consts = {}          # words tuple -> name
         self.helpers = {}         # name -> code
         self.counter = 0
 
     def const(self, mask):
-        words = _words(mask, self.W)
+        """Constant bitboard from a cell-indexed bool mask."""
+        bits = np.zeros(self.W * 32, dtype=bool)
+        bits[self.bit_of[np.nonzero(np.asarray(mask))[0]]] = True
+        words = _words(bits, self.W)
         if words not in self.consts:
             self.consts[words] = f"K{len(self.consts)}"
         return f"{self.consts[words]}()"
@@ -94,11 +98,23 @@ class GameLowering:
         self.spec = spec
         self.board = Board(spec.equipment.board)
         B = self.board
-        if B.family == "hexagon":
-            _fail("hexagon boards are not lowered yet (rows are not shift-regular)")
         self.C = B.num_cells
-        self.W = (self.C + 31) // 32
-        self.em = _Emitter(B, self.W)
+        # Bit layout.  Row-major boards: bit = cell.  Hexagon boards: rows of
+        # different lengths are embedded in a d x d axial grid (row r, column
+        # q + radius), which makes every direction a constant shift; bit order
+        # stays monotone in cell order, so "r-th set bit" is still the r-th
+        # legal cell (reference mechanics.py:488-492).
+        if B.family == "hexagon":
+            d, rad = B.rows, B.radius
+            self.emb_rows = self.emb_cols = d
+            self.bit_of = np.array([(r + rad) * d + (q + rad) for q, r in B.coords])
+        else:
+            self.emb_rows, self.emb_cols = B.rows, B.cols
+            self.bit_of = np.arange(self.C)
+        self.NB = self.emb_rows * self.emb_cols
+        self.ident = bool((self.bit_of == np.arange(self.C)).all())
+        self.W = (self.NB + 31) // 32
+        self.em = _Emitter(B, self.W, self.bit_of)
         self.piece_ids = {p.name: i for i, p in enumerate(spec.equipment.pieces)}
         if len(self.piece_ids) != 1:
             _fail("only single-piece-type games are lowered (board_piece is implied)")
@@ -117,9 +133,10 @@ class GameLowering:
     # ------------------------------------------------------------ geometry
 
     def _check_shift(self, d):
-        """Prove nbr_d(x) == x + S for every x with a d-neighbour."""
+        """Prove bit(nbr_d(x)) == bit(x) + S for every x with a d-neighbour."""
         nt = self.board.neighbors[d]
-        deltas = {int(nt[x]) - x for x in range(self.C) if nt[x] != self.C}
+        bo = self.bit_of
+        deltas = {int(bo[nt[x]]) - int(bo[x]) for x in range(self.C) if nt[x] != self.C}
         if len(deltas) > 1:
             _fail(f"direction {d} is not a constant cell shift on this board")
         return deltas.pop() if deltas else 0
@@ -346,16 +363,37 @@ class GameLowering:
         through the shared-memory mirror instead of whole-board shifts."""
         return self.W >= 6
 
+    def _bitmap_code(self):
+        """cell id <-> bit position maps (identity on row-major boards)."""
+        if self.ident:
+            return ("    static __device__ __forceinline__ int cell_bit(int c) { return c; }\n"
+                    "    static __device__ __forceinline__ int bit_cell(int b) { return b; }")
+        cell_of = np.full(self.NB, -1, dtype=np.int64)
+        cell_of[self.bit_of] = np.arange(self.C)
+        cb = ", ".join(str(int(x)) for x in self.bit_of)
+        bc = ", ".join(str(int(x)) for x in cell_of)
+        return (f"    static __device__ __forceinline__ int cell_bit(int c) {{\n"
+                f"        static __device__ const short t[{self.C}] = {{{cb}}};\n"
+                f"        return t[c];\n    }}\n"
+                f"    static __device__ __forceinline__ int bit_cell(int b) {{\n"
+                f"        static __device__ const short t[{self.NB}] = {{{bc}}};\n"
+                f"        return t[b];\n    }}")
+
     def _max_steps(self, d):
-        """Expression: how many steps along d stay on the board from (r, col)."""
-        dr, dc = self.board.delta(d)
+        """Expression: how many steps along d stay inside the bit grid from
+        (r, col) of the anchor's bit (embedded grid for hexagons: cells outside
+        the hexagon are padding bits that are never set)."""
+        S = self._shift[d]
+        cols = self.emb_cols
+        dr = (S + cols // 2) // cols if S >= 0 else -((-S + cols // 2) // cols)
+        dc = S - dr * cols
         terms = []
         if dr > 0:
-            terms.append(f"({self.board.rows - 1} - r) / {dr}")
+            terms.append(f"({self.emb_rows - 1} - r) / {dr}")
         elif dr < 0:
             terms.append(f"r / {-dr}")
         if dc > 0:
-            terms.append(f"({self.board.cols - 1} - col) / {dc}")
+            terms.append(f"({cols - 1} - col) / {dc}")
         elif dc < 0:
             terms.append(f"col / {-dc}")
         if not terms:
@@ -391,9 +429,9 @@ class GameLowering:
         BBW out = lx::bb_zero<W>();
         if (!(s.last_dest >= 0 && s.last_mover == side)) return out;
         M::store(s.own0, s.own1);
-        const int c = s.last_dest;
-        const int r = c / {self.board.cols};
-        const int col = c - r * {self.board.cols};
+        const int c = cell_bit(s.last_dest);
+        const int r = c / {self.emb_cols};
+        const int col = c - r * {self.emb_cols};
 {body}
         return out;
     }}""")
@@ -416,7 +454,7 @@ class GameLowering:
             for c in range(C):
                 m, x = 0, int(nt[c])
                 while x != C:
-                    m |= 1 << x
+                    m |= 1 << int(self.bit_of[x])
                     x = int(nt[x])
                 vals.append(m)
             rows.append("{" + ", ".join(f"0x{v:016x}ull" for v in vals) + "}")
@@ -482,11 +520,11 @@ class GameLowering:
         typedef lx::Mirror<W> M;
         const int side = {side};
         if (!(s.last_dest >= 0 && s.last_mover == mover)) return false;
-        const int c = s.last_dest;
+        const int c = cell_bit(s.last_dest);
         M::store(s.own0, s.own1);
         if (!M::probe(side, c)) return false;
-        const int r = c / {self.board.cols};
-        const int col = c - r * {self.board.cols};
+        const int r = c / {self.emb_cols};
+        const int col = c - r * {self.emb_cols};
         int run = 0;
 {body}
         return false;
@@ -538,7 +576,7 @@ class GameLowering:
         const BBW tgt = side ? s.own0 : s.own1;
         BBW out = lx::bb_zero<W>();
         if (!(s.last_dest >= 0 && s.last_mover == side)) return out;
-        const BBW a = lx::onehot<W>(s.last_dest);
+        const BBW a = lx::onehot<W>(cell_bit(s.last_dest));
 {body}
         return out;
     }}"""
@@ -667,7 +705,7 @@ class GameLowering:
         body = "\n".join(lines)
         self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const St& s, int mover, const BBW& b) {{
         if (!(s.last_dest >= 0 && s.last_mover == mover)) return false;
-        const BBW a = lx::onehot<W>(s.last_dest);
+        const BBW a = lx::onehot<W>(cell_bit(s.last_dest));
         if (!lx::any(a & b)) return false;
         bool hit = false;
 {body}
@@ -853,7 +891,7 @@ class GameLowering:
                 store = self._slot_set(k, "R")
                 cond = f"side == {sd}"
             out.append(f"""{head}
-            const BBW a = lx::onehot<W>(cell);
+            const BBW a = lx::onehot<W>(cell_bit(cell));
             if (({cond}) && lx::any((a & t0) | (({dil_a}) & R))) {{
                 const BBW mine = side ? s.own1 : s.own0;
                 const BBW free_ = lx::andnot(mine, R);
@@ -1069,12 +1107,13 @@ class GameLowering:
             dil = " | ".join(self.nb(d, "f") for d in plan)
             conn = f"""        const BBW occ[2] = {{s.own0, s.own1}};
         BBW done = lx::bb_zero<W>();
-        for (int c = 0; c < C; c++) {{
-            const bool o0 = lx::test(s.own0, c), o1 = lx::test(s.own1, c);
+        for (int c = 0; c < C; c++) {{                    // ascending cell id = min label
+            const int cb = cell_bit(c);
+            const bool o0 = lx::test(s.own0, cb), o1 = lx::test(s.own1, cb);
             if (!o0 && !o1) {{ out[c] = -1; continue; }}
-            if (lx::test(done, c)) continue;
+            if (lx::test(done, cb)) continue;
             const BBW mine = o0 ? occ[0] : occ[1];
-            BBW f = lx::onehot<W>(c);
+            BBW f = lx::onehot<W>(cb);
             while (true) {{
                 const BBW g = (f | {dil}) & mine;
                 if (lx::equal(g, f)) break;
@@ -1084,7 +1123,11 @@ class GameLowering:
 #pragma unroll
             for (int i = 0; i < W; i++) {{
                 u32 bits = f.w[i];
-                while (bits) {{ const int b = __ffs(bits) - 1; out[32 * i + b] = (short)c; bits &= bits - 1u; }}
+                while (bits) {{
+                    const int b = __ffs(bits) - 1;
+                    out[bit_cell(32 * i + b)] = (short)c;
+                    bits &= bits - 1u;
+                }}
             }}
         }}"""
         fp = " || ".join(f"phase == {p}" for p in fp_cases) or "false"
@@ -1115,8 +1158,11 @@ struct Game {{
     static constexpr int FIRST_PLAYER = {phases[0].order[0]}, NPHASE = {nph};
     static constexpr bool L_SCORES = {str(L['scores']).lower()}, L_PASSING = {str(L['passing']).lower()};
     static constexpr bool L_LAST = {str(L['last_action']).lower()}, L_PHASE = {str(L['phase']).lower()};
+    static constexpr bool IDENT = {str(self.ident).lower()};   // bit position == cell id
+    static constexpr int NB = {self.NB};                       // bit slots (embedded grid)
     typedef lx::BB<W> BBW;
     typedef lx::State<W, NX> St;
+{self._bitmap_code()}
 @@CONSTS@@
 @@HELPERS@@
     static __device__ __forceinline__ void start(St& s) {{
@@ -1136,7 +1182,7 @@ struct Game {{
     static __device__ __forceinline__ bool force_pass(int phase) {{ return {fp}; }}
     static __device__ __forceinline__ void write_place(St& s, int cell, int mover, int phase) {{
         const int side = {owner};
-        const BBW oh = lx::onehot<W>(cell);          // branchless: no warp split on the mover
+        const BBW oh = lx::onehot<W>(cell_bit(cell));   // branchless: no warp split on the mover
         s.own0 = lx::sel(side != 0, s.own0 | oh, s.own0);
         s.own1 = lx::sel(side != 0, s.own1, s.own1 | oh);
         s.last_kind = 0; s.last_dest = cell; s.last_mover = side;

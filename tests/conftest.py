@@ -10,7 +10,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku")
+GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath")
 
 
 def pytest_configure(config):

@@ -29,7 +29,8 @@ struct RefOut {
 
 static void export_one(const St& s, int64_t i, const RefOut* p) {
     for (int c = 0; c < Game::C; c++) {
-        const bool a = lx::test(s.own0, c), b = lx::test(s.own1, c);
+        const int cb = Game::cell_bit(c);
+        const bool a = lx::test(s.own0, cb), b = lx::test(s.own1, cb);
         p->board_owner[i * Game::C + c] = a ? 0 : (b ? 1 : -1);
         p->board_piece[i * Game::C + c] = (a || b) ? 0 : -1;
     }
@@ -90,7 +91,7 @@ int sim_masks(uint64_t seed, int max_plies, uint8_t* masks, int64_t* actions) {
     int t = 0;
     for (; t < max_plies && !s.term; t++) {
         lx::BB<Game::W> legal = Game::legal(s);
-        for (int c = 0; c < Game::C; c++) masks[t * Game::A + c] = lx::test(legal, c);
+        for (int c = 0; c < Game::C; c++) masks[t * Game::A + c] = lx::test(legal, Game::cell_bit(c));
         if (Game::PASS >= 0) masks[t * Game::A + Game::C] = !lx::any(legal) && Game::force_pass(s.phase);
         const int a = lx::sample_action<Game>(s, smix);
         actions[t] = a;

@@ -98,7 +98,7 @@ def test_lowering_shift_proof_and_source(name):
         nt = gl.board.neighbors[d]
         for x in range(gl.C):
             if nt[x] != gl.C:
-                assert nt[x] == x + S
+                assert gl.bit_of[nt[x]] == gl.bit_of[x] + S
     src = gl.lower().source
     assert "struct Game" in src and '#include "lx_kernels.cuh"' in src
 
@@ -114,9 +114,12 @@ def test_lowering_words_bit_order():
     ("""(game "Move" (players 2) (equipment (board (square 4)) (pieces ("p" both)))
         (rules (start (place "p" P1 (0))) (play (repeat (P1 P2) (move (step "p"))))
         (end (if (full_board) (draw)))))""", "movement"),
-    ("""(game "Hexagon" (players 2) (equipment (board (hexagon 5)) (pieces ("s" both)))
+    ("""(game "Two" (players 2) (equipment (board (square 5)) (pieces ("a" both) ("b" both)))
+        (rules (play (repeat (P1 P2) (place "a" (destination (empty)))))
+        (end (if (full_board) (draw)))))""", "two piece types"),
+    ("""(game "Pat" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
         (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
-        (end (if (full_board) (draw)))))""", "hexagon"),
+        (end (if (pattern "s" (2 (0 1 2 3))) (mover win)))))""", "pattern"),
 ])
 def test_unsupported_raises_compile_error(text, what):
     with pytest.raises(CompileError) as e:

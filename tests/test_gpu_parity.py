@@ -28,7 +28,7 @@ def game(name):
 
 
 ORACLE_B = {"tic_tac_toe": 65536, "connect_four": 16384, "hex": 2048, "reversi": 4096,
-            "pente": 512, "gomoku": 1024}
+            "pente": 512, "gomoku": 1024, "yavalath": 8192}
 
 
 @pytest.mark.parametrize("name", GAMES)
