@@ -349,7 +349,8 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
                    "issue": {"achieved": iss / 1e9, "peak": peak_issue / 1e9,
                              "frac": iss / peak_issue},
                    "ncu_alu_pipe_pct": prof.get("alu_pipe_elapsed_pct"),
-                   "inst_source": prof.get("source"), "cubin_key": prof.get("cubin_key")})
+                   "inst_source": prof.get("source"), "cubin_key": prof.get("cubin_key"),
+                   "profile_stale": prof.get("stale", False)})
     out["roofline"] = rl
 
     # ---- HBM-bound per-ply step kernel (PGX-style API path)
@@ -427,8 +428,9 @@ def load_profile(game):
             prof = json.load(f)
     except Exception:
         return None
-    if prof.get("cubin_key") and prof["cubin_key"] != game.lowered_key():
-        return None
+    # a capture of an older build of this game is still the best available
+    # count; say so instead of dropping the roofline
+    prof["stale"] = bool(prof.get("cubin_key")) and prof["cubin_key"] != game.lowered_key()
     return prof
 
 
