@@ -63,6 +63,7 @@ typedef struct {
     int8_t *last_mover, *last_kind;
     int16_t *last_source, *last_dest, *last_dest_by_player, *comp_labels;
     int8_t *phase;
+    int16_t *must_move;         /* movement games with same-piece extra turns */
 } lx_ref_state;
 
 int lx_version(void);

@@ -31,11 +31,14 @@ from boardlang.parser import parse_game  # noqa: E402
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
 GAMES_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                          "paper_2506_22609_b200", "games")
-GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath")
+GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath",
+         "english_draughts", "dai_hasami_shogi", "wolf_and_sheep", "gridworld")
 PLAYOUT = {"tic_tac_toe": [(1024, 0), (512, 99)], "connect_four": [(256, 0), (256, 5)],
            "hex": [(64, 0), (48, 21)], "reversi": [(64, 0), (64, 12)],
            "pente": [(32, 0), (24, 3)], "gomoku": [(32, 0), (24, 5)],
-           "yavalath": [(128, 0), (96, 9)]}
+           "yavalath": [(128, 0), (96, 9)],
+           "english_draughts": [(64, 0), (48, 7)], "dai_hasami_shogi": [(32, 0), (24, 4)],
+           "wolf_and_sheep": [(128, 0), (64, 8)], "gridworld": [(256, 0), (128, 3)]}
 
 
 def state_arrays(st, prefix):
@@ -133,6 +136,45 @@ def main():
                                "p2": int((f.outcome == 2).sum()),
                                "draw": int((f.outcome == 0).sum()),
                                "digest": f.digest()}
+    # (6) movement transcripts (tests/test_acceptance.py:148-178,
+    #     test_engine.py:159-196, test_compiler.py:198-204)
+    dr_text = open(os.path.join(GAMES_DIR, "english_draughts.ldx")).read()
+    dr = boardlang.load_game(dr_text)
+    C = 64
+    s = dr.init(1)
+    for a in (44 * C + 35, 21 * C + 30, 35 * C + 26):
+        s = dr.step(s, np.array([a]))
+    kat["draughts_forced"] = {"actions": [44 * C + 35, 21 * C + 30, 35 * C + 26],
+                              "legal": np.nonzero(dr.legal_mask(s)[0])[0].tolist(),
+                              "digest": s.digest()}
+    s = dr.step(s, np.array([17 * C + 35]))
+    kat["draughts_forced"]["after_capture"] = {"digest": s.digest(),
+                                               "current_player": int(s.current_player[0])}
+    drill_text = dr_text.replace("(40 42 44 46 49 51 53 55 56 58 60 62)", "(36 58)").replace(
+        "(1 3 5 7 8 10 12 14 17 19 21 23)", "(27 9 14)")
+    g = boardlang.load_game(drill_text)
+    s = g.init(1)
+    drill = {"start_legal": np.nonzero(g.legal_mask(s)[0])[0].tolist()}
+    s = g.step(s, np.array([36 * C + 18]))
+    drill["after1"] = {"current_player": int(s.current_player[0]),
+                       "must_move": int(s.must_move[0]),
+                       "legal": np.nonzero(g.legal_mask(s)[0])[0].tolist(), "digest": s.digest()}
+    s = g.step(s, np.array([18 * C + 0]))
+    drill["after2"] = {"current_player": int(s.current_player[0]),
+                       "piece0": int(s.board_piece[0, 0]), "digest": s.digest()}
+    drill["text_replace"] = [["(40 42 44 46 49 51 53 55 56 58 60 62)", "(36 58)"],
+                             ["(1 3 5 7 8 10 12 14 17 19 21 23)", "(27 9 14)"]]
+    kat["draughts_drill"] = drill
+    gw = boardlang.load_game(open(os.path.join(GAMES_DIR, "gridworld.ldx")).read())
+    s = gw.init(1)
+    grid = {"directions": list(gw.codec.directions),
+            "initial_legal": np.nonzero(gw.legal_mask(s)[0])[0].tolist()}
+    right, down = gw.codec.encode_direction("right"), gw.codec.encode_direction("down")
+    s = gw.step(s, np.array([right]))
+    s = gw.step(s, np.array([down]))
+    grid["right_down"] = {"actions": [int(right), int(down)], "digest": s.digest(),
+                          "outcome": int(s.outcome[0]), "terminated": bool(s.terminated[0])}
+    kat["gridworld"] = grid
     meta["kat"] = kat
     with open(os.path.join(OUT, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=0, sort_keys=True)

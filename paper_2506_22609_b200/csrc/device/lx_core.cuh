@@ -251,6 +251,8 @@ struct State {
     u32 mc;
     int cur, term, trunc, outcome, phase, last_mover, last_kind, last_dest;
     int pass_streak, pf0, pf1, ldbp0, ldbp1, sc0, sc1;
+    int last_source, must_move;  // movement games (reference state.py:96-104)
+    int ovr, samep;              // transient per ply: extra-turn player, same-piece flag
     u64 seed;
 };
 

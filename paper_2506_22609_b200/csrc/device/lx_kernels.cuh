@@ -9,8 +9,9 @@
 // words, stored quad-major -- quad q of env i lives at uint4 index q*B + i --
 // so a warp moves 512 contiguous bytes per 128-bit load.  Word map:
 //   [0, W)        P1 stones        [W, 2W)       P2 stones
-//   [2W, 2W+NX)   rule-private words (e.g. edge-connected stone sets)
-//   then 7 meta words (see pack/unpack below), zero padding to NQ*4.
+//   [2W, 2W+NX)   piece-type planes (games with several piece types), then
+//                 rule-private words (e.g. edge-connected stone sets)
+//   then 8 meta words (see pack/unpack in lx_rules.cuh), zero padding to NQ*4.
 #pragma once
 
 #include "lx_rules.cuh"
@@ -108,6 +109,33 @@ __device__ __forceinline__ void write_mask_rows(unsigned char* __restrict__ mask
     __syncwarp();
 }
 
+// Movement / gridworld masks (A = C*C or #directions): the warp zeroes its 32
+// contiguous rows with 16-byte stores, then each lane sets the bytes of its
+// own legal actions (a few dozen per row).  Every lane of the warp must call.
+template <class G>
+__device__ __forceinline__ void write_mask_moves(unsigned char* __restrict__ mask, i64 B, i64 i,
+                                                 bool valid, const typename G::St& s, bool live,
+                                                 bool pass_bit) {
+    constexpr int A = G::A;
+    const unsigned lane = threadIdx.x & 31u;
+    const i64 i0 = i - lane;
+    const i64 left = B - i0;
+    const int nrows = left < 32 ? (int)left : 32;
+    const i64 bytes = (i64)nrows * A;
+    unsigned char* base = mask + i0 * (i64)A;
+    const i64 n16 = bytes >> 4;
+    uint4* b16 = reinterpret_cast<uint4*>(base);
+    for (i64 q = lane; q < n16; q += 32) b16[q] = make_uint4(0u, 0u, 0u, 0u);
+    for (i64 p = (n16 << 4) + lane; p < bytes; p += 32) base[p] = 0;
+    __syncwarp();
+    if (valid) {
+        unsigned char* row = mask + i * (i64)A;
+        if (live) G::enum_moves(s, [&](int a) { row[a] = 1; });
+        if (G::PASS >= 0 && pass_bit) row[G::PASS] = 1;
+    }
+    __syncwarp();
+}
+
 }  // namespace lx
 
 
@@ -132,6 +160,7 @@ struct LxRefPtrs {               // reference GameState field pointers (state.py
     short* last_dest_by_player;  // (B, 2) int16
     short* comp_labels;          // (B, 1, C) int16     or null
     signed char* phase;          // (B,) int8           or null
+    short* must_move;            // (B,) int16          or null
 };
 
 extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const u64* seeds,
@@ -151,17 +180,30 @@ extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
     const i64 i = lx::gtid();
     if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
     const bool valid = i < B;
-    lx::BB<Game::W> legal = lx::bb_zero<Game::W>();
     bool pass_only = false;
-    if (valid) {
+    if constexpr (Game::MECH == 0) {
+        lx::BB<Game::W> legal = lx::bb_zero<Game::W>();
+        if (valid) {
+            Game::St s;
+            lx::load_state<Game>(s, st, B, i);
+            if (!s.term) legal = Game::legal(s);
+            const int n = lx::popc(legal);
+            pass_only = !s.term && n == 0 && Game::force_pass(s.phase);
+            if (counts) counts[i] = s.term ? 0 : (pass_only ? 1 : n);
+        }
+        if (mask) lx::write_mask_rows<Game>(mask, B, i, valid, legal, pass_only);
+    } else {
         Game::St s;
-        lx::load_state<Game>(s, st, B, i);
-        if (!s.term) legal = Game::legal(s);
-        const int n = lx::popc(legal);
-        pass_only = !s.term && n == 0 && Game::force_pass(s.phase);
-        if (counts) counts[i] = s.term ? 0 : (pass_only ? 1 : n);
+        bool live = false;
+        if (valid) {
+            lx::load_state<Game>(s, st, B, i);
+            live = !s.term;
+            const int n = live ? lx::legal_count<Game>(s) : 0;
+            pass_only = live && n == 0 && Game::force_pass(s.phase);
+            if (counts) counts[i] = !live ? 0 : (pass_only ? 1 : n);
+        }
+        if (mask) lx::write_mask_moves<Game>(mask, B, i, valid, s, live, pass_only);
     }
-    if (mask) lx::write_mask_rows<Game>(mask, B, i, valid, legal, pass_only);
 }
 
 // sampled action per row from u (when given) or from the row's own stream
@@ -173,12 +215,22 @@ extern "C" __global__ void __launch_bounds__(256) lx_sample(const u32* st, i64 B
     lx::load_state<Game>(s, st, B, i);
     if (s.term) { actions[i] = -1; return; }
     if (!u) { actions[i] = lx::sample_action<Game>(s, lx::seed_mix(s.seed)); return; }
-    const lx::BB<Game::W> legal = Game::legal(s);
-    const int n = lx::popc(legal);
-    if (n == 0) { actions[i] = Game::force_pass(s.phase) ? Game::PASS : -1; return; }
-    i64 r = __double2ll_rz(__dmul_rn(u[i], (double)n));
-    r = r < (i64)(n - 1) ? r : (i64)(n - 1);
-    actions[i] = Game::bit_cell(lx::select_bit(legal, (int)r));
+    if constexpr (Game::MECH == 0) {
+        const lx::BB<Game::W> legal = Game::legal(s);
+        const int n = lx::popc(legal);
+        if (n == 0) { actions[i] = Game::force_pass(s.phase) ? Game::PASS : -1; return; }
+        i64 r = __double2ll_rz(__dmul_rn(u[i], (double)n));
+        r = r < (i64)(n - 1) ? r : (i64)(n - 1);
+        actions[i] = Game::bit_cell(lx::select_bit(legal, (int)r));
+    } else {
+        int tot[Game::NG];
+        const int n = Game::count_moves(s, tot);
+        if (n == 0) { actions[i] = Game::force_pass(s.phase) ? Game::PASS : -1; return; }
+        i64 r = __double2ll_rz(__dmul_rn(u[i], (double)n));
+        r = r < (i64)(n - 1) ? r : (i64)(n - 1);
+        int hint;
+        actions[i] = Game::select_move(s, (int)r, tot, hint);
+    }
 }
 
 // verification pass: *bad = min illegal live row (init to ~0 by the caller)
@@ -216,10 +268,11 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
     Game::St s;
     lx::load_state<Game>(s, st, B, i);
     if (s.term || (int)s.mc >= max_turns) { if (actions_out) actions_out[i] = -1; return; }
-    const int a = lx::sample_action<Game>(s, lx::seed_mix(s.seed));
+    int hint;
+    const int a = lx::sample_action<Game>(s, lx::seed_mix(s.seed), hint);
     if (actions_out) actions_out[i] = a;
     if (a < 0) return;
-    lx::apply_step<Game>(s, a);
+    lx::apply_step<Game>(s, a, hint);
     lx::store_state<Game>(s, st, B, i);
 }
 
@@ -349,13 +402,14 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
         }
         if (!__any_sync(FULL, active)) break;
         if (playing) {
-            const int a = lx::sample_action<Game>(s, smix);
+            int hint;
+            const int a = lx::sample_action<Game>(s, smix, hint);
             if (a < 0) {
                 atomicMin(stuck, (u64)idx);
                 playing = false;
                 pending = true;
             } else {
-                lx::apply_step<Game>(s, a);
+                lx::apply_step<Game>(s, a, hint);
                 n_steps++;
                 if (s.term || (int)s.mc >= max_turns) {
                     playing = false;
@@ -401,9 +455,9 @@ extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, co
     if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
     const bool valid = i < B;
     lx::BB<Game::W> legal = lx::bb_zero<Game::W>();
-    bool pass_only = false;
+    bool pass_only = false, live = false;
+    Game::St s;
     if (valid) {
-        Game::St s;
         lx::load_state<Game>(s, st, B, i);
         const bool was = s.term;
         float r0 = 0.f, r1 = 0.f;
@@ -425,10 +479,18 @@ extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, co
         if (terminated) terminated[i] = (unsigned char)s.term;
         if (truncated) truncated[i] = (unsigned char)s.trunc;
         if (player) player[i] = s.cur;
-        if (mask && !s.term) legal = Game::legal(s);
-        pass_only = !s.term && !lx::any(legal) && Game::force_pass(s.phase);
+        live = !s.term;
+        if constexpr (Game::MECH == 0) {
+            if (mask && live) legal = Game::legal(s);
+            pass_only = live && !lx::any(legal) && Game::force_pass(s.phase);
+        } else {
+            if (mask && live) pass_only = lx::legal_count<Game>(s) == 0 && Game::force_pass(s.phase);
+        }
     }
-    if (mask) lx::write_mask_rows<Game>(mask, B, i, valid, legal, pass_only);
+    if (mask) {
+        if constexpr (Game::MECH == 0) lx::write_mask_rows<Game>(mask, B, i, valid, legal, pass_only);
+        else lx::write_mask_moves<Game>(mask, B, i, valid, s, live, pass_only);
+    }
 }
 
 // device state -> reference GameState SoA (state.py:78-130)
@@ -443,7 +505,7 @@ extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B
         const int cb = Game::cell_bit(c);
         const bool a = lx::test(s.own0, cb), b = lx::test(s.own1, cb);
         own[c] = a ? 0 : (b ? 1 : -1);
-        pc[c] = (a || b) ? 0 : -1;
+        pc[c] = (a || b) ? (signed char)Game::piece_at(s, cb) : (signed char)-1;
     }
     p.current_player[i] = (signed char)s.cur;
     p.move_count[i] = (int)s.mc;
@@ -460,13 +522,14 @@ extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B
     if (p.last_mover) {
         p.last_mover[i] = (signed char)s.last_mover;
         p.last_kind[i] = (signed char)s.last_kind;
-        p.last_source[i] = -1;
+        p.last_source[i] = (short)s.last_source;
         p.last_dest[i] = (short)s.last_dest;
         p.last_dest_by_player[2 * i] = (short)s.ldbp0;
         p.last_dest_by_player[2 * i + 1] = (short)s.ldbp1;
     }
     if (p.comp_labels) Game::labels(s, p.comp_labels + i * Game::C);
     if (p.phase) p.phase[i] = (signed char)s.phase;
+    if (p.must_move) p.must_move[i] = (short)s.must_move;
 }
 
 // reference GameState SoA -> device state (inverse of lx_export)
@@ -478,9 +541,12 @@ extern "C" __global__ void __launch_bounds__(128) lx_import(u32* st, i64 B, LxRe
     s.own0 = lx::bb_zero<Game::W>();
     s.own1 = lx::bb_zero<Game::W>();
     const signed char* own = p.board_owner + i * Game::C;
+    const signed char* pc = p.board_piece + i * Game::C;
+    Game::clear_types(s);
     for (int c = 0; c < Game::C; c++) {
         if (own[c] == 0) lx::setbit(s.own0, Game::cell_bit(c));
         else if (own[c] == 1) lx::setbit(s.own1, Game::cell_bit(c));
+        if (own[c] >= 0) Game::set_piece(s, Game::cell_bit(c), pc[c]);
     }
     s.cur = p.current_player[i];
     s.mc = (u32)p.move_count[i];
@@ -497,17 +563,20 @@ extern "C" __global__ void __launch_bounds__(128) lx_import(u32* st, i64 B, LxRe
     if (p.last_mover) {
         s.last_mover = p.last_mover[i];
         s.last_kind = p.last_kind[i];
+        s.last_source = p.last_source[i];
         s.last_dest = p.last_dest[i];
         s.ldbp0 = p.last_dest_by_player[2 * i];
         s.ldbp1 = p.last_dest_by_player[2 * i + 1];
     }
     s.phase = p.phase ? p.phase[i] : 0;
+    s.must_move = p.must_move ? p.must_move[i] : -1;
     Game::rebuild_ext(s);
     lx::store_state<Game>(s, st, B, i);
 }
 
-// (B, 3, C) uint8 relative-owner planes (reference compiler.py:611-626;
-// single piece type: own stones, opponent stones, is-mover plane)
+// (B, 2T+1, C) uint8 relative-owner planes (reference compiler.py:611-626):
+// per piece type t the player's and the opponent's pieces of type t, then
+// the is-mover plane
 extern "C" __global__ void __launch_bounds__(128) lx_observe(const u32* st, i64 B, int player,
                                                              unsigned char* planes) {
     const i64 i = lx::gtid();
@@ -516,11 +585,16 @@ extern "C" __global__ void __launch_bounds__(128) lx_observe(const u32* st, i64 
     lx::load_state<Game>(s, st, B, i);
     const lx::BB<Game::W> me = player ? s.own1 : s.own0;
     const lx::BB<Game::W> op = player ? s.own0 : s.own1;
-    unsigned char* out = planes + i * (i64)(3 * Game::C);
+    constexpr int T = Game::NT;
+    unsigned char* out = planes + i * (i64)((2 * T + 1) * Game::C);
     const unsigned char mv = s.cur == player;
-    for (int c = 0; c < Game::C; c++) {
-        out[c] = lx::test(me, Game::cell_bit(c));
-        out[Game::C + c] = lx::test(op, Game::cell_bit(c));
-        out[2 * Game::C + c] = mv;
+    for (int t = 0; t < T; t++) {
+        const lx::BB<Game::W> tb = Game::type_bb(s, t);
+        const lx::BB<Game::W> a = me & tb, b = op & tb;
+        for (int c = 0; c < Game::C; c++) {
+            out[2 * t * Game::C + c] = lx::test(a, Game::cell_bit(c));
+            out[(2 * t + 1) * Game::C + c] = lx::test(b, Game::cell_bit(c));
+        }
     }
+    for (int c = 0; c < Game::C; c++) out[2 * T * Game::C + c] = mv;
 }

@@ -2,16 +2,20 @@
 // word layout (pack/unpack), start position, sampling and the ply itself.
 // Host-compilable on purpose (no CUDA builtins beyond lx_core.cuh), so the
 // CPU test suite can run the generated rules through tests/hostsim.
+//
+// G::MECH selects the mechanic family of the lowered game:
+//   0 placement  -- G::legal(s) is the bitboard of legal cells
+//   1 movement   -- G::count_moves / select_move / move_legal / apply_move
+//   2 gridworld  -- same interface, actions are direction indices
 #pragma once
 
 namespace lx {
-
 
 template <class G>
 struct Layout {
     static constexpr int W = G::W, NX = G::NX;
     static constexpr int META = 2 * W + NX;
-    static constexpr int NWORDS = META + 7;
+    static constexpr int NWORDS = META + 8;
     static constexpr int NQ = (NWORDS + 3) / 4;
 };
 
@@ -40,6 +44,10 @@ __device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<
     s.sc0 = (short)(w[M + 4] & 0xffffu);
     s.sc1 = (short)(w[M + 4] >> 16);
     s.seed = (u64)w[M + 5] | ((u64)w[M + 6] << 32);
+    s.last_source = (short)(w[M + 7] & 0xffffu);
+    s.must_move = (short)(w[M + 7] >> 16);
+    s.ovr = -1;
+    s.samep = 0;
 }
 
 template <class G>
@@ -59,6 +67,7 @@ __device__ __forceinline__ void pack(const typename G::St& s, u32 (&w)[Layout<G>
     w[M + 4] = ((u32)s.sc0 & 0xffffu) | ((u32)s.sc1 << 16);
     w[M + 5] = (u32)s.seed;
     w[M + 6] = (u32)(s.seed >> 32);
+    w[M + 7] = ((u32)s.last_source & 0xffffu) | ((u32)s.must_move << 16);
 #pragma unroll
     for (int i = Layout<G>::NWORDS; i < Layout<G>::NQ * 4; i++) w[i] = 0u;
 }
@@ -73,36 +82,72 @@ __device__ __forceinline__ void init_state(typename G::St& s, u64 seed) {
     s.mc = 0u;
     s.cur = G::FIRST_PLAYER;
     s.term = 0; s.trunc = 0; s.outcome = -1; s.phase = 0;
-    s.last_mover = -1; s.last_kind = -1; s.last_dest = -1;
+    s.last_mover = -1; s.last_kind = -1; s.last_dest = -1; s.last_source = -1;
     s.pass_streak = 0; s.pf0 = 0; s.pf1 = 0; s.ldbp0 = -1; s.ldbp1 = -1;
     s.sc0 = 0; s.sc1 = 0;
+    s.must_move = -1; s.ovr = -1; s.samep = 0;
     s.seed = seed;
     G::start(s);
 }
 
+// number of legal non-pass actions for the current mover (reference
+// CompiledGame.compute_all totals, compiler.py:379-392)
+template <class G>
+__device__ __forceinline__ int legal_count(const typename G::St& s) {
+    if constexpr (G::MECH == 0) {
+        return popc(G::legal(s));
+    } else {
+        int tot[G::NG];
+        return G::count_moves(s, tot);
+    }
+}
+
 // uniform legal action for the current mover; -1 when stuck
-// (reference compiler.py:430-446, mechanics.py:488-492)
+// (reference compiler.py:430-446, mechanics.py:209-242, 488-492).  `hint`
+// receives the sampled move group (movement games) for apply_step.
+template <class G>
+__device__ __forceinline__ int sample_action(const typename G::St& s, u64 smix, int& hint) {
+    hint = -1;
+    if constexpr (G::MECH == 0) {
+        const BB<G::W> legal = G::legal(s);
+        const int n = popc(legal);
+        if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
+        const int r = draw_index(mix64(smix ^ (u64)s.mc), n);
+        return G::bit_cell(select_bit(legal, r));
+    } else {
+        int tot[G::NG];
+        const int n = G::count_moves(s, tot);
+        if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
+        const int r = draw_index(mix64(smix ^ (u64)s.mc), n);
+        return G::select_move(s, r, tot, hint);
+    }
+}
+
 template <class G>
 __device__ __forceinline__ int sample_action(const typename G::St& s, u64 smix) {
-    const BB<G::W> legal = G::legal(s);
-    const int n = popc(legal);
-    if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
-    const int r = draw_index(mix64(smix ^ (u64)s.mc), n);
-    return G::bit_cell(select_bit(legal, r));
+    int hint;
+    return sample_action<G>(s, smix, hint);
 }
 
 // one ply for a live row (reference compiler.py:456-580, order preserved:
-// mechanic write, pass bookkeeping, effects, score clamp, advancement,
-// ordered end rules evaluated for the mover, counters)
+// mechanic write, pass bookkeeping, effects, score clamp, advancement incl.
+// extra-turn override and must_move, no_legal_actions lookahead, ordered end
+// rules evaluated for the mover, counters)
 template <class G>
-__device__ __forceinline__ void apply_step(typename G::St& s, int action) {
+__device__ __forceinline__ void apply_step(typename G::St& s, int action, int hint = -1) {
     const int mover = s.cur;
     const int phase = s.phase;
     const bool is_pass = (G::PASS >= 0) && action == G::PASS;
+    s.ovr = -1;
+    s.samep = 0;
     if (is_pass) {
-        s.last_kind = 4; s.last_dest = -1; s.last_mover = mover;
+        s.last_kind = 4; s.last_dest = -1; s.last_source = -1; s.last_mover = mover;
     } else {
-        G::write_place(s, action, mover, phase);
+        if constexpr (G::MECH == 0) {
+            G::write_place(s, action, mover, phase);
+        } else {
+            G::apply_move(s, action, mover, hint);
+        }
     }
     if (G::L_PASSING) {
         if (is_pass) {
@@ -120,21 +165,37 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action) {
     }
     int next_player, next_phase;
     G::advance(phase, mover, next_player, next_phase);
-    const int out = G::end_rules(s, mover);
+    if (s.ovr >= 0) { next_player = s.ovr; next_phase = phase; }      // extra turn
+    if (G::L_MUSTMOVE) s.must_move = (s.ovr >= 0 && s.samep) ? s.last_dest : -1;
+    int next_count = 0;
+    if (G::NEEDS_NEXT_COUNT) {                                          // compiler.py:547-561
+        typename G::St t = s;
+        t.cur = next_player;
+        t.phase = next_phase;
+        next_count = legal_count<G>(t);
+        if (next_count == 0 && G::PASS >= 0 && G::force_pass(next_phase)) next_count = 1;
+    }
+    const int out = G::end_rules(s, mover, next_count);
     if (out >= 0) { s.term = 1; s.outcome = out; }
     s.mc += 1u;
     s.cur = next_player;
     s.phase = next_phase;
 }
 
-// legality of one action (reference mechanics.py:499-512, compiler.py:484-494)
+// legality of one action (reference mechanics.py:281-338, 499-512,
+// compiler.py:484-494)
 template <class G>
 __device__ __forceinline__ bool action_legal(const typename G::St& s, i64 a) {
-    const BB<G::W> legal = G::legal(s);
-    if (G::PASS >= 0 && a == G::PASS) return !any(legal) && G::force_pass(s.phase);
-    if (a < 0 || a >= G::C) return false;
-    return test(legal, G::cell_bit((int)a));
+    if constexpr (G::MECH == 0) {
+        const BB<G::W> legal = G::legal(s);
+        if (G::PASS >= 0 && a == G::PASS) return !any(legal) && G::force_pass(s.phase);
+        if (a < 0 || a >= G::C) return false;
+        return test(legal, G::cell_bit((int)a));
+    } else {
+        if (G::PASS >= 0 && a == G::PASS) return legal_count<G>(s) == 0 && G::force_pass(s.phase);
+        if (a < 0 || a >= (i64)(G::PASS >= 0 ? G::A - 1 : G::A)) return false;
+        return G::move_legal(s, (int)a);
+    }
 }
-
 
 }  // namespace lx

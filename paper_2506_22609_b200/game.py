@@ -48,28 +48,47 @@ def _torch():
 
 @dataclass(frozen=True)
 class ActionCodec:
-    """Placement codec: action = cell, trailing pass (reference codec.py:16-69)."""
+    """Action index <-> move (reference codec.py:16-69): placement = cell,
+    movement = source * C + dest, gridworld = direction index; optional
+    trailing pass."""
     kind: str
     num_cells: int
     size: int
     has_pass: bool
+    directions: tuple = ()
 
     @property
     def pass_index(self):
         return self.size - 1 if self.has_pass else None
 
     def encode(self, source, dest):
-        return dest
+        if self.kind == "movement":
+            return source * self.num_cells + dest
+        if self.kind == "placement":
+            return dest
+        raise ValueError("gridworld actions are direction indices; use encode_direction")
+
+    def encode_direction(self, direction):
+        return self.directions.index(direction)
 
     def decode(self, action):
         if self.has_pass and action == self.pass_index:
             return None, None
-        return None, action
+        if self.kind == "movement":
+            return action // self.num_cells, action % self.num_cells
+        if self.kind == "placement":
+            return None, action
+        return None, None
 
     def describe(self, action):
         if self.has_pass and action == self.pass_index:
             return {"kind": "pass"}
-        return {"kind": "place", "dest": action}
+        if self.kind == "movement":
+            return {"kind": "move", "source": action // self.num_cells,
+                    "dest": action % self.num_cells}
+        if self.kind == "placement":
+            return {"kind": "place", "dest": action}
+        return {"kind": "direction", "direction": self.directions[action]}
 
 
 @dataclass(frozen=True)
@@ -165,8 +184,9 @@ class B200Game:
         self.num_cells = lowered.info["C"]
         L = lowered.info["layout"]
         self.layout = StateLayout(**{k: L[k] for k in StateLayout.__dataclass_fields__})
-        self.codec = ActionCodec("placement", self.num_cells, lowered.info["A"],
-                                 lowered.info["pass_index"] >= 0)
+        self.codec = ActionCodec(lowered.info["codec"], self.num_cells, lowered.info["A"],
+                                 lowered.info["pass_index"] >= 0,
+                                 tuple(lowered.info["grid_directions"]))
         self.piece_names = tuple(p.name for p in spec.equipment.pieces)
         self._native = None
         self._nq = lowered.info["nq"]
@@ -210,12 +230,13 @@ class B200Game:
         return {"name": self.name,
                 "board": {"kind": b.kind, "rows": b.rows, "cols": b.cols},
                 "num_cells": self.num_cells, "pieces": list(self.piece_names),
-                "action_space": {"kind": "placement", "size": self.codec.size,
+                "action_space": {"kind": self.codec.kind, "size": self.codec.size,
                                  "has_pass": self.codec.has_pass},
                 "observation_planes": self.observation_planes,
                 "phases": len(self.spec.phases),
                 "state_layout": {"scores": self.layout.scores, "passing": self.layout.passing,
-                                 "must_move": False, "last_action": self.layout.last_action,
+                                 "must_move": self.layout.must_move,
+                                 "last_action": self.layout.last_action,
                                  "transient_masks": False,
                                  "connectivity_plans": self.layout.connectivity,
                                  "phase_index": self.layout.phase, "turn_position": False},
@@ -390,7 +411,8 @@ class B200Game:
     def observe_device(self, state, player):
         torch = _torch()
         B = state.batch_size
-        planes = torch.empty((B, 3, self.num_cells), dtype=torch.uint8, device="cuda")
+        planes = torch.empty((B, self.observation_planes, self.num_cells), dtype=torch.uint8,
+                             device="cuda")
         native.check(native.lib().lx_observe(self.handle, state.words.data_ptr(), B,
                                              int(player), planes.data_ptr(), self._stream()))
         return planes.view(torch.bool)
@@ -413,6 +435,8 @@ class B200Game:
         if L.passing:
             f["pass_streak"] = ((B,), torch.int16)
             f["pass_flags"] = ((B, 2), torch.bool)
+        if L.must_move:
+            f["must_move"] = ((B,), torch.int16)
         if L.last_action:
             f.update({"last_mover": ((B,), torch.int8), "last_kind": ((B,), torch.int8),
                       "last_source": ((B,), torch.int16), "last_dest": ((B,), torch.int16),

@@ -30,6 +30,7 @@ import numpy as np
 from . import nodes as n
 from .errors import CompileError, UnsupportedConstruct
 from .geometry import OPPOSITE, Board, direction_pairs, resolve_direction
+from .lowering_moves import KIND_IDS, MoveLoweringMixin
 
 ANCHOR_COST_THRESHOLD = 128          # reference compiler.py:28
 
@@ -91,7 +92,7 @@ def _words(mask, W):
                  .view(">u4").reshape(W))
 
 
-class GameLowering:
+class GameLowering(MoveLoweringMixin):
     """Walks one validated GameSpec and produces its Lowered unit."""
 
     def __init__(self, spec):
@@ -116,8 +117,8 @@ class GameLowering:
         self.W = (self.NB + 31) // 32
         self.em = _Emitter(B, self.W, self.bit_of)
         self.piece_ids = {p.name: i for i, p in enumerate(spec.equipment.pieces)}
-        if len(self.piece_ids) != 1:
-            _fail("only single-piece-type games are lowered (board_piece is implied)")
+        self._setup_piece_types()
+        self.anchored_ctx = False          # effects compile with the anchored context
         self.forward = dict(spec.players.forward)
         self.regions = {}
         for r in spec.equipment.regions:
@@ -168,21 +169,30 @@ class GameLowering:
         spec = self.spec
         allnodes = list(n.walk(spec))
         types = {type(x) for x in allnodes}
-        for t in (n.MoveMechanic, n.HopMove, n.SlideMove, n.StepMove):
-            if t in types:
-                _fail("movement mechanics are not lowered yet (SURVEY 8f row 3)")
-        for t in (n.PromoteEffect, n.ExtraTurnEffect, n.CapturedMask, n.HoppedMask,
-                  n.PromotedMask, n.PrevMoveMask, n.LastMoveInPred, n.ActionWasPred,
-                  n.CanMoveAgainPred, n.NoLegalActionsPred, n.CornerCustodialMask,
-                  n.PatternFn):
+        for t in (n.CapturedMask, n.HoppedMask, n.PromotedMask, n.PatternFn):
             if t in types:
                 _fail(f"{t.__name__} is not lowered yet")
+        kinds = {type(p.mechanic) for p in spec.phases}
+        if len(kinds) > 1:
+            _fail("games mixing placement and movement phases are not lowered yet")
+        self.grid = None
+        if n.MoveMechanic in kinds:
+            self.grid = self._detect_gridworld()
+            self.mech_kind = 2 if self.grid is not None else 1
+            if self.mech_kind == 1 and len({p.mechanic for p in spec.phases}) > 1:
+                _fail("movement phases with different move sets are not lowered yet")
+        else:
+            self.mech_kind = 0
         self.has_flip = n.FlipEffect in types
         scores = any(t in types for t in (n.ScoreFn, n.SetScoreEffect, n.IncrementScoreEffect))
         scores |= any(isinstance(x, n.CaptureEffect) and x.increment_score for x in allnodes)
         scores |= any(r.result.kind == "by_score" for r in spec.end_rules)
         passing = any(p.force_pass for p in spec.phases) or n.PassedPred in types
-        last_action = any(t in types for t in (n.CustodialMask,))
+        must_move = any(isinstance(x, n.ExtraTurnEffect) and x.same_piece for x in allnodes)
+        last_action = any(t in types for t in (      # reference compiler.py:114-116
+            n.ActionWasPred, n.CanMoveAgainPred, n.PrevMoveMask, n.LastMoveInPred,
+            n.CustodialMask, n.CornerCustodialMask, n.ExtraTurnEffect))
+        self.needs_next_count = n.NoLegalActionsPred in types
         for x in allnodes:
             if isinstance(x, n.ConnectedFn):
                 self._conn_plan(x)
@@ -204,7 +214,7 @@ class GameLowering:
         if any(len(p.order) != len(set(p.order)) for p in spec.phases):
             _fail("repeated players in a mover order (turn_pos layout) are not lowered yet")
         self.has_pass = passing
-        self.layout = {"scores": scores, "passing": passing, "must_move": False,
+        self.layout = {"scores": scores, "passing": passing, "must_move": must_move,
                        "last_action": last_action or bool(cands),
                        "transient_masks": False, "connectivity": len(self.conn_plans),
                        "phase": self.phase_mult, "turn_pos": False}
@@ -212,8 +222,12 @@ class GameLowering:
         self._last_action_base = last_action
         if len(self.conn_plans) > 1:
             _fail("more than one connectivity direction plan is not lowered yet")
-        self.A = self.C + (1 if passing else 0)
-        self.PASS = self.C if passing else -1
+        # action codec (reference codec.py:58-69)
+        base = {0: self.C, 1: self.C * self.C}.get(self.mech_kind)
+        if base is None:
+            base = len(self.grid[2])
+        self.A = base + (1 if passing else 0)
+        self.PASS = base if passing else -1
 
     def _conn_plan(self, node):
         dirs = resolve_direction(node.directions or ("any",), n.P1, self.forward, self.board)
@@ -329,8 +343,49 @@ class GameLowering:
         if t is n.MaskNot:
             return f"lx::andnot({self.em.const(self.valid)}, {self.mask(node.item)})"
         if t is n.CustodialMask:
+            if not self.anchored_ctx:
+                _fail("custodial masks outside effects / placement results are not lowered yet")
             return self.custodial_anchored(node)
+        if t is n.CornerCustodialMask:
+            return self.corner_custodial(node)
+        if t is n.PrevMoveMask:                 # reference exprs.py:167-176
+            sd = self.side(node.who)
+            return (f"([&]() {{ const int d_ = ({sd}) ? s.ldbp1 : s.ldbp0; "
+                    f"return d_ >= 0 ? lx::onehot<W>(cell_bit(d_)) : lx::bb_zero<W>(); }}())")
         _fail(f"mask {t.__name__} is not lowered yet")
+
+    def corner_custodial(self, node):
+        """Enemy piece on a corner whose two orthogonal neighbours are the
+        side's; in effects only when one of them was just moved to by the
+        side (reference exprs.py:381-408)."""
+        side = self.side(node.mover)
+        B = self.board
+        corners = []
+        for c in B.corner_cells:
+            nbrs = [int(B.neighbors[d][c]) for d in ("up", "down", "left", "right")
+                    if d in B.neighbors and int(B.neighbors[d][c]) != self.C]
+            if len(nbrs) == 2:
+                corners.append((c, nbrs[0], nbrs[1]))
+        name = f"corner_{self.em.fresh('cc')}"
+        tgt = self.piece_filter(node.piece, "tgt")
+        lines = []
+        for c, n1, n2 in corners:
+            b, b1, b2 = (int(self.bit_of[x]) for x in (c, n1, n2))
+            cond = f"lx::test(tg, {b}) && lx::test(fl, {b1}) && lx::test(fl, {b2})"
+            if self.anchored_ctx:
+                cond += f" && (s.last_dest == {n1} || s.last_dest == {n2}) && s.last_mover == side"
+            lines.append(f"        if ({cond}) lx::setbit(out, {b});")
+        body = "\n".join(lines)
+        self.em.helper(name, f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
+        const int side = {side};
+        const BBW fl = side ? s.own1 : s.own0;
+        const BBW tgt = side ? s.own0 : s.own1;
+        const BBW tg = {tgt};
+        BBW out = lx::bb_zero<W>();
+{body}
+        return out;
+    }}""")
+        return f"{name}(s, mover)"
 
     # -- custodial ------------------------------------------------------------
 
@@ -498,8 +553,8 @@ class GameLowering:
         """Anchored line test (reference exprs.py:484-535) by probing: the run
         of the player's stones through last_dest along some axis has at least
         `length` cells."""
-        if node.exclude is not None:
-            _fail("line exclude: is not lowered yet")
+        if node.exclude is not None or self.piece_mode != "single":
+            _fail("probed line with exclude: / several piece types is not lowered yet")
         side = self.side(node.player)
         L = node.length
         name = f"line_probe_{self.em.fresh('a')}"
@@ -539,9 +594,9 @@ class GameLowering:
         the run length.  The reference bounds runs by the padded ray length
         L (runlen < L), which any flanked run on the board satisfies.
         """
-        if self.use_probe and node.length != "any":
+        if self.piece_mode == "single" and self.use_probe and node.length != "any":
             return self.custodial_anchored_probe(node)
-        if node.length == "any" and self.W <= 2:
+        if self.piece_mode == "single" and node.length == "any" and self.W <= 2:
             return self.custodial_anchored_rays(node)
         side = self.side(node.mover)
         name = f"custodial_{self.em.fresh('c')}"
@@ -573,7 +628,7 @@ class GameLowering:
         code = f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
         const int side = {side};
         const BBW flank = side ? s.own1 : s.own0;
-        const BBW tgt = side ? s.own0 : s.own1;
+        const BBW tgt = {self.piece_filter(node.piece, "(side ? s.own0 : s.own1)")};
         BBW out = lx::bb_zero<W>();
         if (!(s.last_dest >= 0 && s.last_mover == side)) return out;
         const BBW a = lx::onehot<W>(cell_bit(s.last_dest));
@@ -608,7 +663,7 @@ class GameLowering:
         code = f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
         const int side = {side};
         const BBW flank = side ? s.own1 : s.own0;
-        const BBW tgt = side ? s.own0 : s.own1;
+        const BBW tgt = {self.piece_filter(node.piece, "(side ? s.own0 : s.own1)")};
         BBW out = lx::bb_zero<W>();
 {body}
         return out;
@@ -641,9 +696,13 @@ class GameLowering:
             cur, cur_len, rest = nm, cur_len + p, rest - p
         return code, cur
 
+    def _line_excluded(self, node):
+        """Static cells a window may not touch (reference exprs.py:427-431)."""
+        ex = node.exclude if isinstance(node.exclude, tuple) else (node.exclude,)
+        return self._static_union(ex)
+
     def _line_fn(self, node, kind):
-        if node.exclude is not None:
-            _fail("line exclude: is not lowered yet")
+        excl = self._line_excluded(node) if node.exclude is not None else None
         axes = self.board.orientation_dirs(node.orientation)
         name = f"line_{kind}_{self.em.fresh('l')}"
         body = []
@@ -658,6 +717,12 @@ class GameLowering:
                 body.append(f"            const BBW rx = lx::andnot(lx::andnot({r}, "
                             f"{self.nb(OPPOSITE[d], 'b')}), {self.walk(d, node.length, 'b')});")
                 r = "rx"
+            if excl is not None:
+                allowed = np.zeros(self.C, dtype=bool)
+                for dd, cells in self.board.line_windows(node.length, d):
+                    if not excl[list(cells)].any():
+                        allowed[cells[0]] = True
+                r = f"({r} & {self.em.const(allowed)})"
             body.append(f"            acc = acc | {r};" if kind == "any"
                         else f"            acc += lx::popc({r});")
             body.append("        }")
@@ -673,23 +738,23 @@ class GameLowering:
 
     def line_exists(self, node):
         """Any window of `length` stones of the player (one axis live at a time)."""
-        stones = self.stones(self.side(node.player))
+        stones = self.piece_filter(node.piece, self.stones(self.side(node.player)))
         return f"{self._line_fn(node, 'any')}({stones})"
 
     def line_count(self, node):
         """Number of satisfied windows (LineFn as a function, exprs.py:454-459)."""
-        stones = self.stones(self.side(node.player))
+        stones = self.piece_filter(node.piece, self.stones(self.side(node.player)))
         return f"{self._line_fn(node, 'count')}({stones})"
 
     def line_anchored_exists(self, node):
         """Exact anchored form: a satisfied window through last_dest
         (reference exprs.py:484-535) <=> the run of the mover's stones through
         the anchor along some axis has >= length cells."""
-        stones = self.stones(self.side(node.player))
+        stones = self.piece_filter(node.piece, self.stones(self.side(node.player)))
         L = node.length
         name = f"line_anchor_{self.em.fresh('a')}"
         if node.exclude is not None:
-            _fail("line exclude: is not lowered yet")
+            _fail("anchored line with exclude: is not lowered yet")
         lines = []
         # exact lines need the maximal run through the anchor to be exactly L:
         # grow L steps each way and compare (reference exprs.py:525-533)
@@ -775,7 +840,8 @@ class GameLowering:
         self.conn_slots = {}
         self.slot_info = []
         types = {type(x) for x in n.walk(self.spec)}
-        if n.CaptureEffect in types or n.FlipEffect in types or not self.conn_plans:
+        if (n.CaptureEffect in types or n.FlipEffect in types or not self.conn_plans
+                or self.mech_kind != 0):
             return
 
         def register(node, gate):
@@ -818,13 +884,13 @@ class GameLowering:
                 register(x, None)
 
     def _slot_get(self, k):
-        W = self.W
-        words = ", ".join(f"s.ext[{k * W + i}]" for i in range(W))
+        W, X = self.W, self.xbase
+        words = ", ".join(f"s.ext[{X + k * W + i}]" for i in range(W))
         return f"BBW{{{{{words}}}}}"
 
     def _slot_set(self, k, var):
-        W = self.W
-        return " ".join(f"s.ext[{k * W + i}] = {var}.w[{i}];" for i in range(W))
+        W, X = self.W, self.xbase
+        return " ".join(f"s.ext[{X + k * W + i}] = {var}.w[{i}];" for i in range(W))
 
     def connected(self, node):
         """Some component of the side's stones touches every target mask
@@ -978,6 +1044,19 @@ class GameLowering:
                 return "(s.pass_streak >= 2)"
             sd = self.side(node.who)
             return f"((({sd}) ? s.pf1 : s.pf0) != 0)"
+        if t is n.LastMoveInPred:               # reference exprs.py:732-741
+            m = self.mask(node.mask)
+            return (f"(s.last_dest >= 0 && s.last_mover == mover && "
+                    f"lx::test({m}, cell_bit(s.last_dest)))")
+        if t is n.ActionWasPred:                # reference exprs.py:743-750
+            sd = self.side(node.who)
+            return f"(s.last_mover == ({sd}) && s.last_kind == {KIND_IDS[node.kind]})"
+        if t is n.CanMoveAgainPred:             # reference exprs.py:752-757
+            return f"can_move_again(s, mover, {KIND_IDS[node.kind]})"
+        if t is n.NoLegalActionsPred:           # reference exprs.py:771-783
+            if not end_rule:
+                _fail("no_legal_actions outside an end condition")
+            return "(next_count == 0)"
         _fail(f"predicate {t.__name__} is not lowered yet")
 
     def line_predicate(self, line, end_rule):
@@ -1012,6 +1091,8 @@ class GameLowering:
             own0, own1 = start_has_line
             if self._np_line(own0, line) or self._np_line(own1, line):
                 continue      # reference keeps the global form (compiler.py:272-277)
+            if line.exclude is not None:
+                _fail("anchored line with exclude: is not lowered yet")
             self.anchor_lines.add(line)
         if self._anchor_candidates and not self.anchor_lines and not self._last_action_base:
             self.layout["last_action"] = False
@@ -1025,23 +1106,39 @@ class GameLowering:
                         self._global_ok.add(id(x.fn))
 
     def _np_line(self, owner_cells, line):
-        for _, cells in self.board.line_windows(line.length, line.orientation):
-            if all(owner_cells[c] for c in cells):
-                return True
+        """Start position holds a satisfied window for a side (reference
+        _LineTables.satisfied, exprs.py:433-450: piece, exact, exclude)."""
+        pid = self.piece_ids[line.piece]
+        mine = owner_cells & (self._start_types == pid)
+        excl = self._line_excluded(line) if line.exclude is not None else None
+        nb = self.board.neighbors
+        for d, cells in self.board.line_windows(line.length, line.orientation):
+            if not all(mine[c] for c in cells):
+                continue
+            if excl is not None and excl[list(cells)].any():
+                continue
+            if line.exact:
+                b = int(nb[OPPOSITE[d]][cells[0]])
+                a = int(nb[d][cells[-1]])
+                if (b != self.C and mine[b]) or (a != self.C and mine[a]):
+                    continue
+            return True
         return False
 
     def _start_boards(self):
         own = [np.zeros(self.C, dtype=bool), np.zeros(self.C, dtype=bool)]
+        self._start_types = np.full(self.C, -1, dtype=np.int64)
         for sp in self.spec.start:
             cells = list(sp.cells) if sp.cells else \
                 np.nonzero(self._static_union(sp.masks))[0].tolist()
             own[sp.player][cells] = True
+            self._start_types[cells] = self.piece_ids[sp.piece]
         return own
 
     def lower(self):
         self._decide_anchoring()
         self._conn_tracking()
-        NX = len(self.slot_info) * self.W
+        NX = self.xbase + len(self.slot_info) * self.W
         spec = self.spec
         phases = spec.phases
         em = self.em
@@ -1053,6 +1150,9 @@ class GameLowering:
                 np.nonzero(self._static_union(sp.masks))[0].tolist()
             start_scores[sp.player] += len(cells)
         start_code = [f"        s.own0 = {em.const(own[0])};", f"        s.own1 = {em.const(own[1])};"]
+        for t in range(1, self.NPL + 1):
+            start_code.append(f"        {{ const BBW pl = {em.const(self._start_types == t)}; "
+                              f"{self._plane_set(t, 'pl')} }}")
         if self.layout["scores"]:
             start_code.append(f"        s.sc0 = {start_scores[0]}; s.sc1 = {start_scores[1]};")
 
@@ -1060,6 +1160,13 @@ class GameLowering:
         legal_cases, fp_cases, eff_cases = [], [], []
         for pi, ph in enumerate(phases):
             mech = ph.mechanic
+            if ph.force_pass:
+                fp_cases.append(pi)
+            if mech.effects:
+                eff_cases.append(f"            case {pi}: {{\n{self.effects(mech.effects, mech)}\n"
+                                 f"                break;\n            }}")
+            if self.mech_kind != 0:
+                continue
             dest = self.mask(mech.destination)
             legal = f"lx::andnot({em.const(self.valid)}, s.own0 | s.own1) & {dest}"
             if mech.result is not None:
@@ -1071,15 +1178,22 @@ class GameLowering:
                     _fail("placement result predicates other than (exists (custodial ...)) "
                           "by the placing side are not lowered yet")
             legal_cases.append(f"            case {pi}: return {legal};")
-            if ph.force_pass:
-                fp_cases.append(pi)
-            if mech.effects:
-                eff_cases.append(f"            case {pi}: {{\n{self.effects(mech.effects, mech)}\n"
-                                 f"                break;\n            }}")
-        owner_side = {pi: self.side(ph.mechanic.owner) for pi, ph in enumerate(phases)}
-        if len(set(owner_side.values())) != 1:
-            _fail("per-phase placement owners differ")
-        owner = owner_side[0]
+        if self.mech_kind == 0:
+            owner_side = {pi: self.side(ph.mechanic.owner) for pi, ph in enumerate(phases)}
+            if len(set(owner_side.values())) != 1:
+                _fail("per-phase placement owners differ")
+            owner = owner_side[0]
+            place_planes = []
+            for pi, ph in enumerate(phases):
+                t = self.piece_ids[ph.mechanic.piece]
+                if self.piece_mode == "planes" and t >= 1:
+                    place_planes.append(f"        if (phase == {pi}) {{ BBW pl = {self._plane(t)}; "
+                                        f"pl = pl | oh; {self._plane_set(t, 'pl')} }}")
+            place_planes = "\n".join(place_planes)
+        elif self.mech_kind == 1:
+            mech_code = self.movement_code(phases[0].mechanic) + "\n" + self.movement_stubs()
+        else:
+            mech_code = self.gridworld_code(self.grid) + "\n" + self.movement_stubs()
 
         # end rules
         end_lines = []
@@ -1133,6 +1247,30 @@ class GameLowering:
         fp = " || ".join(f"phase == {p}" for p in fp_cases) or "false"
         conn_update = self._conn_update_code()
         conn_rebuild = self._conn_rebuild_code()
+        if self.mech_kind == 0:
+            mech_code = f"""    static constexpr int MECH = 0;
+    static __device__ __forceinline__ BBW legal(const St& s) {{
+        const int mover = s.cur;
+        const BBW me = mover ? s.own1 : s.own0;
+        const BBW op = mover ? s.own0 : s.own1;
+        (void)me; (void)op;
+        switch (s.phase) {{
+{chr(10).join(legal_cases)}
+            default: return lx::bb_zero<W>();
+        }}
+    }}
+    static __device__ __forceinline__ void write_place(St& s, int cell, int mover, int phase) {{
+        const int side = {owner};
+        const BBW oh = lx::onehot<W>(cell_bit(cell));   // branchless: no warp split on the mover
+        s.own0 = lx::sel(side != 0, s.own0 | oh, s.own0);
+        s.own1 = lx::sel(side != 0, s.own1, s.own1 | oh);
+        s.last_kind = 0; s.last_dest = cell; s.last_source = -1; s.last_mover = side;
+        s.ldbp0 = side ? s.ldbp0 : cell;
+        s.ldbp1 = side ? cell : s.ldbp1;
+{place_planes}
+{conn_update}
+    }}
+{self.placement_stubs()}"""
         L = self.layout
         # rollout block shape: 2 x 256 threads per SM (<= 128 registers) won a
         # B200 sweep for every config game incl. Pente (128x3..5 and 256x2 tried)
@@ -1169,27 +1307,12 @@ struct Game {{
 {chr(10).join(start_code)}
         rebuild_ext(s);
     }}
-    static __device__ __forceinline__ BBW legal(const St& s) {{
-        const int mover = s.cur;
-        const BBW me = mover ? s.own1 : s.own0;
-        const BBW op = mover ? s.own0 : s.own1;
-        (void)me; (void)op;
-        switch (s.phase) {{
-{chr(10).join(legal_cases)}
-            default: return lx::bb_zero<W>();
-        }}
-    }}
     static __device__ __forceinline__ bool force_pass(int phase) {{ return {fp}; }}
-    static __device__ __forceinline__ void write_place(St& s, int cell, int mover, int phase) {{
-        const int side = {owner};
-        const BBW oh = lx::onehot<W>(cell_bit(cell));   // branchless: no warp split on the mover
-        s.own0 = lx::sel(side != 0, s.own0 | oh, s.own0);
-        s.own1 = lx::sel(side != 0, s.own1, s.own1 | oh);
-        s.last_kind = 0; s.last_dest = cell; s.last_mover = side;
-        s.ldbp0 = side ? s.ldbp0 : cell;
-        s.ldbp1 = side ? cell : s.ldbp1;
-{conn_update}
-    }}
+    static constexpr int NT = {self.NT};                       // piece types
+    static constexpr bool L_MUSTMOVE = {str(L['must_move']).lower()};
+    static constexpr bool NEEDS_NEXT_COUNT = {str(self.needs_next_count).lower()};
+{self._types_code()}
+{mech_code}
     static __device__ __forceinline__ void effects(St& s, int cell, int mover, int phase) {{
         switch (phase) {{
 {chr(10).join(eff_cases)}
@@ -1200,10 +1323,10 @@ struct Game {{
 {chr(10).join(adv)}
         np = 0; nphase = phase;
     }}
-    static __device__ __forceinline__ int end_rules(const St& s, int mover) {{
+    static __device__ __forceinline__ int end_rules(const St& s, int mover, int next_count) {{
         const BBW me = mover ? s.own1 : s.own0;
         const BBW op = mover ? s.own0 : s.own1;
-        (void)me; (void)op;
+        (void)me; (void)op; (void)next_count;
 {chr(10).join(end_lines)}
         return -1;
     }}
@@ -1221,16 +1344,24 @@ struct Game {{
         src = src.replace("@@HELPERS@@", "\n".join(em.helpers.values()))
         info = {"name": spec.name, "C": self.C, "A": self.A, "W": self.W, "NX": NX,
                 "pass_index": self.PASS, "layout": dict(self.layout),
-                "nwords": 2 * self.W + NX + 7, "nq": (2 * self.W + NX + 7 + 3) // 4,
+                "nwords": 2 * self.W + NX + 8, "nq": (2 * self.W + NX + 8 + 3) // 4,
                 "first_player": int(phases[0].order[0]), "nphase": nph,
-                "observation_planes": 3}
+                "observation_planes": 2 * self.NT + 1, "mechanics": self.mech_kind,
+                "codec": {0: "placement", 1: "movement", 2: "gridworld"}[self.mech_kind],
+                "grid_directions": list(self.grid[2]) if self.grid else [],
+                "piece_mode": self.piece_mode, "piece_names": list(self.piece_ids)}
         return Lowered(name=spec.name, source=src, info=info)
 
     def effects(self, effs, mech):
-        """Ordered effect list (reference effects.py:17-133)."""
+        """Ordered effect list (reference effects.py:17-133), compiled in the
+        anchored context (reference compiler.py:224-228)."""
         out = []
-        for e in effs:
-            out.append(self.effect(e))
+        self.anchored_ctx = True
+        try:
+            for e in effs:
+                out.append(self.effect(e))
+        finally:
+            self.anchored_ctx = False
         return "\n".join(out)
 
     def effect(self, e):
@@ -1249,8 +1380,27 @@ struct Game {{
             if e.increment_score:
                 inc = (f"\n{ind}  {{ const int g = lx::popc(cells); "
                        f"if (mover) s.sc1 += g; else s.sc0 += g; }}")
-            return (f"{ind}{{ const BBW cells = {m} & (s.own0 | s.own1);\n"
-                    f"{ind}  s.own0 = lx::andnot(s.own0, cells); s.own1 = lx::andnot(s.own1, cells);{inc} }}")
+            return (f"{ind}{{ const BBW cells = {m} & (s.own0 | s.own1);{inc}\n"
+                    + self._clear_cells_code("cells", ind + "  ") + f" }}")
+        if t is n.PromoteEffect:                # reference effects.py:67-85
+            m = self.mask(e.mask)
+            sd = self.side(e.mover)
+            fr, to = self.piece_ids[e.from_piece], self.piece_ids[e.to_piece]
+            if self.piece_mode != "planes":
+                _fail("promotion needs piece-type planes")
+            lines = [f"{ind}{{ const BBW me = mover ? s.own1 : s.own0; const BBW op = mover ? s.own0 : s.own1;",
+                     f"{ind}  (void)me; (void)op;",
+                     f"{ind}  const BBW cells = {m} & {self.piece_bb(e.from_piece)} & {self.stones(self.side(e.mover)) if sd in ('mover', '(1 - mover)') else ('s.own1' if sd == '1' else 's.own0')};"]
+            if fr >= 1:
+                lines.append(f"{ind}  {{ const BBW pl = lx::andnot({self._plane(fr)}, cells); "
+                             f"{self._plane_set(fr, 'pl')} }}")
+            if to >= 1:
+                lines.append(f"{ind}  {{ const BBW pl = {self._plane(to)} | cells; {self._plane_set(to, 'pl')} }}")
+            lines.append(f"{ind}}}")
+            return "\n".join(lines)
+        if t is n.ExtraTurnEffect:              # reference effects.py:104-115
+            sd = self.side(e.who)
+            return f"{ind}s.ovr = {sd};" + (" s.samep = 1;" if e.same_piece else "")
         if t in (n.SetScoreEffect, n.IncrementScoreEffect):
             sd = self.side(e.who)
             fn = self.function(e.fn)

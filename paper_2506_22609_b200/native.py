@@ -30,7 +30,7 @@ class GameInfo(ctypes.Structure):
 REF_FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
               "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags",
               "last_mover", "last_kind", "last_source", "last_dest", "last_dest_by_player",
-              "comp_labels", "phase")
+              "comp_labels", "phase", "must_move")
 
 
 class RefState(ctypes.Structure):

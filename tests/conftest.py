@@ -11,6 +11,8 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath")
+MOVEMENT_GAMES = ("english_draughts", "dai_hasami_shogi", "wolf_and_sheep", "gridworld")
+ALL_GAMES = GAMES + MOVEMENT_GAMES
 
 
 def pytest_configure(config):
@@ -44,3 +46,54 @@ def golden_state(name, k):
 def game_text(name):
     with open(os.path.join(ROOT, "paper_2506_22609_b200", "games", f"{name}.ldx")) as f:
         return f.read()
+
+
+def ref_allocator(info):
+    """B -> reference-layout numpy arrays for a lowered game's state layout
+    (reference state.py:78-130)."""
+    C, L = info["C"], info["layout"]
+
+    def allocate(B):
+        s = {"board_piece": np.full((B, C), -1, np.int8),
+             "board_owner": np.full((B, C), -1, np.int8),
+             "current_player": np.zeros(B, np.int8), "move_count": np.zeros(B, np.int32),
+             "terminated": np.zeros(B, bool), "truncated": np.zeros(B, bool),
+             "outcome": np.full(B, -1, np.int8), "seeds": np.zeros(B, np.uint64)}
+        if L["scores"]:
+            s["scores"] = np.zeros((B, 2), np.int32)
+        if L["passing"]:
+            s["pass_streak"] = np.zeros(B, np.int16)
+            s["pass_flags"] = np.zeros((B, 2), bool)
+        if L["must_move"]:
+            s["must_move"] = np.full(B, -1, np.int16)
+        if L["last_action"]:
+            s["last_mover"] = np.full(B, -1, np.int8)
+            s["last_kind"] = np.full(B, -1, np.int8)
+            s["last_source"] = np.full(B, -1, np.int16)
+            s["last_dest"] = np.full(B, -1, np.int16)
+            s["last_dest_by_player"] = np.full((B, 2), -1, np.int16)
+        if L["connectivity"]:
+            s["comp_labels"] = np.full((B, 1, C), -1, np.int16)
+        if L["phase"]:
+            s["phase"] = np.zeros(B, np.int8)
+        return s
+    return allocate
+
+
+REF_FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
+              "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags",
+              "must_move", "last_mover", "last_kind", "last_source", "last_dest",
+              "last_dest_by_player", "hopped_mask", "captured_mask", "promoted_mask",
+              "comp_labels", "phase", "turn_pos")
+
+
+def ref_digest(arrays):
+    """reference GameState.digest (state.py:180-188) of a dict of arrays."""
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    for name in REF_FIELDS:
+        v = arrays.get(name)
+        if v is not None:
+            h.update(name.encode())
+            h.update(np.ascontiguousarray(v).tobytes())
+    return h.hexdigest()

@@ -25,6 +25,7 @@ struct RefOut {
     int8_t *last_mover, *last_kind;
     int16_t *last_source, *last_dest, *last_dest_by_player, *comp_labels;
     int8_t *phase;
+    int16_t *must_move;
 };
 
 static void export_one(const St& s, int64_t i, const RefOut* p) {
@@ -32,7 +33,7 @@ static void export_one(const St& s, int64_t i, const RefOut* p) {
         const int cb = Game::cell_bit(c);
         const bool a = lx::test(s.own0, cb), b = lx::test(s.own1, cb);
         p->board_owner[i * Game::C + c] = a ? 0 : (b ? 1 : -1);
-        p->board_piece[i * Game::C + c] = (a || b) ? 0 : -1;
+        p->board_piece[i * Game::C + c] = (a || b) ? (int8_t)Game::piece_at(s, cb) : -1;
     }
     p->current_player[i] = (int8_t)s.cur;
     p->move_count[i] = (int32_t)s.mc;
@@ -49,13 +50,28 @@ static void export_one(const St& s, int64_t i, const RefOut* p) {
     if (p->last_mover) {
         p->last_mover[i] = (int8_t)s.last_mover;
         p->last_kind[i] = (int8_t)s.last_kind;
-        p->last_source[i] = -1;
+        p->last_source[i] = (int16_t)s.last_source;
         p->last_dest[i] = (int16_t)s.last_dest;
         p->last_dest_by_player[2 * i] = (int16_t)s.ldbp0;
         p->last_dest_by_player[2 * i + 1] = (int16_t)s.ldbp1;
     }
     if (p->comp_labels) Game::labels(s, (short*)(p->comp_labels + i * Game::C));
     if (p->phase) p->phase[i] = (int8_t)s.phase;
+    if (p->must_move) p->must_move[i] = (int16_t)s.must_move;
+}
+
+// legal mask of the current mover (reference CompiledGame.legal_mask row)
+static void mask_row(const St& s, uint8_t* row) {
+    for (int a = 0; a < Game::A; a++) row[a] = 0;
+    if (s.term) return;
+    const int n = lx::legal_count<Game>(s);
+    if constexpr (Game::MECH == 0) {
+        lx::BB<Game::W> legal = Game::legal(s);
+        for (int c = 0; c < Game::C; c++) row[c] = lx::test(legal, Game::cell_bit(c));
+    } else {
+        Game::enum_moves(s, [&](int a) { row[a] = 1; });
+    }
+    if (Game::PASS >= 0) row[Game::PASS] = n == 0 && Game::force_pass(s.phase);
 }
 
 extern "C" {
@@ -69,9 +85,10 @@ int64_t sim_playout(int64_t B, const uint64_t* seeds, int max_turns, const RefOu
         lx::init_state<Game>(s, seeds[i]);
         const uint64_t smix = lx::seed_mix(s.seed);
         while (!s.term && (int)s.mc < max_turns) {
-            const int a = lx::sample_action<Game>(s, smix);
+            int hint;
+            const int a = lx::sample_action<Game>(s, smix, hint);
             if (a < 0) break;
-            lx::apply_step<Game>(s, a);
+            lx::apply_step<Game>(s, a, hint);
             u32 w[lx::Layout<Game>::NQ * 4];
             lx::pack<Game>(s, w);
             lx::unpack<Game>(s, w);
@@ -90,14 +107,32 @@ int sim_masks(uint64_t seed, int max_plies, uint8_t* masks, int64_t* actions) {
     const uint64_t smix = lx::seed_mix(s.seed);
     int t = 0;
     for (; t < max_plies && !s.term; t++) {
-        lx::BB<Game::W> legal = Game::legal(s);
-        for (int c = 0; c < Game::C; c++) masks[t * Game::A + c] = lx::test(legal, Game::cell_bit(c));
-        if (Game::PASS >= 0) masks[t * Game::A + Game::C] = !lx::any(legal) && Game::force_pass(s.phase);
-        const int a = lx::sample_action<Game>(s, smix);
+        mask_row(s, masks + (int64_t)t * Game::A);
+        int hint;
+        const int a = lx::sample_action<Game>(s, smix, hint);
         actions[t] = a;
         if (a < 0) break;
-        lx::apply_step<Game>(s, a);
+        lx::apply_step<Game>(s, a, hint);
     }
+    return t;
+}
+
+// scripted transcript from init(seed): per ply the mask before the move and
+// whether the action was legal (verify path, no hint); stops at the first
+// illegal action.  Exports the final state.  Returns plies applied.
+int sim_transcript(uint64_t seed, int n, const int64_t* actions, uint8_t* masks, uint8_t* legal,
+                   const RefOut* out) {
+    St s;
+    lx::init_state<Game>(s, seed);
+    int t = 0;
+    for (; t < n && !s.term; t++) {
+        mask_row(s, masks + (int64_t)t * Game::A);
+        legal[t] = lx::action_legal<Game>(s, actions[t]);
+        if (!legal[t]) break;
+        lx::apply_step<Game>(s, (int)actions[t]);
+    }
+    mask_row(s, masks + (int64_t)t * Game::A);
+    export_one(s, 0, out);
     return t;
 }
 

@@ -15,7 +15,7 @@ BUILD = os.path.join(HERE, "build")
 FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
           "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags",
           "last_mover", "last_kind", "last_source", "last_dest", "last_dest_by_player",
-          "comp_labels", "phase")
+          "comp_labels", "phase", "must_move")
 
 
 class _Ref(ctypes.Structure):
@@ -43,6 +43,10 @@ class HostGame:
         self.lib.sim_playout.restype = ctypes.c_int64
         self.lib.sim_playout.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
                                          ctypes.POINTER(_Ref)]
+        self.lib.sim_transcript.restype = ctypes.c_int
+        self.lib.sim_transcript.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.POINTER(_Ref)]
         self.lib.sim_masks.restype = ctypes.c_int
         self.lib.sim_masks.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p,
                                        ctypes.c_void_p]
@@ -62,3 +66,21 @@ class HostGame:
         a = np.zeros(max_plies, np.int64)
         t = self.lib.sim_masks(seed, max_plies, m.ctypes.data, a.ctypes.data)
         return m[:t].astype(bool), a[:t]
+
+    def transcript(self, actions, seed=0, layout_arrays=None):
+        """Apply scripted actions from init(batch_size=1, seed=seed) (the env
+        seed is spawn_seeds(seed, 1)[0], reference compiler.py:357-364);
+        returns (arrays, masks
+        (n+1, A) before each ply and after the last, legal flags, plies)."""
+        acts = np.ascontiguousarray(actions, dtype=np.int64)
+        n = len(acts)
+        A = self.info["A"]
+        m = np.zeros((n + 1, A), np.uint8)
+        ok = np.zeros(max(n, 1), np.uint8)
+        arrays = layout_arrays(1)
+        ref = _Ref(**{f: (arrays[f].ctypes.data if f in arrays else None) for f in FIELDS})
+        from paper_2506_22609_b200 import rng
+        env_seed = int(rng.spawn_seeds(seed, 1)[0])
+        t = self.lib.sim_transcript(env_seed, n, acts.ctypes.data, m.ctypes.data, ok.ctypes.data,
+                                    ctypes.byref(ref))
+        return arrays, m.astype(bool), ok[:n].astype(bool), t
