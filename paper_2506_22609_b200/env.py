@@ -108,7 +108,7 @@ class LudaxEnvironment:
         return self._launch(state.game_state, a, out)
 
     def observe(self, state, player=None):
-        """(B, 3, C) bool planes for ``player`` (default: each row's mover is
+        """(B, 2T+1, C) bool planes for ``player`` (default: each row's mover is
         not batched -- pass a player id) (compiler.py:611-626)."""
         p = 0 if player is None else int(player)
         return self.game.observe_device(state.game_state, p)
