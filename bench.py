@@ -31,7 +31,11 @@ sys.path.insert(0, ROOT)
 METRIC = "env steps/sec (uniform-random rollouts) vs batch size at 1/2/4/8 B200"
 UNIT = "env_steps/s"
 GAME_FILES = {"connect_four": "Connect Four 6x7", "tic_tac_toe": "Tic-Tac-Toe",
-              "hex": "Hex 11x11", "reversi": "Reversi 8x8", "pente": "Pente 19x19"}
+              "hex": "Hex 11x11", "reversi": "Reversi 8x8", "pente": "Pente 19x19",
+              "gomoku": "Gomoku 15x15", "yavalath": "Yavalath (hexagon 9)",
+              "english_draughts": "English Draughts 8x8",
+              "dai_hasami_shogi": "Dai Hasami Shogi 9x9", "wolf_and_sheep": "Wolf and Sheep 8x8",
+              "gridworld": "Frozen Lake gridworld 4x4"}
 
 
 def parse():

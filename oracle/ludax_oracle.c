@@ -3,7 +3,10 @@
  *
  * A scalar, cell-array restatement of the reference's rollout hot path
  * (reference: /root/reference/pkg/src/boardlang/, the numpy "boardlang"
- * re-implementation of Ludax) for the five config games.  It works on the
+ * re-implementation of Ludax) for the eleven corpus games: placement games
+ * (mechanics.py:415-515) and, in the movement section below, the movement /
+ * gridworld games (mechanics.py:44-404, 518-608) with their per-source count
+ * formulation of legality and sampling.  It works on the
  * reference's own structure-of-arrays GameState layout (state.py:78-130:
  * int8 boards with -1 = empty, int32 move_count, ...), so its outputs can be
  * hashed with the reference's digest and compared field by field.
@@ -26,7 +29,12 @@
 enum { FAM_GRID = 0, FAM_HEXRECT = 1, FAM_HEXAGON = 2 };
 enum { DEST_EMPTY = 0, DEST_C4 = 1, DEST_CENTER = 2 };
 enum { EFF_NONE = 0, EFF_REVERSI = 1, EFF_PENTE = 2 };
-enum { END_LINE = 0, END_FULL = 1, END_CONN = 2, END_PASSED_BOTH = 3, END_SCORE_GE = 4, END_LINE_LOSE = 5 };
+enum { END_LINE = 0, END_FULL = 1, END_CONN = 2, END_PASSED_BOTH = 3, END_SCORE_GE = 4, END_LINE_LOSE = 5,
+       END_NO_LEGAL = 6, END_LAST_MOVE_IN = 7, END_LINE_EXCL = 8 };
+enum { MECH_PLACE = 0, MECH_MOVE = 1, MECH_GRID = 2 };
+enum { K_PLACE = 0, K_STEP = 1, K_HOP = 2, K_SLIDE = 3, K_PASS = 4 };    /* state.py:23-31 */
+enum { OVER_ANY = 0, OVER_OPP = 1, OVER_MOVER = 2 };
+#define MAXG 16
 enum { RES_MOVER_WIN = 0, RES_DRAW = 1, RES_BY_SCORE = 2, RES_MOVER_LOSE = 3 };
 enum { ST_OK = 0, ST_ILLEGAL = 1, ST_TERMINAL = 2, ST_EMPTY_MASK = 3 };
 
@@ -71,6 +79,17 @@ typedef struct {
     int ncust;
     int cust_dir[8];
     int ray_max;                   /* stacked ray length L (exprs.py:386-396) */
+    /* movement games (compiler.py:311-327; mechanics.py:44-82) */
+    int mech, L_must, needs_next, multi_prio;
+    int ng;
+    struct { int kind, piece, prio, d[2], over, capture, L; } grp[MAXG];
+    int nstart, start_cell[64], start_player[64], start_piece[64];
+    int promote, promote_from, promote_to;                 /* (promote a b (edge forward)) */
+    int extra_hop;                 /* (if (and (action_was mover hop) (can_move_again hop)) (extra_turn mover same_piece:true)) */
+    int cap_custodial, corner_cust;                        /* Dai Hasami Shogi effects */
+    int ncorner, corner[4][3];
+    uint8_t end_mask[4][MAXC];     /* last_move_in masks / line exclusions per end rule */
+    int grid_piece, grid_ndir, grid_dir[8];
 } orc_game;
 
 typedef struct {
@@ -85,6 +104,7 @@ typedef struct {
     int8_t *last_mover, *last_kind;
     int16_t *last_source, *last_dest, *last_dest_by_player, *comp_labels;
     int8_t *phase;
+    int16_t *must_move;
 } orc_soa;
 
 static const char *GRID_DIRS[8] = {"up", "down", "left", "right", "up_left", "up_right",
@@ -183,11 +203,31 @@ static int build_lines(orc_game *g, int len, int exact) {
     return t;
 }
 
-static void build_custodial(orc_game *g) {
+/* windows along explicit grid axes (orientation "orthogonal": right, down) */
+static int build_lines_axes(orc_game *g, int len, int naxes, const char **axes, const char **inv) {
+    int t = g->nlt++;
+    g->lt[t].len = len; g->lt[t].nwin = 0; g->lt[t].exact = 0;
+    for (int a = 0; a < naxes; a++) {
+        int d = dir_index_grid(axes[a]), di = dir_index_grid(inv[a]);
+        for (int s = 0; s < g->C; s++) {
+            int cells[8], k = 1; cells[0] = s;
+            while (k < len && g->nbr[d][cells[k - 1]] != g->C) { cells[k] = g->nbr[d][cells[k - 1]]; k++; }
+            if (k == len) {
+                int w = g->lt[t].nwin++;
+                for (int j = 0; j < len; j++) g->lt[t].win[w][j] = (int16_t)cells[j];
+                g->lt[t].before[w] = g->nbr[di][s];
+                g->lt[t].after[w] = g->nbr[d][cells[len - 1]];
+            }
+        }
+    }
+    return t;
+}
+
+static void build_custodial_n(orc_game *g, int naxes) {
     static const char *axes[4] = {"right", "down", "down_right", "down_left"};
     static const char *inv[4] = {"left", "up", "up_left", "up_right"};
     g->ncust = 0;
-    for (int a = 0; a < 4; a++) {
+    for (int a = 0; a < naxes; a++) {
         g->cust_dir[g->ncust++] = dir_index_grid(axes[a]);
         g->cust_dir[g->ncust++] = dir_index_grid(inv[a]);
     }
@@ -196,6 +236,114 @@ static void build_custodial(orc_game *g) {
         int l = ray_len(g, g->cust_dir[i]);
         if (l > g->ray_max) g->ray_max = l;
     }
+}
+
+static void build_custodial(orc_game *g) { build_custodial_n(g, 4); }
+
+static void add_group(orc_game *g, int kind, int piece, int prio, const char *d1, const char *d2,
+                      int over, int capture) {
+    int k = g->ng++;
+    g->grp[k].kind = kind; g->grp[k].piece = piece; g->grp[k].prio = prio;
+    g->grp[k].d[0] = dir_index_grid(d1); g->grp[k].d[1] = dir_index_grid(d2);
+    g->grp[k].over = over; g->grp[k].capture = capture;
+    int l0 = ray_len(g, g->grp[k].d[0]), l1 = ray_len(g, g->grp[k].d[1]);
+    if (l0 < 1) l0 = 1;
+    if (l1 < 1) l1 = 1;
+    g->grp[k].L = l0 > l1 ? l0 : l1;                  /* mechanics.py:67-80 (distance 0) */
+    if (k > 0 && g->grp[k].prio != g->grp[0].prio) g->multi_prio = 1;
+}
+
+static void add_start(orc_game *g, int player, int piece, const int *cells, int n) {
+    for (int j = 0; j < n; j++) {
+        g->start_cell[g->nstart] = cells[j]; g->start_player[g->nstart] = player;
+        g->start_piece[g->nstart] = piece; g->nstart++;
+    }
+}
+
+static const char *DIAG[4] = {"up_left", "up_right", "down_left", "down_right"};
+static const char *ORTH[4] = {"up", "down", "left", "right"};
+
+/* movement corpus games: groups in the reference's order (compiler.py:311-327;
+   direction_pairs, mechanics.py:25-41) */
+static int new_movement_game(orc_game *g, const char *name) {
+    if (!strcmp(name, "english_draughts")) {          /* games/english_draughts.ldx */
+        static const int p1[12] = {40, 42, 44, 46, 49, 51, 53, 55, 56, 58, 60, 62};
+        static const int p2[12] = {1, 3, 5, 7, 8, 10, 12, 14, 17, 19, 21, 23};
+        g->game = 10; build_topology(g, FAM_GRID, 8, 8); g->mech = MECH_MOVE;
+        add_start(g, 0, 0, p1, 12); add_start(g, 1, 0, p2, 12);
+        /* pawn forward_left / forward_right: P1 up -> up_left/up_right, P2 down -> down_right/down_left */
+        add_group(g, K_HOP, 0, 0, "up_left", "down_right", OVER_OPP, 1);
+        add_group(g, K_HOP, 0, 0, "up_right", "down_left", OVER_OPP, 1);
+        add_group(g, K_STEP, 0, 1, "up_left", "down_right", OVER_ANY, 0);
+        add_group(g, K_STEP, 0, 1, "up_right", "down_left", OVER_ANY, 0);
+        for (int k = 0; k < 4; k++) add_group(g, K_HOP, 1, 0, DIAG[k], DIAG[k], OVER_OPP, 1);
+        for (int k = 0; k < 4; k++) add_group(g, K_STEP, 1, 1, DIAG[k], DIAG[k], OVER_ANY, 0);
+        g->promote = 1; g->promote_from = 0; g->promote_to = 1;
+        g->extra_hop = 1;
+        g->L_must = 1; g->L_last = 1; g->needs_next = 1;
+        g->nend = 1;
+        g->end_kind[0] = END_NO_LEGAL; g->end_res[0] = RES_MOVER_WIN;
+    } else if (!strcmp(name, "dai_hasami_shogi")) {   /* games/dai_hasami_shogi.ldx */
+        int p1[18], p2[18];
+        for (int k = 0; k < 18; k++) { p1[k] = 63 + k; p2[k] = k; }
+        g->game = 11; build_topology(g, FAM_GRID, 9, 9); g->mech = MECH_MOVE;
+        add_start(g, 0, 0, p1, 18); add_start(g, 1, 0, p2, 18);
+        for (int k = 0; k < 4; k++) add_group(g, K_SLIDE, 0, 0, ORTH[k], ORTH[k], OVER_ANY, 0);
+        for (int k = 0; k < 4; k++) add_group(g, K_HOP, 0, 0, ORTH[k], ORTH[k], OVER_ANY, 0);
+        build_custodial_n(g, 2);                     /* orientation orthogonal: right, down */
+        g->cap_custodial = 1; g->corner_cust = 1;
+        /* corners top_left, top_right, bottom_left, bottom_right with their
+           (up, down, left, right) neighbours (exprs.py:381-392) */
+        static const int cs[4] = {0, 8, 72, 80};
+        for (int k = 0; k < 4; k++) {
+            int c = cs[k], m = 0;
+            g->corner[k][0] = c;
+            for (int d = 0; d < 4; d++) if (g->nbr[d][c] != g->C) g->corner[k][1 + m++] = g->nbr[d][c];
+        }
+        g->ncorner = 4;
+        g->L_last = 1;
+        static const char *ax[2] = {"right", "down"}, *iv[2] = {"left", "up"};
+        build_lines_axes(g, 5, 2, ax, iv);
+        g->nend = 2;
+        g->end_kind[0] = END_LINE_EXCL; g->end_arg[0] = 0; g->end_gate[0] = 0; g->end_res[0] = RES_MOVER_WIN;
+        g->end_kind[1] = END_LINE_EXCL; g->end_arg[1] = 0; g->end_gate[1] = 1; g->end_res[1] = RES_MOVER_WIN;
+        for (int c = 0; c < g->C; c++) {
+            int r = c / 9;
+            g->end_mask[0][c] = r == 7 || r == 8;     /* exclude:((row 7) (row 8)) */
+            g->end_mask[1][c] = r == 0 || r == 1;
+        }
+    } else if (!strcmp(name, "wolf_and_sheep")) {     /* games/wolf_and_sheep.ldx */
+        static const int sheep[4] = {56, 58, 60, 62}, wolf[1] = {3};
+        g->game = 12; build_topology(g, FAM_GRID, 8, 8); g->mech = MECH_MOVE;
+        add_start(g, 0, 0, sheep, 4); add_start(g, 1, 1, wolf, 1);
+        add_group(g, K_STEP, 0, 0, "up_left", "down_right", OVER_ANY, 0);
+        add_group(g, K_STEP, 0, 0, "up_right", "down_left", OVER_ANY, 0);
+        for (int k = 0; k < 4; k++) add_group(g, K_STEP, 1, 0, DIAG[k], DIAG[k], OVER_ANY, 0);
+        g->L_last = 1; g->needs_next = 1;
+        g->nend = 2;
+        g->end_kind[0] = END_LAST_MOVE_IN; g->end_gate[0] = 1; g->end_res[0] = RES_MOVER_WIN;
+        for (int c = 0; c < g->C; c++) g->end_mask[0][c] = g->edge[1][c];     /* edge bottom */
+        g->end_kind[1] = END_NO_LEGAL; g->end_res[1] = RES_MOVER_WIN;
+    } else if (!strcmp(name, "gridworld")) {          /* games/gridworld.ldx */
+        static const int walker[1] = {0};
+        g->game = 13; build_topology(g, FAM_GRID, 4, 4); g->mech = MECH_GRID;
+        add_start(g, 0, 0, walker, 1);
+        g->olen[0] = 1; g->order[0][0] = 0;            /* (repeat (P1)) */
+        g->grid_piece = 0; g->grid_ndir = 4;
+        for (int k = 0; k < 4; k++) g->grid_dir[k] = k; /* up, down, left, right */
+        g->L_last = 1;
+        g->nend = 2;
+        g->end_kind[0] = END_LAST_MOVE_IN; g->end_gate[0] = -1; g->end_res[0] = RES_MOVER_WIN;
+        g->end_mask[0][15] = 1;                         /* region target */
+        g->end_kind[1] = END_LAST_MOVE_IN; g->end_gate[1] = -1; g->end_res[1] = RES_MOVER_LOSE;
+        g->end_mask[1][5] = g->end_mask[1][7] = g->end_mask[1][11] = g->end_mask[1][12] = 1;
+    } else {
+        return 0;
+    }
+    if (g->mech == MECH_MOVE) g->A = g->C * g->C;
+    else g->A = g->grid_ndir;
+    g->pass_index = -1;
+    return 1;
 }
 
 orc_game *orc_game_new(const char *name) {
@@ -250,6 +398,7 @@ orc_game *orc_game_new(const char *name) {
         g->end_kind[1] = END_LINE_LOSE; g->end_arg[1] = 1; g->end_anch[1] = 1; g->end_res[1] = RES_MOVER_LOSE;
         g->end_kind[2] = END_FULL; g->end_res[2] = RES_DRAW;
     } else {
+        if (new_movement_game(g, name)) return g;
         free(g);
         return NULL;
     }
@@ -261,10 +410,12 @@ orc_game *orc_game_new(const char *name) {
 void orc_game_free(orc_game *g) { free(g); }
 int orc_num_cells(const orc_game *g) { return g->C; }
 int orc_num_actions(const orc_game *g) { return g->A; }
-/* layout bits: 1 scores, 2 passing, 4 last_action, 8 connectivity, 16 phase */
+/* layout bits: 1 scores, 2 passing, 4 last_action, 8 connectivity, 16 phase, 32 must_move */
 int orc_layout(const orc_game *g) {
-    return g->L_scores | (g->L_passing << 1) | (g->L_last << 2) | (g->L_conn << 3) | (g->L_phase << 4);
+    return g->L_scores | (g->L_passing << 1) | (g->L_last << 2) | (g->L_conn << 3) | (g->L_phase << 4)
+        | (g->L_must << 5);
 }
+int orc_mechanics(const orc_game *g) { return g->mech; }
 
 /* --- per-env views --------------------------------------------------------- */
 typedef struct { const orc_game *g; orc_soa *s; int64_t i; int8_t *own; int8_t *pc; } env_t;
@@ -515,6 +666,309 @@ static int step_one(env_t *e, int64_t action, int verify, uint8_t *scratch) {
     return ST_OK;
 }
 
+/* --- movement / gridworld (mechanics.py:44-404, 518-608) --------------------- */
+
+static inline int must_of(const env_t *e) { return e->s->must_move ? e->s->must_move[e->i] : -1; }
+
+/* MovementMechanics._src_ok (mechanics.py:116-126) */
+static inline int mv_src_ok(const env_t *e, int mover, int piece, int c, int use_must) {
+    if (e->pc[c] != piece || e->own[c] != mover) return 0;
+    if (use_must && e->g->L_must) { int mm = must_of(e); if (mm >= 0 && c != mm) return 0; }
+    return 1;
+}
+
+static inline int mv_over_ok(const env_t *e, int gi, int mover, int mid) {
+    const orc_game *g = e->g;
+    if (mid == g->C) return 0;
+    int mo = e->own[mid];
+    if (mo < 0) return 0;
+    if (g->grp[gi].over == OVER_OPP && mo != 1 - mover) return 0;
+    if (g->grp[gi].over == OVER_MOVER && mo != mover) return 0;
+    return 1;
+}
+
+/* per-source legal counts of one group (MovementMechanics.compute,
+   mechanics.py:134-187); returns the group total */
+static int mv_group_counts(const env_t *e, int gi, int mover, int16_t *cnt) {
+    const orc_game *g = e->g;
+    int C = g->C, d = g->grp[gi].d[mover], total = 0;
+    for (int c = 0; c < C; c++) {
+        int n = 0;
+        if (mv_src_ok(e, mover, g->grp[gi].piece, c, 1)) {
+            if (g->grp[gi].kind == K_STEP) {
+                int x = g->nbr[d][c];
+                n = x != C && e->own[x] < 0;
+            } else if (g->grp[gi].kind == K_HOP) {
+                int mid = g->nbr[d][c], two = mid != C ? g->nbr[d][mid] : C;
+                n = mv_over_ok(e, gi, mover, mid) && two != C && e->own[two] < 0;
+            } else {
+                int x = g->nbr[d][c];
+                for (int k = 0; k < g->grp[gi].L && x != C && e->own[x] < 0; k++) { n++; x = g->nbr[d][x]; }
+            }
+        }
+        if (cnt) cnt[c] = (int16_t)n;
+        total += n;
+    }
+    return total;
+}
+
+/* group totals with move priority (mechanics.py:188-197); returns the sum */
+static int mv_compute(const env_t *e, int mover, int *tot) {
+    const orc_game *g = e->g;
+    int minp = 1000000, n = 0;
+    for (int gi = 0; gi < g->ng; gi++) {
+        tot[gi] = mv_group_counts(e, gi, mover, NULL);
+        if (tot[gi] > 0 && g->grp[gi].prio < minp) minp = g->grp[gi].prio;
+    }
+    for (int gi = 0; gi < g->ng; gi++) {
+        if (g->multi_prio && g->grp[gi].prio != minp) tot[gi] = 0;
+        n += tot[gi];
+    }
+    return n;
+}
+
+static int mv_dest(const orc_game *g, int gi, int mover, int src, int k) {
+    int d = g->grp[gi].d[mover], x = g->nbr[d][src];
+    if (g->grp[gi].kind == K_HOP) return g->nbr[d][x];
+    for (int j = 0; j < k; j++) x = g->nbr[d][x];      /* slide: k-th reach cell */
+    return x;
+}
+
+/* GridworldMechanics (mechanics.py:529-548): the walker is the first cell
+   holding the mover's walker (argmax -> 0 when none) */
+static int gw_src(const env_t *e, int mover) {
+    for (int c = 0; c < e->g->C; c++)
+        if (e->pc[c] == e->g->grid_piece && e->own[c] == mover) return c;
+    return 0;
+}
+static int gw_compute(const env_t *e, int mover, int *ok) {
+    const orc_game *g = e->g;
+    int src = gw_src(e, mover), n = 0;
+    for (int k = 0; k < g->grid_ndir; k++) {
+        int x = g->nbr[g->grid_dir[k]][src];
+        ok[k] = x != g->C && e->own[x] < 0;
+        n += ok[k];
+    }
+    return n;
+}
+
+/* number of legal actions of `mover` (without pass) */
+static int mv_count(const env_t *e, int mover) {
+    int tot[MAXG];
+    return e->g->mech == MECH_GRID ? gw_compute(e, mover, tot) : mv_compute(e, mover, tot);
+}
+
+/* legal mask row (full_mask, mechanics.py:234-266 / 564-568) */
+static void mv_mask(const env_t *e, int mover, uint8_t *row) {
+    const orc_game *g = e->g;
+    int tot[MAXG];
+    memset(row, 0, g->A);
+    if (g->mech == MECH_GRID) { gw_compute(e, mover, tot); for (int k = 0; k < g->grid_ndir; k++) row[k] = tot[k]; return; }
+    mv_compute(e, mover, tot);
+    int16_t cnt[MAXC];
+    for (int gi = 0; gi < g->ng; gi++) {
+        if (!tot[gi]) continue;
+        mv_group_counts(e, gi, mover, cnt);
+        for (int c = 0; c < g->C; c++)
+            for (int k = 0; k < cnt[c]; k++)
+                row[c * g->C + mv_dest(g, gi, mover, c, k)] = 1;
+    }
+}
+
+/* MovementMechanics.sample (mechanics.py:199-232) */
+static int64_t mv_sample(const env_t *e, int mover, double u) {
+    const orc_game *g = e->g;
+    int tot[MAXG];
+    int n = g->mech == MECH_GRID ? gw_compute(e, mover, tot) : mv_compute(e, mover, tot);
+    if (n == 0) return -1;
+    int64_t r = (int64_t)(u * (double)n);
+    if (r > n - 1) r = n - 1;
+    int ng = g->mech == MECH_GRID ? g->grid_ndir : g->ng;
+    for (int gi = 0; gi < ng; gi++) {
+        if (r >= tot[gi]) { r -= tot[gi]; continue; }
+        if (g->mech == MECH_GRID) return gi;
+        int16_t cnt[MAXC];
+        mv_group_counts(e, gi, mover, cnt);
+        for (int c = 0; c < g->C; c++) {
+            if (r < cnt[c]) return (int64_t)c * g->C + mv_dest(g, gi, mover, c, (int)r);
+            r -= cnt[c];
+        }
+    }
+    return -1;
+}
+
+/* first group claiming (src, dst) (MovementMechanics.apply, mechanics.py:283-322) */
+static int mv_claim(const env_t *e, int mover, int src, int dst) {
+    const orc_game *g = e->g;
+    int C = g->C;
+    for (int gi = 0; gi < g->ng; gi++) {
+        if (!mv_src_ok(e, mover, g->grp[gi].piece, src, 1)) continue;
+        int d = g->grp[gi].d[mover], match = 0;
+        if (g->grp[gi].kind == K_STEP) {
+            match = g->nbr[d][src] == dst && e->own[dst] < 0;
+        } else if (g->grp[gi].kind == K_HOP) {
+            int mid = g->nbr[d][src], two = mid != C ? g->nbr[d][mid] : C;
+            match = two == dst && mv_over_ok(e, gi, mover, mid) && e->own[dst] < 0;
+        } else {
+            int pos = g->nbr[d][src], clear = 1;
+            for (int k = 0; k < g->grp[gi].L; k++) {
+                clear = clear && pos != C && e->own[pos] < 0;
+                if (clear && pos == dst) match = 1;
+                pos = pos != C ? g->nbr[d][pos] : C;
+            }
+        }
+        if (match) return gi;
+    }
+    return -1;
+}
+
+static int mv_legal_action(const env_t *e, int mover, int64_t a) {
+    const orc_game *g = e->g;
+    if (g->mech == MECH_GRID) {
+        int ok[8];
+        gw_compute(e, mover, ok);
+        return a >= 0 && a < g->grid_ndir && ok[a];
+    }
+    if (a < 0 || a >= (int64_t)g->C * g->C) return 0;
+    int gi = mv_claim(e, mover, (int)(a / g->C), (int)(a % g->C));
+    if (gi < 0) return 0;
+    if (g->multi_prio) {                               /* mechanics.py:329-338 */
+        int minp = 1000000;
+        for (int k = 0; k < g->ng; k++)
+            if (mv_group_counts(e, k, mover, NULL) > 0 && g->grp[k].prio < minp) minp = g->grp[k].prio;
+        if (g->grp[gi].prio > minp) return 0;
+    }
+    return 1;
+}
+
+/* MovementMechanics.can_move_again (mechanics.py:368-403) */
+static int mv_can_move_again(const env_t *e, int mover, int kind) {
+    const orc_game *g = e->g;
+    orc_soa *s = e->s;
+    int ld = s->last_dest[e->i];
+    if (!(ld >= 0 && s->last_mover[e->i] == mover)) return 0;
+    for (int gi = 0; gi < g->ng; gi++) {
+        if (g->grp[gi].kind != kind) continue;
+        if (!mv_src_ok(e, mover, g->grp[gi].piece, ld, 0)) continue;
+        int d = g->grp[gi].d[mover], x = g->nbr[d][ld];
+        if (kind == K_HOP) {
+            int two = x != g->C ? g->nbr[d][x] : g->C;
+            if (mv_over_ok(e, gi, mover, x) && two != g->C && e->own[two] < 0) return 1;
+        } else if (x != g->C && e->own[x] < 0) {
+            return 1;
+        }
+    }
+    return 0;
+}
+
+static inline void set_last(orc_soa *s, int64_t i, int kind, int src, int dst, int mover) {
+    if (!s->last_kind) return;
+    s->last_kind[i] = (int8_t)kind; s->last_source[i] = (int16_t)src; s->last_dest[i] = (int16_t)dst;
+    s->last_mover[i] = (int8_t)mover; s->last_dest_by_player[i * 2 + mover] = (int16_t)dst;
+}
+
+/* CompiledGame.step_into for one live row of a movement / gridworld game
+   (compiler.py:456-580) */
+static void mv_step_one(env_t *e, int64_t action) {
+    const orc_game *g = e->g;
+    orc_soa *s = e->s;
+    int64_t i = e->i;
+    int C = g->C, mover = s->current_player[i];
+    int ovr = -1, samep = 0;
+    if (g->mech == MECH_GRID) {                        /* mechanics.py:570-602 */
+        int src = gw_src(e, mover), ok[8];
+        gw_compute(e, mover, ok);
+        if (action >= 0 && action < g->grid_ndir && ok[action]) {
+            int dst = g->nbr[g->grid_dir[action]][src];
+            e->pc[dst] = (int8_t)g->grid_piece; e->own[dst] = (int8_t)mover;
+            e->pc[src] = -1; e->own[src] = -1;
+            set_last(s, i, K_STEP, src, dst, mover);
+        }
+    } else {
+        int src = (int)(action / C), dst = (int)(action % C);
+        int gi = mv_claim(e, mover, src, dst);
+        if (gi >= 0) {
+            int8_t pv = e->pc[src], ov = e->own[src];
+            e->pc[src] = -1; e->own[src] = -1;
+            e->pc[dst] = pv; e->own[dst] = ov;
+            if (g->grp[gi].kind == K_HOP && g->grp[gi].capture) {
+                int mid = g->nbr[g->grp[gi].d[mover]][src];
+                e->pc[mid] = -1; e->own[mid] = -1;
+            }
+            set_last(s, i, g->grp[gi].kind, src, dst, mover);
+        }
+        /* effects in order (effects.py) */
+        if (g->promote) {                              /* (promote pawn king (edge forward)) */
+            int edge = mover == 0 ? 0 : 1;             /* P1 forward up -> top, P2 down -> bottom */
+            for (int c = 0; c < C; c++)
+                if (g->edge[edge][c] && e->pc[c] == g->promote_from && e->own[c] == mover)
+                    e->pc[c] = (int8_t)g->promote_to;
+        }
+        if (g->extra_hop) {
+            if (s->last_mover[i] == mover && s->last_kind[i] == K_HOP && mv_can_move_again(e, mover, K_HOP)) {
+                ovr = mover; samep = 1;
+            }
+        }
+        if (g->cap_custodial) {                        /* anchored custodial, any length */
+            int16_t mark[64];
+            int ld = s->last_dest[i];
+            int m = (ld >= 0 && s->last_mover[i] == mover) ? custodial_from(e, ld, mover, 0, mark) : 0;
+            for (int k = 0; k < m; k++) if (e->own[mark[k]] >= 0) { e->own[mark[k]] = -1; e->pc[mark[k]] = -1; }
+        }
+        if (g->corner_cust) {                          /* exprs.py:381-408, anchored */
+            int ld = s->last_dest[i], hit[4];
+            for (int k = 0; k < g->ncorner; k++) {
+                int c = g->corner[k][0], n1 = g->corner[k][1], n2 = g->corner[k][2];
+                hit[k] = e->own[c] == 1 - mover && e->pc[c] == 0 && e->own[n1] == mover && e->own[n2] == mover
+                         && (ld == n1 || ld == n2) && s->last_mover[i] == mover;
+            }
+            for (int k = 0; k < g->ncorner; k++)
+                if (hit[k]) { int c = g->corner[k][0]; e->own[c] = -1; e->pc[c] = -1; }
+        }
+    }
+    /* advancement + extra-turn override + must_move (compiler.py:528-545) */
+    int phase = phase_of(e), pos = 0;
+    for (int k = 0; k < g->olen[phase]; k++) if (g->order[phase][k] == mover) { pos = k; break; }
+    int nxt = pos + 1, next_phase = phase, next_pos = nxt;
+    if (nxt >= g->olen[phase]) { next_pos = 0; if (g->once[phase]) next_phase = phase + 1; }
+    int next_player = next_phase < g->nphase ? g->order[next_phase][next_pos] : 0;
+    if (ovr >= 0) { next_player = ovr; next_phase = phase; }
+    if (s->must_move) s->must_move[i] = (int16_t)((ovr >= 0 && samep) ? s->last_dest[i] : -1);
+    int next_count = 0;
+    if (g->needs_next) next_count = mv_count(e, next_player);
+    for (int r = 0; r < g->nend; r++) {
+        int fired = 0;
+        switch (g->end_kind[r]) {
+        case END_NO_LEGAL: fired = next_count == 0; break;
+        case END_LAST_MOVE_IN: {
+            int ld = s->last_dest[i];
+            fired = (g->end_gate[r] < 0 || mover == g->end_gate[r]) && ld >= 0
+                    && s->last_mover[i] == mover && g->end_mask[r][ld];
+        } break;
+        case END_LINE_EXCL: {                          /* global line, exprs.py:433-450 */
+            if (mover != g->end_gate[r]) break;
+            int t = g->end_arg[r];
+            for (int w = 0; w < g->lt[t].nwin && !fired; w++) {
+                int ok = 1;
+                for (int j = 0; j < g->lt[t].len && ok; j++) {
+                    int c = g->lt[t].win[w][j];
+                    ok = e->own[c] == mover && e->pc[c] == 0 && !g->end_mask[r][c];
+                }
+                fired = ok;
+            }
+        } break;
+        }
+        if (fired) {
+            s->outcome[i] = (int8_t)(g->end_res[r] == RES_MOVER_WIN ? 1 + mover : 2 - mover);
+            s->terminated[i] = 1;
+            break;
+        }
+    }
+    s->move_count[i] += 1;
+    s->current_player[i] = (int8_t)next_player;
+    if (s->phase) s->phase[i] = (int8_t)next_phase;
+}
+
 /* --- exported API ----------------------------------------------------------- */
 
 /* CompiledGame.init (compiler.py:329-364): start template broadcast + seeds */
@@ -533,6 +987,11 @@ void orc_init(const orc_game *g, orc_soa *s, int64_t B, const uint64_t *seeds) {
         }
         if (s->comp_labels) for (int c = 0; c < g->C; c++) s->comp_labels[i * g->C + c] = -1;
         if (s->phase) s->phase[i] = 0;
+        if (s->must_move) s->must_move[i] = -1;
+        for (int k = 0; k < g->nstart; k++) {
+            e.own[g->start_cell[k]] = (int8_t)g->start_player[k];
+            e.pc[g->start_cell[k]] = (int8_t)g->start_piece[k];
+        }
         if (g->game == 3) {                                    /* reversi.ldx start */
             e.own[28] = 0; e.own[35] = 0; e.own[27] = 1; e.own[36] = 1;
             e.pc[28] = e.pc[35] = e.pc[27] = e.pc[36] = 0;
@@ -553,6 +1012,12 @@ void orc_legal(const orc_game *g, orc_soa *s, int64_t B, uint8_t *mask, int64_t 
     uint8_t cells[MAXC];
     for (int64_t i = 0; i < B; i++) {
         env_t e = env_of(g, s, i);
+        if (g->mech != MECH_PLACE) {
+            int term = s->terminated[i];
+            if (mask) { if (term) memset(mask + i * g->A, 0, g->A); else mv_mask(&e, s->current_player[i], mask + i * g->A); }
+            if (counts) counts[i] = term ? 0 : mv_count(&e, s->current_player[i]);
+            continue;
+        }
         int64_t t = legal_count_and_mask(&e, cells, mask ? mask + i * g->A : NULL);
         if (counts) counts[i] = t;
     }
@@ -563,6 +1028,7 @@ void orc_sample(const orc_game *g, orc_soa *s, int64_t B, const double *u, int64
     for (int64_t i = 0; i < B; i++) {
         env_t e = env_of(g, s, i);
         double ui = u ? u[i] : uniform2(s->seeds[i], (uint64_t)s->move_count[i]);
+        if (g->mech != MECH_PLACE) { actions[i] = s->terminated[i] ? -1 : mv_sample(&e, s->current_player[i], ui); continue; }
         actions[i] = sample_one(&e, ui, cells);
     }
 }
@@ -578,6 +1044,10 @@ int orc_step(const orc_game *g, orc_soa *s, int64_t B, const int64_t *actions,
             env_t e = env_of(g, s, i);
             int mover = s->current_player[i], p = phase_of(&e);
             int64_t a = actions[i];
+            if (g->mech != MECH_PLACE) {
+                if (!mv_legal_action(&e, mover, a)) { if (bad_row) *bad_row = i; return ST_ILLEGAL; }
+                continue;
+            }
             int n = legal_cells(&e, mover, cells);
             int ok = (g->has_pass && a == g->pass_index) ? (n == 0 && g->force_pass[p])
                                                           : (a >= 0 && a < g->C && cells[a]);
@@ -587,7 +1057,8 @@ int orc_step(const orc_game *g, orc_soa *s, int64_t B, const int64_t *actions,
     for (int64_t i = 0; i < B; i++) {
         if (s->terminated[i] || (rows && !rows[i])) continue;
         env_t e = env_of(g, s, i);
-        step_one(&e, actions[i], 0, cells);
+        if (g->mech != MECH_PLACE) mv_step_one(&e, actions[i]);
+        else step_one(&e, actions[i], 0, cells);
     }
     return ST_OK;
 }
@@ -601,9 +1072,11 @@ static int64_t playout_range(const orc_game *g, orc_soa *s, int64_t lo, int64_t 
         env_t e = env_of(g, s, i);
         while (!s->terminated[i] && s->move_count[i] < max_turns) {
             double u = uniform2(s->seeds[i], (uint64_t)s->move_count[i]);
-            int64_t a = sample_one(&e, u, cells);
+            int64_t a = g->mech != MECH_PLACE ? mv_sample(&e, s->current_player[i], u)
+                                              : sample_one(&e, u, cells);
             if (a < 0) { if (stuck_row && *stuck_row < 0) *stuck_row = i; break; }
-            step_one(&e, a, 0, cells);
+            if (g->mech != MECH_PLACE) mv_step_one(&e, a);
+            else step_one(&e, a, 0, cells);
             steps++;
         }
         if (!s->terminated[i]) { s->terminated[i] = 1; s->truncated[i] = 1; s->outcome[i] = 0; }

@@ -25,7 +25,8 @@ FIELDS = ("board_piece", "board_owner", "current_player", "move_count",
           "last_dest", "last_dest_by_player", "hopped_mask", "captured_mask",
           "promoted_mask", "comp_labels", "phase", "turn_pos")
 
-GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath")
+GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath",
+         "english_draughts", "dai_hasami_shogi", "wolf_and_sheep", "gridworld")
 
 
 class _SoA(ctypes.Structure):
@@ -33,7 +34,7 @@ class _SoA(ctypes.Structure):
         "board_piece", "board_owner", "current_player", "move_count", "terminated",
         "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags",
         "last_mover", "last_kind", "last_source", "last_dest", "last_dest_by_player",
-        "comp_labels", "phase")]
+        "comp_labels", "phase", "must_move")]
 
 
 def build():
@@ -53,7 +54,7 @@ def lib():
         vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
         L.orc_game_new.restype = vp
         L.orc_game_new.argtypes = [ctypes.c_char_p]
-        for f in ("orc_num_cells", "orc_num_actions", "orc_layout"):
+        for f in ("orc_num_cells", "orc_num_actions", "orc_layout", "orc_mechanics"):
             getattr(L, f).restype = i32
             getattr(L, f).argtypes = [vp]
         L.orc_init.argtypes = [vp, ctypes.POINTER(_SoA), i64, vp]
@@ -87,8 +88,9 @@ class OracleGame:
         lay = lib().orc_layout(self.h)
         self.layout = {"scores": bool(lay & 1), "passing": bool(lay & 2),
                        "last_action": bool(lay & 4), "connectivity": bool(lay & 8),
-                       "phase": bool(lay & 16)}
-        self.pass_index = self.C if self.A > self.C else None
+                       "phase": bool(lay & 16), "must_move": bool(lay & 32)}
+        self.mechanics = lib().orc_mechanics(self.h)
+        self.pass_index = self.C if (self.mechanics == 0 and self.A > self.C) else None
 
     def allocate(self, B):
         C, L = self.C, self.layout
@@ -102,6 +104,8 @@ class OracleGame:
         if L["passing"]:
             s["pass_streak"] = np.zeros(B, np.int16)
             s["pass_flags"] = np.zeros((B, 2), bool)
+        if L["must_move"]:
+            s["must_move"] = np.full(B, -1, np.int16)
         if L["last_action"]:
             s["last_mover"] = np.full(B, -1, np.int8)
             s["last_kind"] = np.full(B, -1, np.int8)

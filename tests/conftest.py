@@ -10,9 +10,9 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath")
+PLACEMENT_GAMES = ("tic_tac_toe", "connect_four", "hex", "reversi", "pente", "gomoku", "yavalath")
 MOVEMENT_GAMES = ("english_draughts", "dai_hasami_shogi", "wolf_and_sheep", "gridworld")
-ALL_GAMES = GAMES + MOVEMENT_GAMES
+GAMES = PLACEMENT_GAMES + MOVEMENT_GAMES          # the reference's 11-game corpus
 
 
 def pytest_configure(config):

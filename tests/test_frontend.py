@@ -37,6 +37,8 @@ def test_layout_and_codec_match_reference(name, golden_meta):
     assert low.info["C"] == d["num_cells"]
     assert low.info["A"] == d["action_space"]["size"]
     assert (low.info["pass_index"] >= 0) == d["action_space"]["has_pass"]
+    assert low.info["codec"] == d["action_space"]["kind"]
+    assert low.info["observation_planes"] == d["observation_planes"]
     L = low.info["layout"]
     ref = d["state_layout"]
     for k_ref, k in (("scores", "scores"), ("passing", "passing"), ("must_move", "must_move"),

@@ -128,13 +128,16 @@ def test_auto_reset_matches_reference_semantics():
 def test_observe_planes(name):
     g = game(name)
     st = lx.engine.playout_random(g, seed=2, batch_size=64, max_turns=7).final
-    own = st.board_owner
+    own, pc = st.board_owner, st.board_piece
+    T = len(g.piece_names)
     for p in (0, 1):
         planes, mask = g.observe(st, p)
-        assert np.array_equal(planes[:, 0], own == p)
-        assert np.array_equal(planes[:, 1], own == 1 - p)
-        assert np.array_equal(planes[:, 2], np.repeat((st.current_player == p)[:, None],
-                                                       g.num_cells, axis=1))
+        assert planes.shape[1] == 2 * T + 1
+        for t in range(T):
+            assert np.array_equal(planes[:, 2 * t], (own == p) & (pc == t))
+            assert np.array_equal(planes[:, 2 * t + 1], (own == 1 - p) & (pc == t))
+        assert np.array_equal(planes[:, 2 * T], np.repeat((st.current_player == p)[:, None],
+                                                           g.num_cells, axis=1))
         assert np.array_equal(mask, g.legal_mask(st))
 
 

@@ -15,7 +15,7 @@ from oracle import oracle as O  # noqa: E402
 
 @pytest.mark.parametrize("name", GAMES)
 def test_env_random_episodes_match_playout(name):
-    env = lx.LudaxEnvironment(name)
+    env = lx.LudaxEnvironment(name, max_steps=200)      # engine.playout_random's cap
     B = 512
     st = env.init(seed=42, batch_size=B)
     assert np.array_equal(st.legal_action_mask.cpu().numpy(),
@@ -30,9 +30,9 @@ def test_env_random_episodes_match_playout(name):
         total += st.rewards
         m = st.legal_action_mask.cpu().numpy()
         assert np.array_equal(m, env.game.legal_mask(st.game_state))
-    want, _ = O.OracleGame(name).playout(B, seed=42, max_turns=1000)
+    want, _ = O.OracleGame(name).playout(B, seed=42, max_turns=200)
     host = st.game_state.host()
-    for f in ("board_owner", "outcome", "move_count", "terminated"):
+    for f in ("board_owner", "board_piece", "outcome", "move_count", "terminated", "truncated"):
         assert np.array_equal(host[f], want[f]), f
     out = want["outcome"]
     exp = np.stack([np.where(out == 1, 1.0, np.where(out == 2, -1.0, 0.0)),

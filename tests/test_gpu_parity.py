@@ -28,7 +28,8 @@ def game(name):
 
 
 ORACLE_B = {"tic_tac_toe": 65536, "connect_four": 16384, "hex": 2048, "reversi": 4096,
-            "pente": 512, "gomoku": 1024, "yavalath": 8192}
+            "pente": 512, "gomoku": 1024, "yavalath": 8192, "english_draughts": 4096,
+            "dai_hasami_shogi": 1024, "wolf_and_sheep": 8192, "gridworld": 65536}
 
 
 @pytest.mark.parametrize("name", GAMES)

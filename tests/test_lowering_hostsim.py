@@ -9,7 +9,8 @@ from oracle import oracle as O
 from paper_2506_22609_b200 import lowering, rng, syntax
 
 B = {"tic_tac_toe": 4096, "connect_four": 2048, "hex": 512, "reversi": 1024, "pente": 128,
-     "gomoku": 256, "yavalath": 1024}
+     "gomoku": 256, "yavalath": 1024, "english_draughts": 256, "dai_hasami_shogi": 128,
+     "wolf_and_sheep": 1024, "gridworld": 4096}
 
 
 @pytest.fixture(scope="module", params=GAMES)
