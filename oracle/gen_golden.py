@@ -181,5 +181,85 @@ def main():
     print("wrote", OUT)
 
 
+def _stats_dict(st):
+    return {"games": st.games, "wins_p1": st.wins_p1, "wins_p2": st.wins_p2, "draws": st.draws,
+            "truncations": st.truncations, "turns": st.turns.tolist(),
+            "legal_counts": st.legal_counts.tolist(),
+            "multi_choice_turns": st.multi_choice_turns, "total_turns": st.total_turns,
+            "coverage": [float.hex(float(x)) for x in st.coverage],
+            "seat_of_a": st.seat_of_a.tolist(), "winner_agent": st.winner_agent.tolist(),
+            "wins_a": st.wins_a, "wins_b": st.wins_b}
+
+
+MATCHES = [
+    # (game, policy a, policy b, games, seed, max_turns); policy = ("mcts", iters, seed) | ("random", seed)
+    ("tic_tac_toe", ("mcts", 30, 1), ("random", 2), 8, 3, 200),
+    ("connect_four", ("mcts", 40, 5), ("mcts", 15, 6), 6, 7, 200),
+    ("reversi", ("mcts", 12, 1), ("random", 3), 4, 2, 200),
+    ("hex", ("mcts", 10, 4), ("mcts", 5, 5), 2, 11, 200),
+    ("english_draughts", ("mcts", 12, 2), ("mcts", 6, 3), 4, 4, 60),
+    ("wolf_and_sheep", ("random", 7), ("mcts", 10, 8), 4, 5, 200),
+]
+
+
+def mcts_fixtures():
+    """MCTS decisions, match statistics and a GAVEL report from the
+    reference agents (agents.py, evaluation.py:85-143)."""
+    from boardlang.agents import MctsConfig, MctsPolicy, RandomPolicy, mcts_search, play_match
+    from boardlang.evaluation import EvalConfig, evaluate_game
+
+    def pol(p):
+        return MctsPolicy(MctsConfig(iterations=p[1], seed=p[2])) if p[0] == "mcts" \
+            else RandomPolicy(seed=p[1])
+    out = {"matches": [], "searches": []}
+    for name, a, b, n, seed, mt in MATCHES:
+        g = boardlang.load_game(open(os.path.join(GAMES_DIR, f"{name}.ldx")).read())
+        st = play_match(g, pol(a), pol(b), n, seed=seed, max_turns=mt)
+        out["matches"].append({"game": name, "a": list(a), "b": list(b), "games": n,
+                               "seed": seed, "max_turns": mt, "stats": _stats_dict(st)})
+        print("match", name, st.wins_a, st.wins_b)
+    for name, seq, iters, seed in (("connect_four", [38, 39, 31], 300, 9),
+                                   ("tic_tac_toe", [4], 200, 3),
+                                   ("reversi", [19], 80, 5),
+                                   ("english_draughts", [44 * 64 + 35, 21 * 64 + 30], 60, 2)):
+        g = boardlang.load_game(open(os.path.join(GAMES_DIR, f"{name}.ldx")).read())
+        s = g.init(1, seed=13)
+        for a in seq:
+            s = g.step(s, np.array([a]))
+        act = mcts_search(g, s, MctsConfig(iterations=iters, seed=seed))
+        out["searches"].append({"game": name, "actions": seq, "iterations": iters,
+                                "seed": seed, "init_seed": 13, "best": int(act)})
+        print("search", name, act)
+    rep = evaluate_game(open(os.path.join(GAMES_DIR, "tic_tac_toe.ldx")).read(),
+                        EvalConfig(matches=6, strong_iterations=20, weak_iterations=8, seed=1))
+    out["gavel_ttt"] = {"config": {"matches": 6, "strong_iterations": 20, "weak_iterations": 8,
+                                   "seed": 1}, "report": rep.as_dict()}
+    with open(os.path.join(OUT, "mcts.json"), "w") as fh:
+        json.dump(out, fh, indent=0, sort_keys=True)
+    print("wrote mcts.json")
+
+
+def jsonl_fixtures():
+    """Recorded trajectories in the reference's JSONL wire format
+    (Playouts.to_jsonl, engine.py:90-120) plus the final digests."""
+    out = {}
+    for name, seed, B in (("tic_tac_toe", 5, 3), ("reversi", 6, 2), ("english_draughts", 7, 2),
+                          ("gridworld", 8, 3), ("pente", 9, 1)):
+        g = boardlang.load_game(open(os.path.join(GAMES_DIR, f"{name}.ldx")).read())
+        po = engine.playout_random(g, seed=seed, batch_size=B, record=True)
+        out[name] = {"seed": seed, "batch": B, "jsonl": [po.to_jsonl(i) for i in range(B)],
+                     "digest": po.final.digest()}
+    with open(os.path.join(OUT, "jsonl.json"), "w") as fh:
+        json.dump(out, fh, indent=0, sort_keys=True)
+    print("wrote jsonl.json")
+
+
 if __name__ == "__main__":
-    main()
+    if "--mcts" in sys.argv:
+        mcts_fixtures()
+    elif "--jsonl" in sys.argv:
+        jsonl_fixtures()
+    else:
+        main()
+        mcts_fixtures()
+        jsonl_fixtures()

@@ -9,7 +9,7 @@ Front end (DSL reader, geometry) on the host; rules lowered to sm_100a
 kernels compiled with NVRTC behind the C-ABI in include/ludax_b200.h.
 """
 
-from . import engine, rng  # noqa: F401
+from . import agents, engine, evaluation, rng  # noqa: F401
 from .errors import (BoardLangError, CompileError, EmptyMask, IllegalAction,  # noqa: F401
                      ParseError, TerminalState)
 from .game import (B200Game, DeviceState, compile_game, load_config_game,  # noqa: F401

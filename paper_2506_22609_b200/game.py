@@ -262,6 +262,39 @@ class B200Game:
         del torch
         return st
 
+    # -- per-row scalars straight from the state words (no full export) --
+    def _meta_cols(self, state):
+        M = 2 * self.info["W"] + self.info["NX"]
+        w = state.words
+        return M, (lambda k: w[k // 4, :, k % 4])
+
+    def meta(self, state):
+        """Host numpy view of current_player, move_count, terminated,
+        truncated, outcome and seeds (one small device->host copy)."""
+        torch = _torch()
+        M, col = self._meta_cols(state)
+        flat = torch.stack([col(M), col(M + 1), col(M + 5), col(M + 6)], 1).cpu().numpy()
+        flat = flat.view(np.uint32)
+        f = flat[:, 1]
+        return {"move_count": flat[:, 0].astype(np.int32),
+                "current_player": (f & 1).astype(np.int8),
+                "terminated": ((f >> 1) & 1).astype(bool),
+                "truncated": ((f >> 2) & 1).astype(bool),
+                "outcome": (((f >> 3) & 3).astype(np.int8) - 1).astype(np.int8),
+                "seeds": flat[:, 2].astype(np.uint64) | (flat[:, 3].astype(np.uint64) << np.uint64(32))}
+
+    def truncate_rows(self, state, rows):
+        """Mark rows terminated + truncated with a draw outcome in place (the
+        reference's stuck / turn-cap handling, engine.py:156-160,
+        agents.py:430-435)."""
+        torch = _torch()
+        M, col = self._meta_cols(state)
+        r = torch.as_tensor(np.ascontiguousarray(rows, dtype=bool), device="cuda")
+        f = col(M + 1)
+        g = (f & ~0x1E) | 0x2 | 0x4 | (1 << 3)          # term, trunc, outcome 0 (stored +1)
+        state.words[(M + 1) // 4, :, (M + 1) % 4] = torch.where(r, g, f)
+        state._touch()
+
     # -- legality / sampling --
     def legal_mask_device(self, state):
         torch = _torch()

@@ -1,0 +1,99 @@
+"""MCTS / match runner / GAVEL scoring and the JSONL trajectory format on the
+device path against the reference's own outputs
+(tests/golden/mcts.json, jsonl.json made by oracle/gen_golden.py)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, game_text
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2506_22609_b200 as lx  # noqa: E402
+from paper_2506_22609_b200 import agents, evaluation  # noqa: E402
+
+with open(os.path.join(GOLDEN, "mcts.json")) as f:
+    MCTS = json.load(f)
+with open(os.path.join(GOLDEN, "jsonl.json")) as f:
+    JSONL = json.load(f)
+
+_G = {}
+
+
+def game(name):
+    if name not in _G:
+        _G[name] = lx.load_config_game(name)
+    return _G[name]
+
+
+def policy(p):
+    if p[0] == "mcts":
+        return agents.MctsPolicy(agents.MctsConfig(iterations=p[1], seed=p[2]))
+    return agents.RandomPolicy(seed=p[1])
+
+
+def stats_dict(st):
+    return {"games": st.games, "wins_p1": st.wins_p1, "wins_p2": st.wins_p2, "draws": st.draws,
+            "truncations": st.truncations, "turns": st.turns.tolist(),
+            "legal_counts": st.legal_counts.tolist(),
+            "multi_choice_turns": st.multi_choice_turns, "total_turns": st.total_turns,
+            "coverage": [float.hex(float(x)) for x in st.coverage],
+            "seat_of_a": st.seat_of_a.tolist(), "winner_agent": st.winner_agent.tolist(),
+            "wins_a": st.wins_a, "wins_b": st.wins_b}
+
+
+@pytest.mark.parametrize("m", MCTS["matches"], ids=lambda m: f"{m['game']}-{m['a'][0]}-{m['b'][0]}")
+def test_play_match_matches_reference(m):
+    st = agents.play_match(game(m["game"]), policy(m["a"]), policy(m["b"]), m["games"],
+                           seed=m["seed"], max_turns=m["max_turns"])
+    assert stats_dict(st) == m["stats"]
+
+
+@pytest.mark.parametrize("s", MCTS["searches"], ids=lambda s: s["game"])
+def test_mcts_search_matches_reference(s):
+    g = game(s["game"])
+    st = g.init(1, seed=s["init_seed"])
+    for a in s["actions"]:
+        st = g.step(st, np.array([a]))
+    best = agents.mcts_search(g, st, agents.MctsConfig(iterations=s["iterations"],
+                                                       seed=s["seed"]))
+    assert best == s["best"]
+
+
+def test_gavel_report_matches_reference():
+    c = MCTS["gavel_ttt"]["config"]
+    rep = evaluation.evaluate_game(game_text("tic_tac_toe"),
+                                   evaluation.EvalConfig(**c))
+    assert rep.as_dict() == MCTS["gavel_ttt"]["report"]
+    bad = evaluation.evaluate_game("(game \"broken\"")
+    assert not bad.playable and bad.diagnostic
+
+
+def test_terminal_search_raises():
+    g = game("tic_tac_toe")
+    s = g.init(1)
+    for a in (0, 1, 4, 2, 8):
+        s = lx.engine.step(g, s, a)
+    with pytest.raises(lx.TerminalState):
+        agents.mcts_search(g, s)
+
+
+@pytest.mark.parametrize("name", sorted(JSONL))
+def test_jsonl_trajectories_match_reference(name):
+    f = JSONL[name]
+    po = lx.engine.playout_random(game(name), seed=f["seed"], batch_size=f["batch"], record=True)
+    assert po.final.digest() == f["digest"]
+    for i in range(f["batch"]):
+        assert po.to_jsonl(i) == f["jsonl"][i]
+
+
+def test_benchmark_throughput_report():
+    g = game("connect_four")
+    rep = evaluation.benchmark_throughput(g, [1024, 4096], warmup_episodes=2, episodes=3)
+    assert rep.rate("Connect Four", 4096) > 0
+    assert rep.to_csv().startswith("game,batch_size")
