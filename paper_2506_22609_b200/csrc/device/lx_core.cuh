@@ -243,8 +243,52 @@ struct Mirror {
     }
 };
 
+// position and in-ply offset of the r-th unit of a bit-sliced multiset:
+// cell x carries c(x) = sum_j 2^j [x in d[j]] units, units are ordered by
+// cell, and r < sum_x c(x).  Returns x; rem = r - (units of cells < x), so
+// 0 <= rem < c(x).  Branch-free: word choice by prefix sums, then a 5-level
+// binary descent inside the word (a slide group's "r-th (source, distance)
+// pair", reference mechanics.py:211-227).
+template <int W, int NB>
+__device__ __forceinline__ int select_weighted(const BB<W> (&d)[NB], int r, int& rem) {
+    int cum = 0, base = 0, word = 0;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < NB; j++) c += __popc(d[j].w[i]) << j;
+        const bool here = !found && r < cum + c;
+        word = here ? i : word;
+        base = here ? cum : base;
+        found = found || here;
+        cum += c;
+    }
+    u32 v[NB];
+#pragma unroll
+    for (int j = 0; j < NB; j++) {
+        u32 t = 0u;
+#pragma unroll
+        for (int i = 0; i < W; i++) t = (word == i) ? d[j].w[i] : t;
+        v[j] = t;
+    }
+    int rr = r - base, pos = 0;
+#pragma unroll
+    for (int half = 16; half >= 1; half >>= 1) {
+        const u32 m = ((1u << half) - 1u) << pos;
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < NB; j++) c += __popc(v[j] & m) << j;
+        const bool up = rr >= c;
+        rr = up ? rr - c : rr;
+        pos = up ? pos + half : pos;
+    }
+    rem = rr;
+    return 32 * word + pos;
+}
+
 // register-resident state of one env (unpacked from the HBM state words)
-template <int W, int NX>
+template <int W, int NX, int NGC = 1>
 struct State {
     BB<W> own0, own1;
     u32 ext[NX > 0 ? NX : 1];
@@ -253,6 +297,8 @@ struct State {
     int pass_streak, pf0, pf1, ldbp0, ldbp1, sc0, sc1;
     int last_source, must_move;  // movement games (reference state.py:96-104)
     int ovr, samep;              // transient per ply: extra-turn player, same-piece flag
+    int ncached;                 // ntot holds the move-group totals of the position (not stored)
+    int ntot[NGC];
     u64 seed;
 };
 

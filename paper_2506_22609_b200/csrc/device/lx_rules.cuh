@@ -48,6 +48,7 @@ __device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<
     s.must_move = (short)(w[M + 7] >> 16);
     s.ovr = -1;
     s.samep = 0;
+    s.ncached = 0;
 }
 
 template <class G>
@@ -85,7 +86,7 @@ __device__ __forceinline__ void init_state(typename G::St& s, u64 seed) {
     s.last_mover = -1; s.last_kind = -1; s.last_dest = -1; s.last_source = -1;
     s.pass_streak = 0; s.pf0 = 0; s.pf1 = 0; s.ldbp0 = -1; s.ldbp1 = -1;
     s.sc0 = 0; s.sc1 = 0;
-    s.must_move = -1; s.ovr = -1; s.samep = 0;
+    s.must_move = -1; s.ovr = -1; s.samep = 0; s.ncached = 0;
     s.seed = seed;
     G::start(s);
 }
@@ -116,7 +117,13 @@ __device__ __forceinline__ int sample_action(const typename G::St& s, u64 smix, 
         return G::bit_cell(select_bit(legal, r));
     } else {
         int tot[G::NG];
-        const int n = G::count_moves(s, tot);
+        int n = 0;
+        if (s.ncached) {               // totals computed by the previous ply's lookahead
+#pragma unroll
+            for (int i = 0; i < G::NG; i++) { tot[i] = s.ntot[i]; n += tot[i]; }
+        } else {
+            n = G::count_moves(s, tot);
+        }
         if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
         const int r = draw_index(mix64(smix ^ (u64)s.mc), n);
         return G::select_move(s, r, tot, hint);
@@ -140,6 +147,7 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
     const bool is_pass = (G::PASS >= 0) && action == G::PASS;
     s.ovr = -1;
     s.samep = 0;
+    s.ncached = 0;
     if (is_pass) {
         s.last_kind = 4; s.last_dest = -1; s.last_source = -1; s.last_mover = mover;
     } else {
@@ -172,7 +180,14 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
         typename G::St t = s;
         t.cur = next_player;
         t.phase = next_phase;
-        next_count = legal_count<G>(t);
+        if constexpr (G::MECH == 0) {
+            next_count = legal_count<G>(t);
+        } else {
+            // the lookahead is exactly the next ply's legality: keep its group
+            // totals for sample_action (the fused rollout stays in registers)
+            next_count = G::count_moves(t, s.ntot);
+            s.ncached = 1;
+        }
         if (next_count == 0 && G::PASS >= 0 && G::force_pass(next_phase)) next_count = 1;
     }
     const int out = G::end_rules(s, mover, next_count);

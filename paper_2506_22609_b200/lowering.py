@@ -1247,6 +1247,8 @@ class GameLowering(MoveLoweringMixin):
         fp = " || ".join(f"phase == {p}" for p in fp_cases) or "false"
         conn_update = self._conn_update_code()
         conn_rebuild = self._conn_rebuild_code()
+        self.ngc = {0: 1, 1: len(getattr(self, "groups", ())) or 1,
+                    2: len(self.grid[2]) if self.grid else 1}[self.mech_kind]
         if self.mech_kind == 0:
             mech_code = f"""    static constexpr int MECH = 0;
     static __device__ __forceinline__ BBW legal(const St& s) {{
@@ -1299,7 +1301,8 @@ struct Game {{
     static constexpr bool IDENT = {str(self.ident).lower()};   // bit position == cell id
     static constexpr int NB = {self.NB};                       // bit slots (embedded grid)
     typedef lx::BB<W> BBW;
-    typedef lx::State<W, NX> St;
+    static constexpr int NGC = {self.ngc};                     // cached move-group totals
+    typedef lx::State<W, NX, NGC> St;
 {self._bitmap_code()}
 @@CONSTS@@
 @@HELPERS@@

@@ -386,6 +386,99 @@ class MoveLoweringMixin:
                              f"{body}\n    }}")
         return name
 
+    def _select_code(self, groups):
+        """select_move body: the r-th action over groups in order, then source
+        cell, then distance (reference mechanics.py:199-232), without
+        per-group branches -- lanes of a warp pick different groups, so every
+        group's candidate plane is built and the chosen one kept by select
+        (divergent per-group code was the dominant cost).  Step / hop: r-th
+        set bit of the chosen plane.  Slides: the reach planes R_1 >= .. >=
+        R_L of each slide group become bit-sliced per-source counts and
+        lx::select_weighted finds (source, distance) by prefix popcounts."""
+        C = self.C
+        NG = len(groups)
+        out = ["        int g = -1, rr = r;"]
+        for gi in range(NG):
+            out.append(f"        {{ const bool h = g < 0 && rr < tot[{gi}]; "
+                       f"rr = (g < 0 && !h) ? rr - tot[{gi}] : rr; g = h ? {gi} : g; }}")
+        out.append("        hint = g;")
+        out.append("        if (g < 0) return -1;")
+        sh = [gi for gi, g in enumerate(groups) if g.kind in (KIND_STEP, KIND_HOP)]
+        sl = [gi for gi, g in enumerate(groups) if g.kind == KIND_SLIDE]
+
+        def off_expr(g):
+            k = 1 if g.kind == KIND_STEP else 2
+            o1, o2 = k * self._shift_of(g.d1), k * self._shift_of(g.d2)
+            return str(o1) if o1 == o2 else f"(mover ? {o2} : {o1})"
+        if sh:
+            out.append("        BBW cs = lx::bb_zero<W>();")
+            out.append("        int off = 0;")
+            for gi in sh:
+                g = groups[gi]
+                S = self._src_expr(g)
+                if g.symmetric:
+                    plane = self._count_plane(g, g.d1, S)
+                else:
+                    plane = (f"lx::sel(mover != 0, {self._count_plane(g, g.d1, S)}, "
+                             f"{self._count_plane(g, g.d2, S)})")
+                out.append(f"        {{ const BBW c = {plane}; "
+                           f"cs = lx::sel(g == {gi}, cs, c); off = g == {gi} ? {off_expr(g)} : off; }}")
+        if sl:
+            NB = max(groups[gi].L for gi in sl).bit_length()
+            out.append(f"        BBW dg[{NB}];")
+            out.append(f"#pragma unroll")
+            out.append(f"        for (int j = 0; j < {NB}; j++) dg[j] = lx::bb_zero<W>();")
+            out.append("        int ss = 0;")
+
+            def digits(g, d, S, tag):
+                lines = [f"            BBW R0_{tag} = {S};"]
+                prev = f"R0_{tag}"
+                for k in range(1, g.L + 1):
+                    lines.append(f"            const BBW R{k}_{tag} = {prev} & {self.walk(d, k, 'E')};")
+                    prev = f"R{k}_{tag}"
+                segs = []
+                for m in range(1, g.L + 1):
+                    seg = f"R{m}_{tag}" if m == g.L else f"lx::andnot(R{m}_{tag}, R{m + 1}_{tag})"
+                    lines.append(f"            const BBW G{m}_{tag} = {seg};")
+                    segs.append(m)
+                dig = []
+                for j in range(NB):
+                    parts = [f"G{m}_{tag}" for m in segs if (m >> j) & 1]
+                    dig.append(" | ".join(parts) if parts else "lx::bb_zero<W>()")
+                return lines, dig
+            for gi in sl:
+                g = groups[gi]
+                S = self._src_expr(g)
+                out.append("        {")
+                if g.symmetric:
+                    lines, dig = digits(g, g.d1, S, "a")
+                    out += lines
+                    for j in range(NB):
+                        out.append(f"            dg[{j}] = lx::sel(g == {gi}, dg[{j}], BBW({dig[j]}));")
+                    out.append(f"            ss = g == {gi} ? {self._shift_of(g.d1)} : ss;")
+                else:
+                    la, da = digits(g, g.d1, S, "a")
+                    lb, db = digits(g, g.d2, S, "b")
+                    out += la + lb
+                    for j in range(NB):
+                        out.append(f"            dg[{j}] = lx::sel(g == {gi}, dg[{j}], "
+                                   f"lx::sel(mover != 0, BBW({da[j]}), BBW({db[j]})));")
+                    out.append(f"            ss = g == {gi} ? (mover ? {self._shift_of(g.d2)} : "
+                               f"{self._shift_of(g.d1)}) : ss;")
+                out.append("        }")
+            cond = " || ".join(f"g == {gi}" for gi in sl)
+            out.append(f"        if ({cond}) {{")
+            out.append("            int rem;")
+            out.append(f"            const int x = lx::select_weighted<W, {NB}>(dg, rr, rem);")
+            out.append(f"            return bit_cell(x) * {C} + bit_cell(x + (rem + 1) * ss);")
+            out.append("        }")
+        if sh:
+            out.append("        const int x = lx::select_bit(cs, rr);")
+            out.append(f"        return bit_cell(x) * {C} + bit_cell(x + off);")
+        else:
+            out.append("        return -1;")
+        return "\n".join(out)
+
     def _match_helper(self, gi, g):
         """match_g(s, bs, bd): group g moves the piece on bit bs to bit bd
         (reference mechanics.py:287-318, without the source test)."""
@@ -488,9 +581,7 @@ class MoveLoweringMixin:
         for gi in range(NG):
             filt.append(f"        n_ += tot[{gi}];")
         filt = "\n".join(filt)
-        picks = [self._pick_helper(gi, g) for gi, g in enumerate(groups)]
-        sel = "\n".join(f"        if (r < tot[{gi}]) {{ hint = {gi}; return {picks[gi]}(s, r); }}\n"
-                        f"        r -= tot[{gi}];" for gi in range(NG))
+        sel = self._select_code(groups)
         matches = [self._match_helper(gi, g) for gi, g in enumerate(groups)]
         claim = []
         for gi, g in enumerate(groups):
@@ -564,9 +655,8 @@ class MoveLoweringMixin:
     }}
     static __device__ __forceinline__ int select_move(const St& s, int r, const int (&tot)[{NG}],
                                                       int& hint) {{
+{pre}
 {sel}
-        hint = -1;
-        return -1;
     }}
     static __device__ __forceinline__ int claim(const St& s, int mover_, int bs, int bd) {{
 {pre.replace("s.cur", "mover_")}

@@ -63,8 +63,15 @@ def main():
     p.add_argument("--out", default="profiles")
     a = p.parse_args()
     os.makedirs(a.out, exist_ok=True)
-    names = {"tic_tac_toe": "Tic-Tac-Toe", "connect_four": "Connect_Four", "hex": "Hex",
-             "reversi": "Reversi", "pente": "Pente"}
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2506_22609_b200.game import GAMES_DIR
+    from paper_2506_22609_b200.syntax import parse_game
+    names = {}
+    for fn in sorted(os.listdir(GAMES_DIR)):
+        if fn.endswith(".ldx"):
+            with open(os.path.join(GAMES_DIR, fn)) as f:
+                names[fn[:-4]] = parse_game(f.read()).name.replace(" ", "_")
     for game, gname in names.items():
         rep = os.path.join(a.src, f"prof_{game}.ncu-rep")
         plain = os.path.join(a.src, f"plain_{game}.json")
