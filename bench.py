@@ -166,7 +166,53 @@ def run_reference(args):
     ref = numpy_reference_rate(args.game, seconds=3.0, max_turns=args.max_turns)
     if ref:
         line["reference_numpy"] = ref
+    mp = numpy_reference_mp(args.game, seconds=6.0, max_turns=args.max_turns)
+    if mp:
+        line["reference_numpy_all_cores"] = mp
     print(json.dumps(line), flush=True)
+
+
+def _mp_worker(args):
+    """One forked worker of numpy_reference_mp: the unmodified reference
+    _run_episode on its own episodes until `seconds` of loop time."""
+    game, wid, seconds, max_turns, batch = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    sys.path.insert(0, ref_dir)
+    import numpy as np
+    import boardlang
+    from boardlang import evaluation, rng as rrng
+    with open(os.path.join(ROOT, "paper_2506_22609_b200", "games", f"{game}.ldx")) as f:
+        g = boardlang.load_game(f.read())
+    steps, t, e = 0, 0.0, 0
+    while t < seconds:
+        seed = rrng.hash_key(np.uint64(0), np.uint64(batch), np.uint64(10_000 + 1000 * wid + e))
+        s, dt = evaluation._run_episode(g, batch, seed, max_turns)
+        steps += s
+        t += dt
+        e += 1
+    return steps, t, e
+
+
+def numpy_reference_mp(game, seconds, max_turns, batch=1024):
+    """The unmodified reference on every host core:
+    os.cpu_count() forked workers, OMP_NUM_THREADS=1, each timing its own
+    _run_episode loop (evaluation.py:197-211) on independent B=1024 episodes;
+    rate = sum of steps / max worker loop time.  Context only."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "boardlang")):
+        return None
+    try:
+        import multiprocessing as mp
+        n = os.cpu_count() or 1
+        with mp.get_context("fork").Pool(n) as pool:
+            res = pool.map(_mp_worker, [(game, w, seconds, max_turns, batch) for w in range(n)])
+        steps = sum(r[0] for r in res)
+        tmax = max(r[1] for r in res)
+        return {"value": steps / tmax, "unit": UNIT, "cores": n, "kind": "reference",
+                "sample": f"{sum(r[2] for r in res)} episodes x {batch} envs, {n} forked "
+                          f"workers of boardlang.evaluation._run_episode, ~{seconds:.0f}s each"}
+    except Exception as exc:
+        return {"error": repr(exc)[:200]}
 
 
 def numpy_reference_rate(game, seconds, max_turns, batch=1024):
