@@ -39,7 +39,7 @@ typedef struct lx_game lx_game;
    compiler.py:628-650, plus the device state layout). */
 typedef struct {
     int32_t num_cells;          /* C */
-    int32_t num_actions;        /* A = C (+1 pass), ActionCodec.size (codec.py:58-69) */
+    int32_t num_actions;        /* A: C, C*C (movement) or #directions (gridworld), +1 pass; ActionCodec.size (codec.py:58-69) */
     int32_t pass_index;         /* -1 when the game has no pass action */
     int32_t board_words;        /* W: 32-bit words per player bitboard */
     int32_t state_quads;        /* NQ: 16-byte quads per env in HBM */
