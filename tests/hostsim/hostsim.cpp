@@ -4,8 +4,7 @@
 // suite can compare the lowering against the oracle without a GPU.
 // Built per game by tests/hostsim/hostsim.py with -DGAME_SOURCE="<file>".
 #include "host_compat.h"
-#include "lx_core.cuh"
-#include GAME_SOURCE
+#include GAME_SOURCE          // its #defines (block shape, arena sizes) precede lx_core.cuh
 #include "lx_rules.cuh"
 
 #include <cstring>
