@@ -113,6 +113,19 @@ int lx_step(const lx_game *g, void *state, int64_t B, const int64_t *actions,
 int lx_random_step(const lx_game *g, void *state, int64_t B, int max_turns,
                    int64_t *actions_out, void *stream);
 
+/* MCTS expansion with rollouts (agents._Search._attach_and_rollout and
+   agents._rollout, agents.py:211-238, 313-353), one thread per child: in a
+   node pool of `cap` env rows, child row children[i] = parent row parents[i]
+   stepped with actions[i]; info[i] = current_player | terminated << 2 |
+   (outcome + 1) << 3 | legal_count << 8; masks (n, A) uint8 or NULL gets the
+   child's legal mask; rolled[i] = outcome of one uniform-random rollout from
+   a live child with legal actions, drawing with seeds[i] and capped at
+   max_turns total plies (0 draw / cap / stuck, 1 P1, 2 P2), else -1.
+   All pointers are device memory. */
+int lx_expand(const lx_game *g, void *pool, int64_t cap, const int64_t *parents,
+              const int64_t *actions, const int64_t *children, int64_t n, const uint64_t *seeds,
+              int max_turns, int32_t *info, int8_t *rolled, uint8_t *masks, void *stream);
+
 /* Fused register-resident rollout (engine.playout_random, engine.py:123-163;
    evaluation._run_episode, evaluation.py:197-211).
    mode bit 0: start envs from seeds (seeds[i] or spawn(seed, first_index+i))

@@ -438,6 +438,64 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
     }
 }
 
+// MCTS expansion + rollout, one thread per expanded child (reference
+// agents._Search._attach_and_rollout + _rollout, agents.py:211-238, 313-353).
+// States live in a node pool (quad-major, row stride `cap`): child row
+// children[i] = parent row parents[i] stepped with actions[i].  Per child:
+// info[i] = current_player | terminated << 2 | (outcome + 1) << 3 |
+// legal count << 8, its (A,) legal mask row in masks (when non-null), and
+// when it is live and has a legal action, the outcome of one uniform-random
+// rollout from it drawing with seeds[i] (0 draw / stuck / cap, 1 P1, 2 P2)
+// in rolled[i] (else -1).
+extern "C" __global__ void __launch_bounds__(128) lx_expand(u32* pool, i64 cap, const i64* parents,
+                                                            const i64* actions,
+                                                            const i64* children, i64 n,
+                                                            const u64* seeds, int max_turns,
+                                                            int* info, signed char* rolled,
+                                                            unsigned char* masks) {
+    const i64 i = lx::gtid();
+    if (i >= n) return;
+    Game::St s;
+    lx::load_state<Game>(s, pool, cap, parents[i]);
+    if (!s.term) lx::apply_step<Game>(s, (int)actions[i]);
+    lx::store_state<Game>(s, pool, cap, children[i]);
+    int cnt = 0;
+    bool pass_only = false;
+    if (!s.term) {
+        cnt = lx::legal_count<Game>(s);
+        pass_only = cnt == 0 && Game::force_pass(s.phase);
+        if (pass_only) cnt = 1;
+    }
+    info[i] = s.cur | (s.term << 2) | ((s.outcome + 1) << 3) | (cnt << 8);
+    if (masks) {
+        unsigned char* row = masks + i * (i64)Game::A;
+        for (int a = 0; a < Game::A; a++) row[a] = 0;
+        if (!s.term) {
+            if constexpr (Game::MECH == 0) {
+                const lx::BB<Game::W> legal = Game::legal(s);
+                for (int c = 0; c < Game::C; c++) row[c] = lx::test(legal, Game::cell_bit(c));
+            } else {
+                Game::enum_moves(s, [&](int a) { row[a] = 1; });
+            }
+            if (Game::PASS >= 0 && pass_only) row[Game::PASS] = 1;
+        }
+    }
+    signed char out = -1;
+    if (!s.term && cnt > 0) {
+        s.seed = seeds[i];
+        s.ncached = 0;
+        const u64 smix = lx::seed_mix(s.seed);
+        while (!s.term && (int)s.mc < max_turns) {
+            int hint;
+            const int a = lx::sample_action<Game>(s, smix, hint);
+            if (a < 0) break;                      // stuck: scored as a draw
+            lx::apply_step<Game>(s, a, hint);
+        }
+        out = (signed char)(s.term && !s.trunc ? s.outcome : 0);
+    }
+    rolled[i] = out;
+}
+
 // PGX-style environment step (env.LudaxEnvironment.step), one launch per ply:
 // apply actions[i] to live rows (actions == null: no move, just refresh the
 // outputs), reward the terminating ply from the outcome (reference

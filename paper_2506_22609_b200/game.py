@@ -283,6 +283,35 @@ class B200Game:
                 "outcome": (((f >> 3) & 3).astype(np.int8) - 1).astype(np.int8),
                 "seeds": flat[:, 2].astype(np.uint64) | (flat[:, 3].astype(np.uint64) << np.uint64(32))}
 
+    def expand(self, pool_words, cap, parents, actions, children, seeds, max_turns,
+               masks=True):
+        """MCTS expansion + rollouts in one launch (lx_expand): children rows of
+        the node pool get their parents' states stepped with `actions`; returns
+        host arrays (info int32, rolled int8, masks (n, A) bool or None) --
+        one host->device and one device->host copy."""
+        torch = _torch()
+        n = len(parents)
+        A = self.codec.size
+        host = np.empty(4 * n, dtype=np.int64)
+        host[:n] = parents
+        host[n:2 * n] = actions
+        host[2 * n:3 * n] = children
+        host[3 * n:] = np.asarray(seeds, dtype=np.uint64).view(np.int64)
+        dev_in = torch.from_numpy(host).pin_memory().to("cuda", non_blocking=True)
+        nb = 4 * n + n + (n * A if masks else 0)
+        out = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        info = out[:4 * n]
+        rolled = out[4 * n:5 * n]
+        mk = out[5 * n:] if masks else None
+        p = dev_in.data_ptr()
+        native.check(native.lib().lx_expand(
+            self.handle, pool_words.data_ptr(), int(cap), p, p + 8 * n, p + 16 * n, n, p + 24 * n,
+            int(max_turns), info.data_ptr(), rolled.data_ptr(),
+            mk.data_ptr() if mk is not None else None, self._stream()))
+        h = out.cpu().numpy()
+        return (h[:4 * n].view(np.int32), h[4 * n:5 * n].view(np.int8),
+                h[5 * n:].reshape(n, A).astype(bool) if masks else None)
+
     def truncate_rows(self, state, rows):
         """Mark rows terminated + truncated with a draw outcome in place (the
         reference's stuck / turn-cap handling, engine.py:156-160,
