@@ -215,8 +215,12 @@ def mcts_fixtures():
     for name, a, b, n, seed, mt in MATCHES:
         g = boardlang.load_game(open(os.path.join(GAMES_DIR, f"{name}.ldx")).read())
         st = play_match(g, pol(a), pol(b), n, seed=seed, max_turns=mt)
+        from boardlang.evaluation import harmonic_mean, score_match
+        sc = score_match(st)
         out["matches"].append({"game": name, "a": list(a), "b": list(b), "games": n,
-                               "seed": seed, "max_turns": mt, "stats": _stats_dict(st)})
+                               "seed": seed, "max_turns": mt, "stats": _stats_dict(st),
+                               "scores": {k: float.hex(v) for k, v in sc.as_dict().items()},
+                               "gavel": float.hex(harmonic_mean(sc.values()))})
         print("match", name, st.wins_a, st.wins_b)
     for name, seq, iters, seed in (("connect_four", [38, 39, 31], 300, 9),
                                    ("tic_tac_toe", [4], 200, 3),
