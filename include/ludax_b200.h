@@ -64,6 +64,8 @@ typedef struct {
     int16_t *last_source, *last_dest, *last_dest_by_player, *comp_labels;
     int8_t *phase;
     int16_t *must_move;         /* movement games with same-piece extra turns */
+    int8_t *turn_pos;           /* orders with a repeated player */
+    uint8_t *hopped_mask, *captured_mask, *promoted_mask;   /* (B, C) transient masks */
 } lx_ref_state;
 
 int lx_version(void);

@@ -258,7 +258,49 @@ def jsonl_fixtures():
     print("wrote jsonl.json")
 
 
+def fuzz_fixtures(limit=150, tries=6000):
+    """Programs from the reference's own random generator (generator.py,
+    sample_game with SamplerConfig(seed=7)) that the reference compiles and
+    plays (playout_random, B=16, 60-ply cap) -- a corpus for checking the
+    lowering's generality: every one must either be lowered bit-exactly or
+    rejected with CompileError."""
+    import signal
+    from boardlang.generator import SamplerConfig, sample_game
+
+    class _Timeout(Exception):
+        pass
+
+    def _alarm(*_):
+        raise _Timeout()
+    signal.signal(signal.SIGALRM, _alarm)
+    out = []
+    for i in range(tries):
+        if len(out) >= limit:
+            break
+        text = sample_game(SamplerConfig(seed=7), index=i)
+        try:
+            signal.alarm(10)
+            g = boardlang.load_game(text)
+            runs = []
+            for seed in (1, 2):
+                po = engine.playout_random(g, seed=seed, batch_size=16, max_turns=60)
+                runs.append({"seed": seed, "digest": po.final.digest(),
+                             "turns": int(po.turns_taken.sum())})
+            signal.alarm(0)
+        except Exception:
+            signal.alarm(0)
+            continue
+        out.append({"index": i, "text": text, "runs": runs})
+    with open(os.path.join(OUT, "fuzz.json"), "w") as fh:
+        json.dump({"sampler_seed": 7, "batch": 16, "max_turns": 60, "programs": out}, fh,
+                  indent=0, sort_keys=True)
+    print("wrote fuzz.json", len(out))
+
+
 if __name__ == "__main__":
+    if "--fuzz" in sys.argv:
+        fuzz_fixtures()
+        sys.exit(0)
     if "--mcts" in sys.argv:
         mcts_fixtures()
     elif "--jsonl" in sys.argv:

@@ -293,7 +293,7 @@ struct State {
     BB<W> own0, own1;
     u32 ext[NX > 0 ? NX : 1];
     u32 mc;
-    int cur, term, trunc, outcome, phase, last_mover, last_kind, last_dest;
+    int cur, term, trunc, outcome, phase, pos, last_mover, last_kind, last_dest;
     int pass_streak, pf0, pf1, ldbp0, ldbp1, sc0, sc1;
     int last_source, must_move;  // movement games (reference state.py:96-104)
     int ovr, samep;              // transient per ply: extra-turn player, same-piece flag

@@ -161,6 +161,10 @@ struct LxRefPtrs {               // reference GameState field pointers (state.py
     short* comp_labels;          // (B, 1, C) int16     or null
     signed char* phase;          // (B,) int8           or null
     short* must_move;            // (B,) int16          or null
+    signed char* turn_pos;       // (B,) int8           or null
+    unsigned char* hopped_mask;  // (B, C) bool         or null (transient masks)
+    unsigned char* captured_mask;
+    unsigned char* promoted_mask;
 };
 
 extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const u64* seeds,
@@ -588,6 +592,10 @@ extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B
     if (p.comp_labels) Game::labels(s, p.comp_labels + i * Game::C);
     if (p.phase) p.phase[i] = (signed char)s.phase;
     if (p.must_move) p.must_move[i] = (short)s.must_move;
+    if (p.turn_pos) p.turn_pos[i] = (signed char)s.pos;
+    if (p.hopped_mask) Game::export_transient(s, p.hopped_mask + i * Game::C,
+                                              p.captured_mask + i * Game::C,
+                                              p.promoted_mask + i * Game::C);
 }
 
 // reference GameState SoA -> device state (inverse of lx_export)
@@ -628,6 +636,10 @@ extern "C" __global__ void __launch_bounds__(128) lx_import(u32* st, i64 B, LxRe
     }
     s.phase = p.phase ? p.phase[i] : 0;
     s.must_move = p.must_move ? p.must_move[i] : -1;
+    s.pos = p.turn_pos ? p.turn_pos[i] : 0;
+    if (p.hopped_mask) Game::import_transient(s, p.hopped_mask + i * Game::C,
+                                              p.captured_mask + i * Game::C,
+                                              p.promoted_mask + i * Game::C);
     Game::rebuild_ext(s);
     lx::store_state<Game>(s, st, B, i);
 }

@@ -37,6 +37,7 @@ __device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<
     s.pf0 = (f >> 10) & 1u;
     s.pf1 = (f >> 11) & 1u;
     s.last_kind = (int)((f >> 12) & 7u) - 1;
+    s.pos = (f >> 15) & 31u;
     s.last_dest = (short)(w[M + 2] & 0xffffu);
     s.pass_streak = (short)(w[M + 2] >> 16);
     s.ldbp0 = (short)(w[M + 3] & 0xffffu);
@@ -62,7 +63,7 @@ __device__ __forceinline__ void pack(const typename G::St& s, u32 (&w)[Layout<G>
     w[M + 1] = (u32)s.cur | ((u32)s.term << 1) | ((u32)s.trunc << 2) |
                ((u32)(s.outcome + 1) << 3) | ((u32)s.phase << 5) |
                ((u32)(s.last_mover + 1) << 8) | ((u32)s.pf0 << 10) | ((u32)s.pf1 << 11) |
-               ((u32)(s.last_kind + 1) << 12);
+               ((u32)(s.last_kind + 1) << 12) | ((u32)s.pos << 15);
     w[M + 2] = ((u32)s.last_dest & 0xffffu) | ((u32)s.pass_streak << 16);
     w[M + 3] = ((u32)s.ldbp0 & 0xffffu) | ((u32)s.ldbp1 << 16);
     w[M + 4] = ((u32)s.sc0 & 0xffffu) | ((u32)s.sc1 << 16);
@@ -82,7 +83,7 @@ __device__ __forceinline__ void init_state(typename G::St& s, u64 seed) {
     for (int i = 0; i < (G::NX > 0 ? G::NX : 1); i++) s.ext[i] = 0u;
     s.mc = 0u;
     s.cur = G::FIRST_PLAYER;
-    s.term = 0; s.trunc = 0; s.outcome = -1; s.phase = 0;
+    s.term = 0; s.trunc = 0; s.outcome = -1; s.phase = 0; s.pos = 0;
     s.last_mover = -1; s.last_kind = -1; s.last_dest = -1; s.last_source = -1;
     s.pass_streak = 0; s.pf0 = 0; s.pf1 = 0; s.ldbp0 = -1; s.ldbp1 = -1;
     s.sc0 = 0; s.sc1 = 0;
@@ -148,6 +149,7 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
     s.ovr = -1;
     s.samep = 0;
     s.ncached = 0;
+    G::clear_transient(s);
     if (is_pass) {
         s.last_kind = 4; s.last_dest = -1; s.last_source = -1; s.last_mover = mover;
     } else {
@@ -171,9 +173,9 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
         s.sc0 = s.sc0 < 0 ? 0 : s.sc0;
         s.sc1 = s.sc1 < 0 ? 0 : s.sc1;
     }
-    int next_player, next_phase;
-    G::advance(phase, mover, next_player, next_phase);
-    if (s.ovr >= 0) { next_player = s.ovr; next_phase = phase; }      // extra turn
+    int next_player, next_phase, next_pos;
+    G::advance(phase, s.pos, mover, next_player, next_phase, next_pos);
+    if (s.ovr >= 0) { next_player = s.ovr; next_phase = phase; next_pos = s.pos; }   // extra turn
     if (G::L_MUSTMOVE) s.must_move = (s.ovr >= 0 && s.samep) ? s.last_dest : -1;
     int next_count = 0;
     if (G::NEEDS_NEXT_COUNT) {                                          // compiler.py:547-561
@@ -195,6 +197,7 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
     s.mc += 1u;
     s.cur = next_player;
     s.phase = next_phase;
+    if (G::L_TURNPOS) s.pos = next_pos;
 }
 
 // legality of one action (reference mechanics.py:281-338, 499-512,

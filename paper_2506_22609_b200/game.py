@@ -237,9 +237,10 @@ class B200Game:
                 "state_layout": {"scores": self.layout.scores, "passing": self.layout.passing,
                                  "must_move": self.layout.must_move,
                                  "last_action": self.layout.last_action,
-                                 "transient_masks": False,
+                                 "transient_masks": self.layout.transient_masks,
                                  "connectivity_plans": self.layout.connectivity,
-                                 "phase_index": self.layout.phase, "turn_position": False},
+                                 "phase_index": self.layout.phase,
+                                 "turn_position": self.layout.turn_pos},
                 "device_state_bytes": self._nq * 16}
 
     # -- allocation --
@@ -503,10 +504,15 @@ class B200Game:
             f.update({"last_mover": ((B,), torch.int8), "last_kind": ((B,), torch.int8),
                       "last_source": ((B,), torch.int16), "last_dest": ((B,), torch.int16),
                       "last_dest_by_player": ((B, 2), torch.int16)})
+        if L.transient_masks:
+            for k in ("hopped_mask", "captured_mask", "promoted_mask"):
+                f[k] = ((B, C), torch.bool)
         if L.connectivity:
             f["comp_labels"] = ((B, 1, C), torch.int16)
         if L.phase:
             f["phase"] = ((B,), torch.int8)
+        if L.turn_pos:
+            f["turn_pos"] = ((B,), torch.int8)
         return {k: torch.empty(shape, dtype=dt, device=device) for k, (shape, dt) in f.items()}
 
     def _ref_struct(self, tensors):

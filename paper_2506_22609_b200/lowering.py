@@ -169,18 +169,22 @@ class GameLowering(MoveLoweringMixin):
         spec = self.spec
         allnodes = list(n.walk(spec))
         types = {type(x) for x in allnodes}
-        for t in (n.CapturedMask, n.HoppedMask, n.PromotedMask, n.PatternFn):
-            if t in types:
-                _fail(f"{t.__name__} is not lowered yet")
+        if n.PatternFn in types:
+            _fail("PatternFn is not lowered yet")
+        # transient per-ply masks (reference compiler.py:112-113, state.py:121-123):
+        # three bitboards after the piece-type planes
+        self.transient = any(t in types for t in (n.CapturedMask, n.HoppedMask,
+                                                   n.PromotedMask))
+        self.tbase = self.xbase
+        if self.transient:
+            self.xbase += 3 * self.W
+        # codec / mechanics family (reference compiler.py:212-221): any movement
+        # phase makes the movement codec; placement phases then act on cells
         kinds = {type(p.mechanic) for p in spec.phases}
-        if len(kinds) > 1:
-            _fail("games mixing placement and movement phases are not lowered yet")
         self.grid = None
         if n.MoveMechanic in kinds:
             self.grid = self._detect_gridworld()
             self.mech_kind = 2 if self.grid is not None else 1
-            if self.mech_kind == 1 and len({p.mechanic for p in spec.phases}) > 1:
-                _fail("movement phases with different move sets are not lowered yet")
         else:
             self.mech_kind = 0
         self.has_flip = n.FlipEffect in types
@@ -211,13 +215,12 @@ class GameLowering(MoveLoweringMixin):
                             cands.append(line)
         self.phase_mult = len(spec.phases) > 1 or any(p.kind == "once_through"
                                                       for p in spec.phases)
-        if any(len(p.order) != len(set(p.order)) for p in spec.phases):
-            _fail("repeated players in a mover order (turn_pos layout) are not lowered yet")
+        self.turn_pos = any(len(p.order) != len(set(p.order)) for p in spec.phases)
         self.has_pass = passing
         self.layout = {"scores": scores, "passing": passing, "must_move": must_move,
                        "last_action": last_action or bool(cands),
-                       "transient_masks": False, "connectivity": len(self.conn_plans),
-                       "phase": self.phase_mult, "turn_pos": False}
+                       "transient_masks": self.transient, "connectivity": len(self.conn_plans),
+                       "phase": self.phase_mult, "turn_pos": self.turn_pos}
         self._anchor_candidates = cands
         self._last_action_base = last_action
         if len(self.conn_plans) > 1:
@@ -348,6 +351,9 @@ class GameLowering(MoveLoweringMixin):
             return self.custodial_anchored(node)
         if t is n.CornerCustodialMask:
             return self.corner_custodial(node)
+        if t in (n.HoppedMask, n.CapturedMask, n.PromotedMask):   # exprs.py:152-165
+            k = {n.HoppedMask: 0, n.CapturedMask: 1, n.PromotedMask: 2}[t]
+            return self._tplane(k)
         if t is n.PrevMoveMask:                 # reference exprs.py:167-176
             sd = self.side(node.who)
             return (f"([&]() {{ const int d_ = ({sd}) ? s.ldbp1 : s.ldbp0; "
@@ -1179,10 +1185,11 @@ class GameLowering(MoveLoweringMixin):
                           "by the placing side are not lowered yet")
             legal_cases.append(f"            case {pi}: return {legal};")
         if self.mech_kind == 0:
-            owner_side = {pi: self.side(ph.mechanic.owner) for pi, ph in enumerate(phases)}
-            if len(set(owner_side.values())) != 1:
-                _fail("per-phase placement owners differ")
-            owner = owner_side[0]
+            owner_side = [self.side(ph.mechanic.owner) for ph in phases]
+            owner = owner_side[-1]
+            if len(set(owner_side)) > 1:            # per-phase placement owners
+                for pi in range(len(phases) - 2, -1, -1):
+                    owner = f"(phase == {pi} ? {owner_side[pi]} : {owner})"
             place_planes = []
             for pi, ph in enumerate(phases):
                 t = self.piece_ids[ph.mechanic.piece]
@@ -1191,7 +1198,7 @@ class GameLowering(MoveLoweringMixin):
                                         f"pl = pl | oh; {self._plane_set(t, 'pl')} }}")
             place_planes = "\n".join(place_planes)
         elif self.mech_kind == 1:
-            mech_code = self.movement_code(phases[0].mechanic) + "\n" + self.movement_stubs()
+            mech_code = self.movement_code(phases) + "\n" + self.movement_stubs()
         else:
             mech_code = self.gridworld_code(self.grid) + "\n" + self.movement_stubs()
 
@@ -1206,15 +1213,19 @@ class GameLowering(MoveLoweringMixin):
         adv = []
         for pi, ph in enumerate(phases):
             order = list(ph.order)
-            for pl in (0, 1):
-                pos = order.index(pl) if pl in order else 0
+            # turn_pos layout: keyed by the stored position; else the mover's
+            # first position in the order (reference _pos_lookup)
+            keys = (range(len(order)) if self.turn_pos else (0, 1))
+            for key in keys:
+                pos = key if self.turn_pos else (order.index(key) if key in order else 0)
                 nxt = pos + 1
                 wrap = nxt >= len(order)
                 nphase = pi + 1 if (wrap and ph.kind == "once_through") else pi
                 npos = 0 if wrap else nxt
                 nplayer = phases[nphase].order[npos] if nphase < nph else 0
-                adv.append(f"        if (phase == {pi} && mover == {pl}) {{ np = {nplayer}; "
-                           f"nphase = {nphase}; return; }}")
+                cond = f"pos == {key}" if self.turn_pos else f"mover == {key}"
+                adv.append(f"        if (phase == {pi} && {cond}) {{ np = {nplayer}; "
+                           f"nphase = {nphase}; npos = {npos}; return; }}")
         conn = ""
         if self.conn_plans:
             plan = self.conn_plans[0]
@@ -1298,6 +1309,7 @@ struct Game {{
     static constexpr int FIRST_PLAYER = {phases[0].order[0]}, NPHASE = {nph};
     static constexpr bool L_SCORES = {str(L['scores']).lower()}, L_PASSING = {str(L['passing']).lower()};
     static constexpr bool L_LAST = {str(L['last_action']).lower()}, L_PHASE = {str(L['phase']).lower()};
+    static constexpr bool L_TURNPOS = {str(L['turn_pos']).lower()};
     static constexpr bool IDENT = {str(self.ident).lower()};   // bit position == cell id
     static constexpr int NB = {self.NB};                       // bit slots (embedded grid)
     typedef lx::BB<W> BBW;
@@ -1315,6 +1327,7 @@ struct Game {{
     static constexpr bool L_MUSTMOVE = {str(L['must_move']).lower()};
     static constexpr bool NEEDS_NEXT_COUNT = {str(self.needs_next_count).lower()};
 {self._types_code()}
+{self._transient_code()}
 {mech_code}
     static __device__ __forceinline__ void effects(St& s, int cell, int mover, int phase) {{
         switch (phase) {{
@@ -1322,9 +1335,11 @@ struct Game {{
             default: break;
         }}
     }}
-    static __device__ __forceinline__ void advance(int phase, int mover, int& np, int& nphase) {{
+    static __device__ __forceinline__ void advance(int phase, int pos, int mover, int& np,
+                                                   int& nphase, int& npos) {{
+        (void)pos; (void)mover;
 {chr(10).join(adv)}
-        np = 0; nphase = phase;
+        np = 0; nphase = phase; npos = 0;
     }}
     static __device__ __forceinline__ int end_rules(const St& s, int mover, int next_count) {{
         const BBW me = mover ? s.own1 : s.own0;
@@ -1383,7 +1398,10 @@ struct Game {{
             if e.increment_score:
                 inc = (f"\n{ind}  {{ const int g = lx::popc(cells); "
                        f"if (mover) s.sc1 += g; else s.sc0 += g; }}")
-            return (f"{ind}{{ const BBW cells = {m} & (s.own0 | s.own1);{inc}\n"
+            mark = ""
+            if self.transient:                  # effects.py:45-46
+                mark = f"\n{ind}  {{ const BBW cm = {self._tplane(1)} | cells; {self._tplane_set(1, 'cm')} }}"
+            return (f"{ind}{{ const BBW cells = {m} & (s.own0 | s.own1);{inc}{mark}\n"
                     + self._clear_cells_code("cells", ind + "  ") + f" }}")
         if t is n.PromoteEffect:                # reference effects.py:67-85
             m = self.mask(e.mask)
@@ -1399,6 +1417,9 @@ struct Game {{
                              f"{self._plane_set(fr, 'pl')} }}")
             if to >= 1:
                 lines.append(f"{ind}  {{ const BBW pl = {self._plane(to)} | cells; {self._plane_set(to, 'pl')} }}")
+            if self.transient:                  # effects.py:83-84
+                lines.append(f"{ind}  {{ const BBW pm = {self._tplane(2)} | cells; "
+                             f"{self._tplane_set(2, 'pm')} }}")
             lines.append(f"{ind}}}")
             return "\n".join(lines)
         if t is n.ExtraTurnEffect:              # reference effects.py:104-115

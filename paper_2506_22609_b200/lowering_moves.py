@@ -53,6 +53,9 @@ class MoveGroup:
     hop_over: str = ""
     capture: bool = False
     L: int = 1
+    phase: int = 0
+    legal: str = ""          # placement pseudo-group: legal-cell bitboard expression
+    owner: str = ""          # placement pseudo-group: owner side expression
 
     @property
     def symmetric(self):
@@ -260,6 +263,49 @@ class MoveLoweringMixin:
                 f"    static __device__ __forceinline__ void set_piece(St& s, int b, int t) {{\n{setp}\n    }}\n"
                 f"    static __device__ __forceinline__ void clear_types(St& s) {{\n{clr}\n    }}")
 
+    def _tplane(self, k):
+        """Transient mask k (0 hopped, 1 captured, 2 promoted) as a BBW."""
+        W, T = self.W, self.tbase
+        words = ", ".join(f"s.ext[{T + k * W + i}]" for i in range(W))
+        return f"BBW{{{{{words}}}}}"
+
+    def _tplane_set(self, k, var):
+        W, T = self.W, self.tbase
+        return " ".join(f"s.ext[{T + k * W + i}] = {var}.w[{i}];" for i in range(W))
+
+    def _transient_code(self):
+        """clear_transient (start of every ply, compiler.py:473-476) and the
+        (B, C) bool export / import of the three transient masks."""
+        if not self.transient:
+            return ("    static __device__ __forceinline__ void clear_transient(St&) {}\n"
+                    "    static __device__ __forceinline__ void export_transient(const St&, "
+                    "unsigned char*, unsigned char*, unsigned char*) {}\n"
+                    "    static __device__ __forceinline__ void import_transient(St&, "
+                    "const unsigned char*, const unsigned char*, const unsigned char*) {}")
+        W, T = self.W, self.tbase
+        clr = " ".join(f"s.ext[{T + i}] = 0u;" for i in range(3 * W))
+        return f"""    static __device__ __forceinline__ void clear_transient(St& s) {{ {clr} }}
+    static __device__ __forceinline__ void export_transient(const St& s, unsigned char* h,
+                                                            unsigned char* c, unsigned char* p) {{
+        const BBW hb = {self._tplane(0)}, cb = {self._tplane(1)}, pb = {self._tplane(2)};
+        for (int x = 0; x < C; x++) {{
+            const int b = cell_bit(x);
+            h[x] = lx::test(hb, b); c[x] = lx::test(cb, b); p[x] = lx::test(pb, b);
+        }}
+    }}
+    static __device__ __forceinline__ void import_transient(St& s, const unsigned char* h,
+                                                            const unsigned char* c,
+                                                            const unsigned char* p) {{
+        BBW hb = lx::bb_zero<W>(), cb = lx::bb_zero<W>(), pb = lx::bb_zero<W>();
+        for (int x = 0; x < C; x++) {{
+            const int b = cell_bit(x);
+            if (h[x]) lx::setbit(hb, b);
+            if (c[x]) lx::setbit(cb, b);
+            if (p[x]) lx::setbit(pb, b);
+        }}
+        {self._tplane_set(0, 'hb')} {self._tplane_set(1, 'cb')} {self._tplane_set(2, 'pb')}
+    }}"""
+
     def _clear_cells_code(self, cells, ind):
         """Remove whatever stands on `cells` (both owners, every type plane)."""
         out = [f"{ind}s.own0 = lx::andnot(s.own0, {cells}); s.own1 = lx::andnot(s.own1, {cells});"]
@@ -386,25 +432,24 @@ class MoveLoweringMixin:
                              f"{body}\n    }}")
         return name
 
-    def _select_code(self, groups):
-        """select_move body: the r-th action over groups in order, then source
-        cell, then distance (reference mechanics.py:199-232), without
-        per-group branches -- lanes of a warp pick different groups, so every
-        group's candidate plane is built and the chosen one kept by select
-        (divergent per-group code was the dominant cost).  Step / hop: r-th
-        set bit of the chosen plane.  Slides: the reach planes R_1 >= .. >=
-        R_L of each slide group become bit-sliced per-source counts and
-        lx::select_weighted finds (source, distance) by prefix popcounts."""
+    def _select_code(self, items):
+        """Candidate planes of one phase's groups and the chosen action, given
+        `g` (chosen group) and `rr` (index inside it) -- the r-th action over
+        groups in order, then source cell, then distance (reference
+        mechanics.py:199-232), without per-group branches: lanes of a warp pick
+        different groups, so every group's candidate plane is built and the
+        chosen one kept by select (divergent per-group code was the dominant
+        cost).  Step / hop: r-th set bit of the chosen plane.  Slides: the
+        reach planes R_1 >= .. >= R_L of each slide group become bit-sliced
+        per-source counts and lx::select_weighted finds (source, distance) by
+        prefix popcounts.  Placement: r-th legal cell."""
         C = self.C
-        NG = len(groups)
-        out = ["        int g = -1, rr = r;"]
-        for gi in range(NG):
-            out.append(f"        {{ const bool h = g < 0 && rr < tot[{gi}]; "
-                       f"rr = (g < 0 && !h) ? rr - tot[{gi}] : rr; g = h ? {gi} : g; }}")
-        out.append("        hint = g;")
-        out.append("        if (g < 0) return -1;")
-        sh = [gi for gi, g in enumerate(groups) if g.kind in (KIND_STEP, KIND_HOP)]
-        sl = [gi for gi, g in enumerate(groups) if g.kind == KIND_SLIDE]
+        out = []
+        pl = [(gi, g) for gi, g in items if g.kind == KIND_PLACE]
+        sh = [(gi, g) for gi, g in items if g.kind in (KIND_STEP, KIND_HOP)]
+        sl = [(gi, g) for gi, g in items if g.kind == KIND_SLIDE]
+        for gi, g in pl:
+            out.append(f"        if (g == {gi}) return bit_cell(lx::select_bit({g.legal}, rr));")
 
         def off_expr(g):
             k = 1 if g.kind == KIND_STEP else 2
@@ -413,8 +458,7 @@ class MoveLoweringMixin:
         if sh:
             out.append("        BBW cs = lx::bb_zero<W>();")
             out.append("        int off = 0;")
-            for gi in sh:
-                g = groups[gi]
+            for gi, g in sh:
                 S = self._src_expr(g)
                 if g.symmetric:
                     plane = self._count_plane(g, g.d1, S)
@@ -424,9 +468,9 @@ class MoveLoweringMixin:
                 out.append(f"        {{ const BBW c = {plane}; "
                            f"cs = lx::sel(g == {gi}, cs, c); off = g == {gi} ? {off_expr(g)} : off; }}")
         if sl:
-            NB = max(groups[gi].L for gi in sl).bit_length()
+            NB = max(g.L for _, g in sl).bit_length()
             out.append(f"        BBW dg[{NB}];")
-            out.append(f"#pragma unroll")
+            out.append("#pragma unroll")
             out.append(f"        for (int j = 0; j < {NB}; j++) dg[j] = lx::bb_zero<W>();")
             out.append("        int ss = 0;")
 
@@ -436,18 +480,15 @@ class MoveLoweringMixin:
                 for k in range(1, g.L + 1):
                     lines.append(f"            const BBW R{k}_{tag} = {prev} & {self.walk(d, k, 'E')};")
                     prev = f"R{k}_{tag}"
-                segs = []
                 for m in range(1, g.L + 1):
                     seg = f"R{m}_{tag}" if m == g.L else f"lx::andnot(R{m}_{tag}, R{m + 1}_{tag})"
                     lines.append(f"            const BBW G{m}_{tag} = {seg};")
-                    segs.append(m)
                 dig = []
                 for j in range(NB):
-                    parts = [f"G{m}_{tag}" for m in segs if (m >> j) & 1]
+                    parts = [f"G{m}_{tag}" for m in range(1, g.L + 1) if (m >> j) & 1]
                     dig.append(" | ".join(parts) if parts else "lx::bb_zero<W>()")
                 return lines, dig
-            for gi in sl:
-                g = groups[gi]
+            for gi, g in sl:
                 S = self._src_expr(g)
                 out.append("        {")
                 if g.symmetric:
@@ -466,7 +507,7 @@ class MoveLoweringMixin:
                     out.append(f"            ss = g == {gi} ? (mover ? {self._shift_of(g.d2)} : "
                                f"{self._shift_of(g.d1)}) : ss;")
                 out.append("        }")
-            cond = " || ".join(f"g == {gi}" for gi in sl)
+            cond = " || ".join(f"g == {gi}" for gi, _ in sl)
             out.append(f"        if ({cond}) {{")
             out.append("            int rem;")
             out.append(f"            const int x = lx::select_weighted<W, {NB}>(dg, rr, rem);")
@@ -552,24 +593,95 @@ class MoveLoweringMixin:
         out.append("        }")
         return out
 
-    def movement_code(self, mech):
-        """struct Game members of a movement game (MECH 1)."""
+    def _place_group(self, pi, mech):
+        """A placement phase inside a movement-codec game: one pseudo-group
+        whose actions are the legal cells (reference PlacementMechanics,
+        mechanics.py:415-515)."""
         from .lowering import _fail
-        groups = self._movement_groups(mech)
-        if not groups:
-            _fail("movement phase without moves")
+        legal = f"(lx::andnot({self.em.const(self.valid)}, s.own0 | s.own1) & {self.mask(mech.destination)})"
+        if mech.result is not None:
+            r = mech.result
+            if (isinstance(r, n.ExistsPred) and isinstance(r.mask, n.CustodialMask)
+                    and r.mask.mover == mech.owner):
+                legal = f"({legal} & {self.would_custodial(r.mask)})"
+            else:
+                _fail("placement result predicates other than (exists (custodial ...)) "
+                      "by the placing side are not lowered yet")
+        return MoveGroup(KIND_PLACE, mech.piece, 0, "", "", phase=pi, legal=legal,
+                         owner=self.side(mech.owner))
+
+    def _place_write(self, g, ind):
+        """_write_placement (mechanics.py:463-479) of a placement phase."""
+        t = self.piece_ids[g.piece]
+        plane = ""
+        if self.piece_mode == "planes" and t >= 1:
+            plane = f"\n{ind}{{ BBW pl = {self._plane(t)} | oh; {self._plane_set(t, 'pl')} }}"
+        return (f"{ind}const int side = {g.owner};\n"
+                f"{ind}const BBW oh = lx::onehot<W>(cell_bit(a));\n"
+                f"{ind}s.own0 = lx::sel(side != 0, s.own0 | oh, s.own0);\n"
+                f"{ind}s.own1 = lx::sel(side != 0, s.own1, s.own1 | oh);{plane}\n"
+                f"{ind}s.last_kind = {KIND_PLACE}; s.last_source = -1; s.last_dest = a; "
+                f"s.last_mover = side;\n"
+                f"{ind}s.ldbp0 = side ? s.ldbp0 : a;\n"
+                f"{ind}s.ldbp1 = side ? a : s.ldbp1;")
+
+    def movement_code(self, phases):
+        """struct Game members of a movement-codec game (MECH 1): every phase
+        is a set of move groups (or one placement pseudo-group), dispatched on
+        the state's phase; the dead phase after a finished once_through
+        sequence has no legal action (compiler.py:251-267, 379-392)."""
+        from .lowering import _fail
+        groups, by_phase = [], []
+        for pi, ph in enumerate(phases):
+            mech = ph.mechanic
+            if isinstance(mech, n.MoveMechanic):
+                gs = self._movement_groups(mech)
+                if not gs:
+                    _fail("movement phase without moves")
+                for g in gs:
+                    g.phase = pi
+            else:
+                gs = [self._place_group(pi, mech)]
+            by_phase.append(list(range(len(groups), len(groups) + len(gs))))
+            groups += gs
         self.groups = groups
         NG = len(groups)
         C = self.C
         prios = [g.prio for g in groups]
-        multi = len(set(prios)) > 1
-        safe = self._group_claim_safe(groups)
+        multi = len({g.prio for g in groups if g.kind != KIND_PLACE}) > 1
+        safe = [True] * NG
+        for idx in by_phase:
+            mv = [i for i in idx if groups[i].kind != KIND_PLACE]
+            for i, ok in zip(mv, self._group_claim_safe([groups[i] for i in mv])):
+                safe[i] = ok
         pre = "\n".join(self._mv_prelude())
+        is_place = {pi: groups[idx[0]].kind == KIND_PLACE for pi, idx in enumerate(by_phase)}
+
+        def phase_switch(body_of, default="break;"):
+            out = ["        switch (s.phase) {"]
+            for pi, idx in enumerate(by_phase):
+                body = body_of(pi, idx)
+                if body is None:
+                    continue
+                out.append(f"            case {pi}: {{")
+                out.append(body)
+                out.append("            } break;")
+            out.append(f"            default: {default}")
+            out.append("        }")
+            return "\n".join(out)
+
         # counts (+ priority activity, reference mechanics.py:188-197)
-        cnt = []
-        for gi, g in enumerate(groups):
-            cnt += self._group_count_code(gi, g, "        ")
-        raw = "\n".join(cnt)
+        def count_body(pi, idx):
+            lines = []
+            for gi in idx:
+                g = groups[gi]
+                if g.kind == KIND_PLACE:
+                    lines.append(f"        tot[{gi}] = lx::popc({g.legal});")
+                else:
+                    lines += self._group_count_code(gi, g, "        ")
+            return "\n".join(lines)
+        zero = " ".join(f"tot[{gi}] = 0;" for gi in range(NG))
+        raw = f"        {zero}\n" + phase_switch(count_body)
         filt = []
         if multi:
             filt.append(f"        int minp = {BIG_PRIO};")
@@ -581,12 +693,25 @@ class MoveLoweringMixin:
         for gi in range(NG):
             filt.append(f"        n_ += tot[{gi}];")
         filt = "\n".join(filt)
-        sel = self._select_code(groups)
-        matches = [self._match_helper(gi, g) for gi, g in enumerate(groups)]
-        claim = []
-        for gi, g in enumerate(groups):
-            claim.append(f"        if (lx::test({self._src_expr(g)}, bs) && {matches[gi]}(s, bs, bd)) return {gi};")
-        claim = "\n".join(claim)
+        scan = ["        int g = -1, rr = r;"]
+        for gi in range(NG):
+            scan.append(f"        {{ const bool h = g < 0 && rr < tot[{gi}]; "
+                        f"rr = (g < 0 && !h) ? rr - tot[{gi}] : rr; g = h ? {gi} : g; }}")
+        scan.append("        hint = g;")
+        scan.append("        if (g < 0) return -1;")
+        sel = "\n".join(scan) + "\n" + phase_switch(
+            lambda pi, idx: self._select_code([(gi, groups[gi]) for gi in idx]))
+        matches = {gi: self._match_helper(gi, g) for gi, g in enumerate(groups)
+                   if g.kind != KIND_PLACE}
+
+        def claim_body(pi, idx):
+            if is_place[pi]:
+                return None
+            return "\n".join(
+                f"        if (lx::test({self._src_expr(groups[gi])}, bs) && {matches[gi]}(s, bs, bd)) "
+                f"return {gi};" for gi in idx)
+        claim = phase_switch(claim_body)
+
         def chain(vals):
             out = str(vals[-1])
             for i in range(len(vals) - 2, -1, -1):
@@ -598,48 +723,78 @@ class MoveLoweringMixin:
         # apply: piece move, hop capture, last-action bookkeeping
         hop_cases = []
         for gi, g in enumerate(groups):
-            if g.kind == KIND_HOP and g.capture:
+            if g.kind == KIND_HOP and (g.capture or self.transient):
                 S1, S2 = self._shift_of(g.d1), self._shift_of(g.d2)
                 off = str(S1) if S1 == S2 else f"(mover ? {S2} : {S1})"
-                hop_cases.append(f"            case {gi}: mid = bs + {off}; break;")
+                hop_cases.append(f"            case {gi}: mid = bs + {off}; cap = {int(g.capture)}; break;")
         hop_sw = ""
         if hop_cases:
-            hop_sw = ("        int mid = -1;\n        switch (g) {\n" + "\n".join(hop_cases)
+            marks = ""
+            if self.transient:                 # mechanics.py:347-358
+                marks = (f"            {{ const BBW hm = {self._tplane(0)} | om; {self._tplane_set(0, 'hm')} }}\n"
+                         f"            if (cap) {{ const BBW cm = {self._tplane(1)} | om; "
+                         f"{self._tplane_set(1, 'cm')} }}\n")
+            hop_sw = ("        int mid = -1, cap = 0;\n        switch (g) {\n" + "\n".join(hop_cases)
                       + "\n            default: break;\n        }\n"
                       "        if (mid >= 0) {\n            const BBW om = lx::onehot<W>(mid);\n"
-                      + self._clear_cells_code("om", "            ") + "\n        }")
+                      + marks
+                      + "            if (cap) {\n"
+                      + self._clear_cells_code("om", "                ") + "\n            }\n        }")
         planes_mv = []
         for t in range(1, self.NPL + 1):
             planes_mv.append(f"        {{ const BBW pl = {self._plane(t)}; const bool bt = lx::test(pl, bs);\n"
                              f"          const BBW q = lx::andnot(pl, os) | lx::sel(bt, lx::bb_zero<W>(), od); "
                              f"{self._plane_set(t, 'q')} }}")
         planes_mv = "\n".join(planes_mv)
-        all_safe = all(safe)
-        pick_g = ("hint >= 0 ? hint : claim(s, mover, bs, bd)" if all_safe else
+        pick_g = ("hint >= 0 ? hint : claim(s, mover, bs, bd)" if all(safe) else
                   "(hint >= 0 && group_safe(hint)) ? hint : claim(s, mover, bs, bd)")
-        enum = []
-        for gi, g in enumerate(groups):
-            enum += self._enum_code(gi, g)
-        enum = "\n".join(enum)
+        place_apply = phase_switch(
+            lambda pi, idx: (self._place_write(groups[idx[0]], "                ")
+                             + "\n                return;") if is_place[pi] else None)
+        place_legal = phase_switch(
+            lambda pi, idx: (f"                return a < {C} && "
+                             f"lx::test({groups[idx[0]].legal}, cell_bit(a));") if is_place[pi] else None)
+
+        def enum_body(pi, idx):
+            g = groups[idx[0]]
+            if is_place[pi]:
+                return (f"        {{ const BBW c = {g.legal};\n"
+                        f"#pragma unroll\n"
+                        f"        for (int w_ = 0; w_ < W; w_++) {{\n"
+                        f"            u32 b_ = c.w[w_];\n"
+                        f"            while (b_) {{ const int x = 32 * w_ + __ffs(b_) - 1; b_ &= b_ - 1u; "
+                        f"f(bit_cell(x)); }}\n"
+                        f"        }} }}")
+            lines = []
+            for gi in idx:
+                lines += self._enum_code(gi, groups[gi])
+            return "\n".join(lines)
+        enum = phase_switch(enum_body)
+
         # can_move_again: the piece on last_dest, raw group geometry, no
-        # priority / must_move (reference mechanics.py:368-403)
-        cma = []
-        for kind in (KIND_STEP, KIND_HOP, KIND_SLIDE):
-            parts = []
-            for g in groups:
-                if g.kind != kind:
-                    continue
-                S = f"({self._src_expr(g, must=False)} & A_)"
-                if kind == KIND_HOP:
-                    f1 = self._count_plane(g, g.d1, S)
-                    f2 = self._count_plane(g, g.d2, S)
-                else:   # step and slide: first step along the direction
-                    f1 = f"({S} & {self.nb(g.d1, 'E')})"
-                    f2 = f"({S} & {self.nb(g.d2, 'E')})"
-                parts.append(f1 if g.symmetric else f"lx::sel(mover != 0, {f1}, {f2})")
-            expr = " | ".join(parts) if parts else "lx::bb_zero<W>()"
-            cma.append(f"        if (kind == {kind}) return lx::any({expr});")
-        cma = "\n".join(cma)
+        # priority / must_move (reference mechanics.py:368-403, compiler.py:599-607)
+        def cma_body(pi, idx):
+            if is_place[pi]:
+                return None
+            lines = []
+            for kind in (KIND_STEP, KIND_HOP, KIND_SLIDE):
+                parts = []
+                for gi in idx:
+                    g = groups[gi]
+                    if g.kind != kind:
+                        continue
+                    S = f"({self._src_expr(g, must=False)} & A_)"
+                    if kind == KIND_HOP:
+                        f1 = self._count_plane(g, g.d1, S)
+                        f2 = self._count_plane(g, g.d2, S)
+                    else:   # step and slide: first step along the direction
+                        f1 = f"({S} & {self.nb(g.d1, 'E')})"
+                        f2 = f"({S} & {self.nb(g.d2, 'E')})"
+                    parts.append(f1 if g.symmetric else f"lx::sel(mover != 0, {f1}, {f2})")
+                if parts:
+                    lines.append(f"        if (kind == {kind}) return lx::any({' | '.join(parts)});")
+            return "\n".join(lines) if lines else None
+        cma = phase_switch(cma_body)
         code = f"""    static constexpr int MECH = 1, NG = {NG};
     static __device__ __forceinline__ int group_prio(int g) {{ return {prio_fn}; }}
     static __device__ __forceinline__ int group_kind(int g) {{ return {kind_fn}; }}
@@ -657,6 +812,7 @@ class MoveLoweringMixin:
                                                       int& hint) {{
 {pre}
 {sel}
+        return -1;
     }}
     static __device__ __forceinline__ int claim(const St& s, int mover_, int bs, int bd) {{
 {pre.replace("s.cur", "mover_")}
@@ -664,12 +820,16 @@ class MoveLoweringMixin:
         return -1;
     }}
     static __device__ __forceinline__ bool move_legal(const St& s, int a) {{
+{pre}
+{place_legal}
+        if (a >= {C * C}) return false;
         const int bs = cell_bit(a / {C}), bd = cell_bit(a % {C});
         const int g = claim(s, s.cur, bs, bd);
         if (g < 0) return false;
         {"int tot[NG]; count_raw(s, tot); int minp = " + str(BIG_PRIO) + "; for (int i = 0; i < NG; i++) if (tot[i] > 0 && group_prio(i) < minp) minp = group_prio(i); return group_prio(g) <= minp;" if multi else "return true;"}
     }}
     static __device__ __forceinline__ void apply_move(St& s, int a, int mover, int hint) {{
+{place_apply}
         const int src = a / {C}, dst = a % {C};
         const int bs = cell_bit(src), bd = cell_bit(dst);
         const int g = {pick_g};
@@ -698,7 +858,7 @@ class MoveLoweringMixin:
         const BBW op = mover ? s.own0 : s.own1;
         const BBW E = lx::andnot({self.em.const(self.valid)}, s.own0 | s.own1);
         const BBW A_ = lx::onehot<W>(cell_bit(s.last_dest));
-        (void)me; (void)op; (void)E;
+        (void)me; (void)op; (void)E; (void)A_;
 {cma}
         return false;
     }}"""
@@ -740,6 +900,10 @@ class MoveLoweringMixin:
 {pre}
         const int x = walker(s, mover);
 {oks}
+        if (s.phase >= NPHASE) {{                 // dead phase after once_through: no moves
+#pragma unroll
+            for (int i = 0; i < {NG}; i++) tot[i] = 0;
+        }}
     }}
     static __device__ __forceinline__ int count_moves(const St& s, int (&tot)[{NG}]) {{
         count_raw(s, tot);

@@ -30,7 +30,8 @@ class GameInfo(ctypes.Structure):
 REF_FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
               "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags",
               "last_mover", "last_kind", "last_source", "last_dest", "last_dest_by_player",
-              "comp_labels", "phase", "must_move")
+              "comp_labels", "phase", "must_move", "turn_pos", "hopped_mask", "captured_mask",
+              "promoted_mask")
 
 
 class RefState(ctypes.Structure):

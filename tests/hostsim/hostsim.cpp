@@ -25,6 +25,8 @@ struct RefOut {
     int16_t *last_source, *last_dest, *last_dest_by_player, *comp_labels;
     int8_t *phase;
     int16_t *must_move;
+    int8_t *turn_pos;
+    uint8_t *hopped_mask, *captured_mask, *promoted_mask;
 };
 
 static void export_one(const St& s, int64_t i, const RefOut* p) {
@@ -57,6 +59,10 @@ static void export_one(const St& s, int64_t i, const RefOut* p) {
     if (p->comp_labels) Game::labels(s, (short*)(p->comp_labels + i * Game::C));
     if (p->phase) p->phase[i] = (int8_t)s.phase;
     if (p->must_move) p->must_move[i] = (int16_t)s.must_move;
+    if (p->turn_pos) p->turn_pos[i] = (int8_t)s.pos;
+    if (p->hopped_mask) Game::export_transient(s, p->hopped_mask + i * Game::C,
+                                               p->captured_mask + i * Game::C,
+                                               p->promoted_mask + i * Game::C);
 }
 
 // legal mask of the current mover (reference CompiledGame.legal_mask row)
@@ -73,11 +79,16 @@ static void mask_row(const St& s, uint8_t* row) {
     if (Game::PASS >= 0) row[Game::PASS] = n == 0 && Game::force_pass(s.phase);
 }
 
+// each game's .so keeps its own copies of the (identically named) inline
+// rule functions and their static tables: built with -fvisibility=hidden
+// -fno-gnu-unique, only these entry points are exported
+#define SIM_API __attribute__((visibility("default")))
+
 extern "C" {
 
 // engine.playout_random from given seeds; also round-trips every state
 // through pack/unpack each ply (checks the HBM word layout).
-int64_t sim_playout(int64_t B, const uint64_t* seeds, int max_turns, const RefOut* out) {
+SIM_API int64_t sim_playout(int64_t B, const uint64_t* seeds, int max_turns, const RefOut* out) {
     int64_t steps = 0;
     for (int64_t i = 0; i < B; i++) {
         St s;
@@ -100,7 +111,7 @@ int64_t sim_playout(int64_t B, const uint64_t* seeds, int max_turns, const RefOu
 }
 
 // per-ply legal masks of env `seed` (A bytes per ply, up to max_plies)
-int sim_masks(uint64_t seed, int max_plies, uint8_t* masks, int64_t* actions) {
+SIM_API int sim_masks(uint64_t seed, int max_plies, uint8_t* masks, int64_t* actions) {
     St s;
     lx::init_state<Game>(s, seed);
     const uint64_t smix = lx::seed_mix(s.seed);
@@ -119,7 +130,7 @@ int sim_masks(uint64_t seed, int max_plies, uint8_t* masks, int64_t* actions) {
 // scripted transcript from init(seed): per ply the mask before the move and
 // whether the action was legal (verify path, no hint); stops at the first
 // illegal action.  Exports the final state.  Returns plies applied.
-int sim_transcript(uint64_t seed, int n, const int64_t* actions, uint8_t* masks, uint8_t* legal,
+SIM_API int sim_transcript(uint64_t seed, int n, const int64_t* actions, uint8_t* masks, uint8_t* legal,
                    const RefOut* out) {
     St s;
     lx::init_state<Game>(s, seed);

@@ -15,7 +15,8 @@ BUILD = os.path.join(HERE, "build")
 FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
           "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags",
           "last_mover", "last_kind", "last_source", "last_dest", "last_dest_by_player",
-          "comp_labels", "phase", "must_move")
+          "comp_labels", "phase", "must_move", "turn_pos", "hopped_mask", "captured_mask",
+          "promoted_mask")
 
 
 class _Ref(ctypes.Structure):
@@ -36,6 +37,7 @@ class HostGame:
             with open(gsrc, "w") as f:
                 f.write(src)
             subprocess.run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-ffp-contract=off",
+                            "-fno-gnu-unique", "-fvisibility=hidden", "-fvisibility-inlines-hidden",
                             "-w", f"-I{HERE}", f"-I{DEVICE}", f'-DGAME_SOURCE="{gsrc}"',
                             os.path.join(HERE, "hostsim.cpp"), "-o", so + ".tmp"], check=True)
             os.replace(so + ".tmp", so)

@@ -113,14 +113,13 @@ def test_lowering_words_bit_order():
 
 
 @pytest.mark.parametrize("text,what", [
-    ("""(game "Mix" (players 2) (equipment (board (square 4)) (pieces ("p" both)))
-        (rules (start (place "p" P1 (0)))
-          (play (once_through (P1 P2) (place "p" (destination (empty))))
-                (repeat (P1 P2) (move (step "p"))))
-        (end (if (full_board) (draw)))))""", "placement + movement phases"),
-    ("""(game "Cap" (players 2) (equipment (board (square 5)) (pieces ("a" both)))
-        (rules (play (repeat (P1 P2) (place "a" (destination (empty)))))
-        (end (if (exists (captured)) (mover win)))))""", "transient masks"),
+    ("""(game "Cust" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
+        (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
+        (end (if (exists (custodial "s" any)) (mover win)))))""", "custodial end rule"),
+    ("""(game "Tri" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
+        (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
+        (end (if (connected "s" ((edge top) (edge bottom) (edge left))) (mover win)))))""",
+     "three-target connected"),
     ("""(game "Pat" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
         (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
         (end (if (pattern "s" (2 (0 1 2 3))) (mover win)))))""", "pattern"),
