@@ -347,7 +347,7 @@ class GameLowering(MoveLoweringMixin):
             return f"lx::andnot({self.em.const(self.valid)}, {self.mask(node.item)})"
         if t is n.CustodialMask:
             if not self.anchored_ctx:
-                _fail("custodial masks outside effects / placement results are not lowered yet")
+                return self.custodial_global(node)
             return self.custodial_anchored(node)
         if t is n.CornerCustodialMask:
             return self.corner_custodial(node)
@@ -644,6 +644,51 @@ class GameLowering(MoveLoweringMixin):
         self.em.helper(name, code)
         return f"{name}(s, mover)"
 
+    def custodial_global(self, node):
+        """Every flanked target run on the board (reference
+        mask_custodial_global, exprs.py:294-319): a target cell is marked when
+        its maximal target run along an axis is bounded by the side's pieces
+        at both ends (any length), or for a fixed length n when that run has
+        exactly n cells.  Runs reaching the board edge are never flanked."""
+        side = self.side(node.mover)
+        name = f"custodial_global_{self.em.fresh('g')}"
+        lines = []
+        for d in self.board.orientation_dirs(node.orientation):
+            e = OPPOSITE[d]
+            lines.append("        {")
+            if node.length == "any":
+                ray = max(self.board.ray_length(d), 1)
+                lines += self._ks_fill(d, "flank", "tgt", ray, ind="            ")
+                lines.append("            const BBW fwd = g & tgt;")
+                lines.append("        {")
+                lines += self._ks_fill(e, "flank", "tgt", ray, ind="            ")
+                lines.append("            out = out | (fwd & g & tgt);")
+                lines.append("        }")
+            else:
+                n_len = int(node.length)
+                for dd in (d,):                  # the inverse walk marks the same runs
+                    od = OPPOSITE[dd]
+                    conds = [f"{self.nb(od, 'flank')}", "tgt"]
+                    for k in range(1, n_len):
+                        conds.append(self.walk(dd, k, "tgt"))
+                    conds.append(self.walk(dd, n_len, "flank"))
+                    lines.append("            {")
+                    lines.append(f"                const BBW st = {' & '.join(conds)};")
+                    marks = ["st"] + [self.walk(od, k, "st") for k in range(1, n_len)]
+                    lines.append(f"                out = out | {' | '.join(marks)};")
+                    lines.append("            }")
+            lines.append("        }")
+        body = "\n".join(lines)
+        self.em.helper(name, f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
+        const int side = {side};
+        const BBW flank = side ? s.own1 : s.own0;
+        const BBW tgt = {self.piece_filter(node.piece, "(side ? s.own0 : s.own1)")};
+        BBW out = lx::bb_zero<W>();
+{body}
+        return out;
+    }}""")
+        return f"{name}(s, mover)"
+
     def would_custodial(self, node):
         """Placement-result fast path (reference exprs.py:334-378): cells whose
         placement would flank a run, computed on the pre-placement board by
@@ -760,7 +805,11 @@ class GameLowering(MoveLoweringMixin):
         L = node.length
         name = f"line_anchor_{self.em.fresh('a')}"
         if node.exclude is not None:
-            _fail("anchored line with exclude: is not lowered yet")
+            # a window through the anchor avoiding excluded cells <=> a run of
+            # >= L owned non-excluded cells through the anchor
+            if node.exact:
+                _fail("exact anchored line with exclude: is not lowered yet")
+            stones = f"lx::andnot({stones}, {self.em.const(self._line_excluded(node))})"
         lines = []
         # exact lines need the maximal run through the anchor to be exactly L:
         # grow L steps each way and compare (reference exprs.py:525-533)
@@ -1078,8 +1127,8 @@ class GameLowering(MoveLoweringMixin):
         passes through the placed stone.  Otherwise the exact anchored form
         is emitted."""
         if end_rule and id(line) in self._anchored_lines:
-            if self.use_probe:                 # exact anchored semantics, cheap on big boards
-                return self.line_anchored_probe(line)
+            if self.use_probe and line.exclude is None and self.piece_mode == "single":
+                return self.line_anchored_probe(line)   # exact anchored semantics, big boards
             if id(line) in self._global_ok:
                 return self.line_exists(line)
             return self.line_anchored_exists(line)
@@ -1097,8 +1146,6 @@ class GameLowering(MoveLoweringMixin):
             own0, own1 = start_has_line
             if self._np_line(own0, line) or self._np_line(own1, line):
                 continue      # reference keeps the global form (compiler.py:272-277)
-            if line.exclude is not None:
-                _fail("anchored line with exclude: is not lowered yet")
             self.anchor_lines.add(line)
         if self._anchor_candidates and not self.anchor_lines and not self._last_action_base:
             self.layout["last_action"] = False

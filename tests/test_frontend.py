@@ -113,9 +113,9 @@ def test_lowering_words_bit_order():
 
 
 @pytest.mark.parametrize("text,what", [
-    ("""(game "Cust" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
-        (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
-        (end (if (exists (custodial "s" any)) (mover win)))))""", "custodial end rule"),
+    ("""(game "Res" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
+        (rules (play (repeat (P1 P2) (place "s" (destination (empty)) (result (full_board)))))
+        (end (if (full_board) (draw)))))""", "simulated placement result"),
     ("""(game "Tri" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
         (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
         (end (if (connected "s" ((edge top) (edge bottom) (edge left))) (mover win)))))""",

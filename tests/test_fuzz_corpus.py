@@ -16,7 +16,7 @@ from paper_2506_22609_b200.errors import CompileError
 with open(os.path.join(GOLDEN, "fuzz.json")) as f:
     FUZZ = json.load(f)
 PROGRAMS = FUZZ["programs"]
-MAX_UNSUPPORTED = 11        # custodial masks outside effects / placement results, probed exclude
+MAX_UNSUPPORTED = 0
 
 
 def lowered(prog):
@@ -29,7 +29,7 @@ def lowered(prog):
 def test_fuzz_corpus_coverage():
     unsupported = [p["index"] for p in PROGRAMS if lowered(p) is None]
     assert len(unsupported) <= MAX_UNSUPPORTED, unsupported
-    assert len(PROGRAMS) - len(unsupported) >= 139
+    assert len(PROGRAMS) - len(unsupported) >= 150
 
 
 @pytest.mark.parametrize("prog", PROGRAMS[::4], ids=lambda p: f"sample-{p['index']}")
@@ -66,4 +66,4 @@ def test_fuzz_device_matches_reference():
             assert po.final.digest() == run["digest"], prog["index"]
             assert int(np.asarray(po.turns_taken).sum()) == run["turns"], prog["index"]
         checked += 1
-    assert checked >= (139 if every == 1 else 19)
+    assert checked >= (150 if every == 1 else 21)
