@@ -258,9 +258,9 @@ def jsonl_fixtures():
     print("wrote jsonl.json")
 
 
-def fuzz_fixtures(limit=150, tries=6000):
+def fuzz_fixtures(corpora=((7, 5, 150), (11, 6, 120)), tries=20000):
     """Programs from the reference's own random generator (generator.py,
-    sample_game with SamplerConfig(seed=7)) that the reference compiles and
+    sample_game with SamplerConfig(seed=7) and (seed=11, max_depth=6)) that the reference compiles and
     plays (playout_random, B=16, 60-ply cap) -- a corpus for checking the
     lowering's generality: every one must either be lowered bit-exactly or
     rejected with CompileError."""
@@ -274,10 +274,21 @@ def fuzz_fixtures(limit=150, tries=6000):
         raise _Timeout()
     signal.signal(signal.SIGALRM, _alarm)
     out = []
+    for sampler_seed, depth, limit in corpora:
+        out += _fuzz_corpus(sampler_seed, depth, limit, tries, _Timeout)
+    with open(os.path.join(OUT, "fuzz.json"), "w") as fh:
+        json.dump({"batch": 16, "max_turns": 60, "programs": out}, fh, indent=0, sort_keys=True)
+    print("wrote fuzz.json", len(out))
+
+
+def _fuzz_corpus(sampler_seed, depth, limit, tries, timeout_exc):
+    from boardlang.generator import SamplerConfig, sample_game
+    import signal
+    out = []
     for i in range(tries):
         if len(out) >= limit:
             break
-        text = sample_game(SamplerConfig(seed=7), index=i)
+        text = sample_game(SamplerConfig(seed=sampler_seed, max_depth=depth), index=i)
         try:
             signal.alarm(10)
             g = boardlang.load_game(text)
@@ -290,11 +301,8 @@ def fuzz_fixtures(limit=150, tries=6000):
         except Exception:
             signal.alarm(0)
             continue
-        out.append({"index": i, "text": text, "runs": runs})
-    with open(os.path.join(OUT, "fuzz.json"), "w") as fh:
-        json.dump({"sampler_seed": 7, "batch": 16, "max_turns": 60, "programs": out}, fh,
-                  indent=0, sort_keys=True)
-    print("wrote fuzz.json", len(out))
+        out.append({"sampler": [sampler_seed, depth], "index": i, "text": text, "runs": runs})
+    return out
 
 
 if __name__ == "__main__":

@@ -169,8 +169,6 @@ class GameLowering(MoveLoweringMixin):
         spec = self.spec
         allnodes = list(n.walk(spec))
         types = {type(x) for x in allnodes}
-        if n.PatternFn in types:
-            _fail("PatternFn is not lowered yet")
         # transient per-ply masks (reference compiler.py:112-113, state.py:121-123):
         # three bitboards after the piece-type planes
         self.transient = any(t in types for t in (n.CapturedMask, n.HoppedMask,
@@ -351,6 +349,8 @@ class GameLowering(MoveLoweringMixin):
             return self.custodial_anchored(node)
         if t is n.CornerCustodialMask:
             return self.corner_custodial(node)
+        if t is n.LineFn:
+            return self.line_mask(node)
         if t in (n.HoppedMask, n.CapturedMask, n.PromotedMask):   # exprs.py:152-165
             k = {n.HoppedMask: 0, n.CapturedMask: 1, n.PromotedMask: 2}[t]
             return self._tplane(k)
@@ -787,6 +787,105 @@ class GameLowering(MoveLoweringMixin):
     }}""")
         return name
 
+    def line_mask(self, node):
+        """Cells of satisfied windows (reference _compile_line_mask,
+        exprs.py:468-481): every window-start bit spread over its L cells."""
+        stones = self.piece_filter(node.piece, self.stones(self.side(node.player)))
+        excl = self._line_excluded(node) if node.exclude is not None else None
+        name = f"line_mask_{self.em.fresh('m')}"
+        body = []
+        for d in self.board.orientation_dirs(node.orientation):
+            code, r = self._line_axis(node.length, d)
+            body.append("        {")
+            body += code
+            if node.exact:
+                body.append(f"            const BBW rx = lx::andnot(lx::andnot({r}, "
+                            f"{self.nb(OPPOSITE[d], 'b')}), {self.walk(d, node.length, 'b')});")
+                r = "rx"
+            if excl is not None:
+                allowed = np.zeros(self.C, dtype=bool)
+                for _, cells in self.board.line_windows(node.length, d):
+                    if not excl[list(cells)].any():
+                        allowed[cells[0]] = True
+                r = f"({r} & {self.em.const(allowed)})"
+            body.append(f"            const BBW st = {r};")
+            parts = ["st"] + [self.walk(OPPOSITE[d], k, "st") for k in range(1, node.length)]
+            body.append(f"            acc = acc | {' | '.join(parts)};")
+            body.append("        }")
+        self.em.helper(name, f"""    static __device__ __forceinline__ BBW {name}(const BBW& b) {{
+        BBW acc = lx::bb_zero<W>();
+{chr(10).join(body)}
+        return acc;
+    }}""")
+        return f"{name}({stones})"
+
+    def pattern_count(self, node):
+        """Number of placements of an offset pattern owned by the player
+        (reference _compile_pattern, exprs.py:599-626; placements from
+        topology.pattern_table: all distinct rotations with rotate:true).
+        Per normalised variant: anchors with a full placement (constant
+        mask, exclusions applied) AND the player's stones gathered at each
+        offset's constant bit shift; count = sum of popcounts (placements of
+        distinct variants are distinct cell sets)."""
+        B = self.board
+        if node.shape is not None:
+            offs = list(Board(node.shape).coords)
+        else:
+            offs = [(i // node.width, i % node.width) for i in node.offsets]
+        if not offs:
+            _fail("empty pattern")
+
+        def norm(o):
+            amin = min(a for a, _ in o)
+            bmin = min(b for _, b in o)
+            return tuple(sorted(set((a - amin, b - bmin) for a, b in o)))
+        variants = {norm(offs)}
+        if node.rotate:
+            cur = offs
+            hexish = B.kind in ("hexagon", "hex_rectangle")
+            for _ in range((6 if hexish else 4) - 1):
+                cur = [(-b, a + b) for a, b in cur] if hexish else [(b, -a) for a, b in cur]
+                variants.add(norm(cur))
+        excl = None
+        if node.exclude is not None:
+            ex = node.exclude if isinstance(node.exclude, tuple) else (node.exclude,)
+            excl = self._static_union(ex)
+        stones = self.piece_filter(node.piece, self.stones(self.side(node.player)))
+        terms = []
+        for var in sorted(variants):
+            anchors = np.zeros(self.C, dtype=bool)
+            shifts = {}
+            for x, (a, b) in enumerate(B.coords):
+                cells = []
+                for da, db in var:
+                    j = B.cell_at((a + da, b + db))
+                    if j is None:
+                        break
+                    cells.append(j)
+                if len(cells) != len(var):
+                    continue
+                if excl is not None and excl[cells].any():
+                    continue
+                anchors[x] = True
+                for (da, db), j in zip(var, cells):
+                    shifts.setdefault((da, db), set()).add(int(self.bit_of[j]) - int(self.bit_of[x]))
+            if not anchors.any():
+                continue
+            if any(len(v) != 1 for v in shifts.values()):
+                _fail("pattern offsets are not constant bit shifts on this board")
+            parts = [self.em.const(anchors)]
+            for (da, db) in var:
+                S = shifts[(da, db)].pop()
+                parts.append(f"lx::gather<W, {S}>(pb)")
+            terms.append(f"lx::popc({' & '.join(parts)})")
+        if not terms:
+            return "0"
+        name = f"pattern_{self.em.fresh('p')}"
+        self.em.helper(name, f"""    static __device__ __forceinline__ int {name}(const BBW& pb) {{
+        return {' + '.join(terms)};
+    }}""")
+        return f"{name}({stones})"
+
     def line_exists(self, node):
         """Any window of `length` stones of the player (one axis live at a time)."""
         stones = self.piece_filter(node.piece, self.stones(self.side(node.player)))
@@ -1064,6 +1163,8 @@ class GameLowering(MoveLoweringMixin):
             return f"({self.function(node.a)} - {self.function(node.b)})"
         if t is n.LineFn:
             return self.line_count(node)
+        if t is n.PatternFn:
+            return self.pattern_count(node)
         if t is n.ConnectedFn:
             return f"(int){self.connected(node)}"
         _fail(f"function {t.__name__} is not lowered yet")

@@ -32,7 +32,8 @@ def test_fuzz_corpus_coverage():
     assert len(PROGRAMS) - len(unsupported) >= 150
 
 
-@pytest.mark.parametrize("prog", PROGRAMS[::4], ids=lambda p: f"sample-{p['index']}")
+@pytest.mark.parametrize("prog", PROGRAMS[::4],
+                         ids=lambda p: f"s{p.get('sampler', [7])[0]}-{p['index']}")
 def test_fuzz_hostsim_matches_reference(prog):
     from hostsim.hostsim import HostGame
     low = lowered(prog)
