@@ -120,9 +120,11 @@ def test_lowering_words_bit_order():
         (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
         (end (if (connected "s" ((edge top) (edge bottom) (edge left))) (mover win)))))""",
      "three-target connected"),
-    ("""(game "Pat" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
+    ("""(game "Two" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
         (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
-        (end (if (pattern "s" (2 (0 1 2 3))) (mover win)))))""", "pattern"),
+        (end (if (connected "s" ((edge top) (edge bottom)) direction:orthogonal) (mover win))
+             (if (connected "s" ((edge left) (edge right))) (mover win)))))""",
+     "two connectivity plans"),
 ])
 def test_unsupported_raises_compile_error(text, what):
     with pytest.raises(CompileError) as e:
