@@ -1531,6 +1531,14 @@ struct Game {{
         return "\n".join(out)
 
     def effect(self, e):
+        """One effect as a block that sees the board as left by the previous
+        effects (me / op re-read)."""
+        code = self._effect(e)
+        ind = "                "
+        return (f"{ind}{{ const BBW me = mover ? s.own1 : s.own0; const BBW op = mover ? s.own0 : s.own1;\n"
+                f"{ind}  (void)me; (void)op;\n{code}\n{ind}}}")
+
+    def _effect(self, e):
         t = type(e)
         ind = "                "
         if t is n.FlipEffect:
