@@ -644,6 +644,42 @@ class GameLowering(MoveLoweringMixin):
         self.em.helper(name, code)
         return f"{name}(s, mover)"
 
+    def result_sim(self, pred, cand, write_stmt):
+        """Placement result predicate by simulation (reference
+        PlacementMechanics._simulate, mechanics.py:445-461): for every
+        candidate cell, place on a copy of the state (transient masks
+        cleared, last-action fields and reach sets updated as by a real
+        placement) and evaluate the predicate in the anchored context."""
+        name = f"result_sim_{self.em.fresh('r')}"
+        self.anchored_ctx = True
+        try:
+            cond = self.predicate(pred)
+        finally:
+            self.anchored_ctx = False
+        self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}_p(const St& s, int mover) {{
+        const BBW me = mover ? s.own1 : s.own0;
+        const BBW op = mover ? s.own0 : s.own1;
+        (void)me; (void)op;
+        return {cond};
+    }}
+    static __device__ __forceinline__ BBW {name}(const St& s, const BBW& cand) {{
+        const int mover = s.cur;
+        BBW out = lx::bb_zero<W>();
+        for (int w = 0; w < W; w++) {{
+            u32 bits = cand.w[w];
+            while (bits) {{
+                const int b = 32 * w + __ffs(bits) - 1;
+                bits &= bits - 1u;
+                St t = s;
+                clear_transient(t);
+                {write_stmt}
+                if ({name}_p(t, mover)) lx::setbit(out, b);
+            }}
+        }}
+        return out;
+    }}""")
+        return f"{name}(s, {cand})"
+
     def custodial_global(self, node):
         """Every flanked target run on the board (reference
         mask_custodial_global, exprs.py:294-319): a target cell is marked when
@@ -1329,8 +1365,8 @@ class GameLowering(MoveLoweringMixin):
                         and r.mask.mover == mech.owner):
                     legal += f" & {self.would_custodial(r.mask)}"
                 else:
-                    _fail("placement result predicates other than (exists (custodial ...)) "
-                          "by the placing side are not lowered yet")
+                    legal = self.result_sim(r, f"({legal})",
+                                            "write_place(t, bit_cell(b), mover, t.phase);")
             legal_cases.append(f"            case {pi}: return {legal};")
         if self.mech_kind == 0:
             owner_side = [self.side(ph.mechanic.owner) for ph in phases]
@@ -1563,7 +1599,7 @@ struct Game {{
             m = self.mask(e.mask)
             sd = self.side(e.mover)
             fr, to = self.piece_ids[e.from_piece], self.piece_ids[e.to_piece]
-            if self.piece_mode != "planes":
+            if self.piece_mode != "planes" and fr != to:
                 _fail("promotion needs piece-type planes")
             lines = [f"{ind}{{ const BBW me = mover ? s.own1 : s.own0; const BBW op = mover ? s.own0 : s.own1;",
                      f"{ind}  (void)me; (void)op;",

@@ -598,6 +598,11 @@ class MoveLoweringMixin:
         whose actions are the legal cells (reference PlacementMechanics,
         mechanics.py:415-515)."""
         from .lowering import _fail
+        g = MoveGroup(KIND_PLACE, mech.piece, 0, "", "", phase=pi, owner=self.side(mech.owner))
+        wname = f"place_write_p{pi}"
+        self.em.helper(wname, f"""    static __device__ __forceinline__ void {wname}(St& s, int a, int mover) {{
+{self._place_write(g, "        ")}
+    }}""")
         legal = f"(lx::andnot({self.em.const(self.valid)}, s.own0 | s.own1) & {self.mask(mech.destination)})"
         if mech.result is not None:
             r = mech.result
@@ -605,10 +610,9 @@ class MoveLoweringMixin:
                     and r.mask.mover == mech.owner):
                 legal = f"({legal} & {self.would_custodial(r.mask)})"
             else:
-                _fail("placement result predicates other than (exists (custodial ...)) "
-                      "by the placing side are not lowered yet")
-        return MoveGroup(KIND_PLACE, mech.piece, 0, "", "", phase=pi, legal=legal,
-                         owner=self.side(mech.owner))
+                legal = self.result_sim(r, legal, f"{wname}(t, bit_cell(b), mover);")
+        g.legal = legal
+        return g
 
     def _place_write(self, g, ind):
         """_write_placement (mechanics.py:463-479) of a placement phase."""
@@ -749,8 +753,8 @@ class MoveLoweringMixin:
         pick_g = ("hint >= 0 ? hint : claim(s, mover, bs, bd)" if all(safe) else
                   "(hint >= 0 && group_safe(hint)) ? hint : claim(s, mover, bs, bd)")
         place_apply = phase_switch(
-            lambda pi, idx: (self._place_write(groups[idx[0]], "                ")
-                             + "\n                return;") if is_place[pi] else None)
+            lambda pi, idx: (f"                place_write_p{pi}(s, a, mover);\n"
+                             f"                return;") if is_place[pi] else None)
         place_legal = phase_switch(
             lambda pi, idx: (f"                return a < {C} && "
                              f"lx::test({groups[idx[0]].legal}, cell_bit(a));") if is_place[pi] else None)

@@ -113,9 +113,10 @@ def test_lowering_words_bit_order():
 
 
 @pytest.mark.parametrize("text,what", [
-    ("""(game "Res" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
-        (rules (play (repeat (P1 P2) (place "s" (destination (empty)) (result (full_board)))))
-        (end (if (full_board) (draw)))))""", "simulated placement result"),
+    ("""(game "Dyn" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
+        (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
+        (end (if (connected "s" ((edge top) (adjacent (occupied)))) (mover win)))))""",
+     "dynamic connected target"),
     ("""(game "Tri" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
         (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
         (end (if (connected "s" ((edge top) (edge bottom) (edge left))) (mover win)))))""",
