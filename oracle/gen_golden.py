@@ -258,9 +258,9 @@ def jsonl_fixtures():
     print("wrote jsonl.json")
 
 
-def fuzz_fixtures(corpora=((7, 5, 150), (11, 6, 120)), tries=20000):
+def fuzz_fixtures(corpora=((7, 5, 150), (11, 6, 120), (23, 8, 150), (31, 10, 150)), tries=20000):
     """Programs from the reference's own random generator (generator.py,
-    sample_game with SamplerConfig(seed=7) and (seed=11, max_depth=6)) that the reference compiles and
+    sample_game; sampler seeds 7, 11, 23, 31 at depths 5, 6, 8, 10) that the reference compiles and
     plays (playout_random, B=16, 60-ply cap) -- a corpus for checking the
     lowering's generality: every one must either be lowered bit-exactly or
     rejected with CompileError."""
@@ -305,7 +305,31 @@ def _fuzz_corpus(sampler_seed, depth, limit, tries, timeout_exc):
     return out
 
 
+def validate_fixtures(per_corpus=150):
+    """Validation reports of generated programs, valid or not (validate.py,
+    raised as ValidationFailure by load_game)."""
+    from boardlang.generator import SamplerConfig, sample_game
+    from boardlang.topology import build_topology
+    from boardlang.validate import validate
+    out = []
+    for seed, depth in ((7, 5), (11, 6), (23, 8), (31, 10)):
+        for i in range(per_corpus):
+            text = sample_game(SamplerConfig(seed=seed, max_depth=depth), index=i)
+            try:
+                spec = parse_game(text)
+                rep = str(validate(spec, build_topology(spec.equipment.board)))
+            except Exception as exc:
+                rep = f"EXC {type(exc).__name__}: {exc}"
+            out.append({"sampler": [seed, depth], "index": i, "text": text, "report": rep})
+    with open(os.path.join(OUT, "validate.json"), "w") as fh:
+        json.dump(out, fh, indent=0, sort_keys=True)
+    print("wrote validate.json", len(out), sum(o["report"] == "valid" for o in out), "valid")
+
+
 if __name__ == "__main__":
+    if "--validate" in sys.argv:
+        validate_fixtures()
+        sys.exit(0)
     if "--fuzz" in sys.argv:
         fuzz_fixtures()
         sys.exit(0)

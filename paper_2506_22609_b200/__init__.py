@@ -11,7 +11,8 @@ kernels compiled with NVRTC behind the C-ABI in include/ludax_b200.h.
 
 from . import agents, engine, evaluation, rng  # noqa: F401
 from .errors import (BoardLangError, CompileError, EmptyMask, IllegalAction,  # noqa: F401
-                     ParseError, TerminalState)
+                     ParseError, TerminalState, ValidationFailure)
+from .validate import validate  # noqa: F401
 from .game import (B200Game, DeviceState, compile_game, load_config_game,  # noqa: F401
                    load_game, precompile)
 from .env import EnvState, LudaxEnvironment  # noqa: F401

@@ -33,6 +33,14 @@ class ArityError(ParseError):
     """Wrong number / type of arguments (reference errors.py:28)."""
 
 
+class ValidationFailure(BoardLangError):
+    """Semantic check findings (reference errors.py:32-37); str = the report."""
+
+    def __init__(self, report):
+        self.report = report
+        super().__init__(str(report))
+
+
 class InvalidShapeParam(BoardLangError):
     """Board shape parameters out of range (reference errors.py:40)."""
 

@@ -575,9 +575,16 @@ def compile_game(spec):
 
 
 def load_game(text):
-    """Parse + lower (+ NVRTC on first device use); raises on any failure
-    (reference __init__.py:34-41 load_game)."""
+    """Parse, validate, lower (+ NVRTC on first device use); raises on any
+    failure like the reference (__init__.py:34-41 load_game): ParseError,
+    InvalidShapeParam, ValidationFailure, CompileError."""
+    from .errors import ValidationFailure
+    from .geometry import Board
+    from .validate import validate
     spec = parse_game(text)
+    report = validate(spec, Board(spec.equipment.board))
+    if not report.ok:
+        raise ValidationFailure(report)
     return B200Game(spec, text)
 
 
