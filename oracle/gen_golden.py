@@ -305,6 +305,35 @@ def _fuzz_corpus(sampler_seed, depth, limit, tries, timeout_exc):
     return out
 
 
+def gavel_fixtures(n_valid=10, n_invalid=4):
+    """GAVEL reports (evaluation.evaluate_game) of generated programs: valid
+    ones (playable or stuck) and a few invalid ones, small match config."""
+    from boardlang.evaluation import EvalConfig, evaluate_game
+    from boardlang.generator import SamplerConfig, sample_game
+    from boardlang.topology import build_topology
+    from boardlang.validate import validate
+    cfg = {"matches": 4, "strong_iterations": 8, "weak_iterations": 4, "max_turns": 60, "seed": 3}
+    out, nv, ni = [], 0, 0
+    for i in range(2000):
+        if nv >= n_valid and ni >= n_invalid:
+            break
+        text = sample_game(SamplerConfig(seed=11, max_depth=6), index=i)
+        spec = parse_game(text)
+        ok = validate(spec, build_topology(spec.equipment.board)).ok
+        if (ok and nv >= n_valid) or (not ok and ni >= n_invalid):
+            continue
+        rep = evaluate_game(text, EvalConfig(**cfg)).as_dict()
+        if ok:
+            nv += 1
+        else:
+            ni += 1
+        out.append({"index": i, "text": text, "report": {k: (float.hex(v) if isinstance(v, float)
+                                                            else v) for k, v in rep.items()}})
+        print("gavel", i, rep.get("playable"), rep.get("diagnostic", "")[:60])
+    with open(os.path.join(OUT, "gavel.json"), "w") as fh:
+        json.dump({"config": cfg, "programs": out}, fh, indent=0, sort_keys=True)
+
+
 def validate_fixtures(per_corpus=150):
     """Validation reports of generated programs, valid or not (validate.py,
     raised as ValidationFailure by load_game)."""
@@ -327,6 +356,9 @@ def validate_fixtures(per_corpus=150):
 
 
 if __name__ == "__main__":
+    if "--gavel" in sys.argv:
+        gavel_fixtures()
+        sys.exit(0)
     if "--validate" in sys.argv:
         validate_fixtures()
         sys.exit(0)
