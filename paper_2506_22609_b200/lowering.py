@@ -277,7 +277,8 @@ class GameLowering(MoveLoweringMixin):
         for m in masks:
             s = self.static_mask(m)
             if s is None:
-                _fail(f"{type(m).__name__} is not a static mask")
+                # the reference cannot compile this either (exprs.py:92-97)
+                raise UnsupportedConstruct(f"{type(m).__name__} is not static")
             out |= s
         return out
 
@@ -976,9 +977,8 @@ class GameLowering(MoveLoweringMixin):
         else:
             targets = [self.static_mask(m) for m in node.masks]
             if any(t is None for t in targets):
-                _fail("connected targets must be static masks")
-        if len(targets) != 2:
-            _fail("connected with other than two targets is not lowered yet")
+                bad = next(m for m, t in zip(node.masks, targets) if t is None)
+                raise UnsupportedConstruct(f"{type(bad).__name__} is not static")
         return targets
 
     def _dilate(self, plan, var):
@@ -1046,6 +1046,8 @@ class GameLowering(MoveLoweringMixin):
                 sides = [1]
             else:
                 sides = [0, 1]
+            if len(self._conn_targets(node)) != 2:
+                return                      # no reach set: per-component flood test
             for sd in sides:
                 key = (id(node), sd)
                 if key not in self.conn_slots:
@@ -1087,6 +1089,8 @@ class GameLowering(MoveLoweringMixin):
         (reference exprs.py:629-652, labels from connectivity.py)."""
         plan = self.conn_plans[self._conn_plan(node)]
         targets = self._conn_targets(node)
+        if len(targets) != 2:
+            return self._connected_multi(node, plan, targets)
         t0, t1 = self.em.const(targets[0]), self.em.const(targets[1])
         slots = {sd: k for (nid, sd), k in self.conn_slots.items() if nid == id(node)}
         if slots:
@@ -1110,6 +1114,30 @@ class GameLowering(MoveLoweringMixin):
             f = g;
         }}
         return lx::any(f & {t1});
+    }}""")
+        return f"{name}({stones})"
+
+    def _connected_multi(self, node, plan, targets):
+        """Any number of targets: flood each component that touches target 0
+        in turn and test it against every other target."""
+        stones = self.stones(self.side(node.mover))
+        ts = [self.em.const(t) for t in targets]
+        dil_f = self._dilate(plan, "f")
+        touch = " && ".join(f"lx::any(f & {t})" for t in ts[1:]) or "true"
+        name = f"connected_multi_{self.em.fresh('k')}"
+        self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const BBW& mine) {{
+        BBW rem = mine & {ts[0]};
+        while (lx::any(rem)) {{
+            BBW f = lx::onehot<W>(lx::select_bit(rem, 0));
+            while (true) {{
+                const BBW g = (f | {dil_f}) & mine;
+                if (lx::equal(g, f)) break;
+                f = g;
+            }}
+            if ({touch}) return true;
+            rem = lx::andnot(rem, f);
+        }}
+        return false;
     }}""")
         return f"{name}({stones})"
 
@@ -1650,5 +1678,5 @@ struct Game {{
 def lower_game(spec):
     try:
         return GameLowering(spec).lower()
-    except (KeyError, UnsupportedConstruct) as exc:
+    except KeyError as exc:
         raise CompileError("lower", str(exc)) from exc

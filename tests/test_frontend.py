@@ -113,14 +113,10 @@ def test_lowering_words_bit_order():
 
 
 @pytest.mark.parametrize("text,what", [
-    ("""(game "Dyn" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
+    ("""(game "AX" (players 2) (equipment (board (square 8)) (pieces ("s" both)))
         (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
-        (end (if (connected "s" ((edge top) (adjacent (occupied)))) (mover win)))))""",
-     "dynamic connected target"),
-    ("""(game "Tri" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
-        (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
-        (end (if (connected "s" ((edge top) (edge bottom) (edge left))) (mover win)))))""",
-     "three-target connected"),
+        (end (if (and (mover_is P1) (line "s" 4 exact:true exclude:((row 0)))) (mover win))
+             (if (full_board) (draw)))))""", "exact anchored line with exclude"),
     ("""(game "Two" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
         (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
         (end (if (connected "s" ((edge top) (edge bottom)) direction:orthogonal) (mover win))
@@ -131,3 +127,15 @@ def test_unsupported_raises_compile_error(text, what):
     with pytest.raises(CompileError) as e:
         lowering.lower_game(syntax.parse_game(text))
     assert e.value.stage == "lower"
+
+
+def test_reference_unsupported_constructs_raise_like_the_reference():
+    """Constructs the reference cannot compile either raise its
+    UnsupportedConstruct with its message (exprs.py:92-97)."""
+    from paper_2506_22609_b200.errors import UnsupportedConstruct
+    text = """(game "Dyn" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
+        (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
+        (end (if (connected "s" ((edge top) (adjacent (occupied)))) (mover win)))))"""
+    with pytest.raises(UnsupportedConstruct) as e:
+        lowering.lower_game(syntax.parse_game(text))
+    assert str(e.value) == "AdjacentMask is not static"

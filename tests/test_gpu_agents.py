@@ -97,3 +97,17 @@ def test_benchmark_throughput_report():
     rep = evaluation.benchmark_throughput(g, [1024, 4096], warmup_episodes=2, episodes=3)
     assert rep.rate("Connect Four", 4096) > 0
     assert rep.to_csv().startswith("game,batch_size")
+
+
+with open(os.path.join(GOLDEN, "gavel.json")) as f:
+    GAVEL = json.load(f)
+
+
+@pytest.mark.parametrize("prog", GAVEL["programs"], ids=lambda p: f"sample-{p['index']}")
+def test_gavel_on_generated_programs(prog):
+    """evaluate_game on programs from the reference's generator: same
+    playable verdicts, diagnostics (ValidationFailure / EmptyMask /
+    UnsupportedConstruct text) and scores as the reference."""
+    rep = evaluation.evaluate_game(prog["text"], evaluation.EvalConfig(**GAVEL["config"]))
+    got = {k: (float.hex(v) if isinstance(v, float) else v) for k, v in rep.as_dict().items()}
+    assert got == prog["report"]
