@@ -140,6 +140,15 @@ __device__ __forceinline__ void write_mask_moves(unsigned char* __restrict__ mas
 
 
 // ---------------------------------------------------------------- kernels
+//
+// The native runtime compiles the kernels in groups, one NVRTC program per
+// group in parallel (LX_GROUP = group id; unset: every kernel):
+//   0 init / rollout / export / import   1 legal / sample / observe
+//   2 verify / step / random_step        3 expand (MCTS)   4 env_step
+#ifndef LX_GROUP
+#define LX_GROUP -1
+#endif
+#define LX_IN_GROUP(g) (LX_GROUP < 0 || LX_GROUP == (g))
 
 struct LxRefPtrs {               // reference GameState field pointers (state.py:78-130)
     signed char* board_piece;    // (B, C) int8, -1 empty
@@ -167,6 +176,7 @@ struct LxRefPtrs {               // reference GameState field pointers (state.py
     unsigned char* promoted_mask;
 };
 
+#if LX_IN_GROUP(0)
 extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const u64* seeds,
                                                           u64 seed_base, i64 first) {
     const i64 i = lx::gtid();
@@ -176,9 +186,11 @@ extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const 
     lx::init_state<Game>(s, seed);
     lx::store_state<Game>(s, st, B, i);
 }
+#endif
 
 // (B, A) uint8 mask (null to skip) and (B,) int64 counts (null to skip);
 // terminated rows are all-false / zero (reference compiler.py:394-428)
+#if LX_IN_GROUP(1)
 extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
                                                            unsigned char* mask, i64* counts) {
     const i64 i = lx::gtid();
@@ -209,8 +221,10 @@ extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
         if (mask) lx::write_mask_moves<Game>(mask, B, i, valid, s, live, pass_only);
     }
 }
+#endif
 
 // sampled action per row from u (when given) or from the row's own stream
+#if LX_IN_GROUP(1)
 extern "C" __global__ void __launch_bounds__(256) lx_sample(const u32* st, i64 B,
                                                             const double* u, i64* actions) {
     const i64 i = lx::gtid();
@@ -236,8 +250,10 @@ extern "C" __global__ void __launch_bounds__(256) lx_sample(const u32* st, i64 B
         actions[i] = Game::select_move(s, (int)r, tot, hint);
     }
 }
+#endif
 
 // verification pass: *bad = min illegal live row (init to ~0 by the caller)
+#if LX_IN_GROUP(2)
 extern "C" __global__ void __launch_bounds__(256) lx_verify(const u32* st, i64 B,
                                                             const i64* actions,
                                                             const unsigned char* rows,
@@ -250,8 +266,10 @@ extern "C" __global__ void __launch_bounds__(256) lx_verify(const u32* st, i64 B
     if (s.term) return;
     if (!lx::action_legal<Game>(s, actions[i])) atomicMin(bad, (u64)i);
 }
+#endif
 
 // in-place step of live rows (rows & ~terminated)
+#if LX_IN_GROUP(2)
 extern "C" __global__ void __launch_bounds__(256) lx_step(u32* st, i64 B, const i64* actions,
                                                           const unsigned char* rows) {
     const i64 i = lx::gtid();
@@ -263,8 +281,10 @@ extern "C" __global__ void __launch_bounds__(256) lx_step(u32* st, i64 B, const 
     lx::apply_step<Game>(s, (int)actions[i]);
     lx::store_state<Game>(s, st, B, i);
 }
+#endif
 
 // fused sample+step for live rows, one ply (engine.random_actions + step_into)
+#if LX_IN_GROUP(2)
 extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B, int max_turns,
                                                                  i64* actions_out) {
     const i64 i = lx::gtid();
@@ -279,6 +299,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
     lx::apply_step<Game>(s, a, hint);
     lx::store_state<Game>(s, st, B, i);
 }
+#endif
 
 // Fused rollout.  Persistent threads: each thread plays one env at a time to
 // the end with the whole state in registers, then starts another, so no lane
@@ -308,6 +329,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
 #ifndef LX_REFILL_WAIT
 #define LX_REFILL_WAIT 6
 #endif
+#if LX_IN_GROUP(0)
 extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB)
 lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* seeds, i64 first,
            u64* stats, u64* counter, u64* stuck, signed char* outcomes, int* turns) {
@@ -441,6 +463,7 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
         atomicAdd(stats + 5, (u64)n_done);
     }
 }
+#endif
 
 // MCTS expansion + rollout, one thread per expanded child (reference
 // agents._Search._attach_and_rollout + _rollout, agents.py:211-238, 313-353).
@@ -451,6 +474,7 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
 // when it is live and has a legal action, the outcome of one uniform-random
 // rollout from it drawing with seeds[i] (0 draw / stuck / cap, 1 P1, 2 P2)
 // in rolled[i] (else -1).
+#if LX_IN_GROUP(3)
 extern "C" __global__ void __launch_bounds__(128) lx_expand(u32* pool, i64 cap, const i64* parents,
                                                             const i64* actions,
                                                             const i64* children, i64 n,
@@ -499,6 +523,7 @@ extern "C" __global__ void __launch_bounds__(128) lx_expand(u32* pool, i64 cap, 
     }
     rolled[i] = out;
 }
+#endif
 
 // PGX-style environment step (env.LudaxEnvironment.step), one launch per ply:
 // apply actions[i] to live rows (actions == null: no move, just refresh the
@@ -507,6 +532,7 @@ extern "C" __global__ void __launch_bounds__(128) lx_expand(u32* pool, i64 cap, 
 // max_turns (> 0), optionally auto-reset finished rows with seed
 // hash_key(seed, 0xE9) (engine.reset_rows, engine.py:58-65), and write the
 // legal mask / flags / player of the resulting state.
+#if LX_IN_GROUP(4)
 extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, const i64* actions,
                                                               int max_turns, int auto_reset,
                                                               unsigned char* mask, float* rewards,
@@ -554,8 +580,10 @@ extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, co
         else lx::write_mask_moves<Game>(mask, B, i, valid, s, live, pass_only);
     }
 }
+#endif
 
 // device state -> reference GameState SoA (state.py:78-130)
+#if LX_IN_GROUP(0)
 extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B, LxRefPtrs p) {
     const i64 i = lx::gtid();
     if (i >= B) return;
@@ -597,8 +625,10 @@ extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B
                                               p.captured_mask + i * Game::C,
                                               p.promoted_mask + i * Game::C);
 }
+#endif
 
 // reference GameState SoA -> device state (inverse of lx_export)
+#if LX_IN_GROUP(0)
 extern "C" __global__ void __launch_bounds__(128) lx_import(u32* st, i64 B, LxRefPtrs p) {
     const i64 i = lx::gtid();
     if (i >= B) return;
@@ -643,10 +673,12 @@ extern "C" __global__ void __launch_bounds__(128) lx_import(u32* st, i64 B, LxRe
     Game::rebuild_ext(s);
     lx::store_state<Game>(s, st, B, i);
 }
+#endif
 
 // (B, 2T+1, C) uint8 relative-owner planes (reference compiler.py:611-626):
 // per piece type t the player's and the opponent's pieces of type t, then
 // the is-mover plane
+#if LX_IN_GROUP(1)
 extern "C" __global__ void __launch_bounds__(128) lx_observe(const u32* st, i64 B, int player,
                                                              unsigned char* planes) {
     const i64 i = lx::gtid();
@@ -668,3 +700,5 @@ extern "C" __global__ void __launch_bounds__(128) lx_observe(const u32* st, i64 
     }
     for (int c = 0; c < Game::C; c++) out[2 * T * Game::C + c] = mv;
 }
+#endif
+

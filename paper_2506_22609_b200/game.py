@@ -600,10 +600,10 @@ def precompile(names=("tic_tac_toe", "connect_four", "hex", "reversi", "pente"),
         with open(os.path.join(GAMES_DIR, f"{name}.ldx")) as f:
             low = lower_game(parse_game(f.read()))
         keys[name] = native.compile_only(low.source, low.name)
-    if prune:
-        live = {f"{k}.cubin" for k in keys.values()}
+    if prune:                       # cubins are <key>-g<group>.cubin
+        live = set(keys.values())
         for fn in os.listdir(native.CACHE_DIR):
-            if fn.endswith(".cubin") and fn not in live:
+            if fn.endswith(".cubin") and fn.split("-g")[0] not in live:
                 os.remove(os.path.join(native.CACHE_DIR, fn))
     return keys
 

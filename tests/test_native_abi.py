@@ -26,12 +26,13 @@ def test_every_header_symbol_is_exported():
 
 
 def test_nvrtc_compiles_config_games_for_sm100a():
-    keys = precompile()
+    keys = precompile(prune=False)
     for k in keys.values():
-        path = os.path.join(native.CACHE_DIR, f"{k}.cubin")
-        with open(path, "rb") as f:
-            head = f.read(64)
-        assert head[:4] == b"\x7fELF"
+        for g in range(5):                     # one cubin per kernel group
+            path = os.path.join(native.CACHE_DIR, f"{k}-g{g}.cubin")
+            with open(path, "rb") as f:
+                head = f.read(64)
+            assert head[:4] == b"\x7fELF"
 
 
 def test_create_without_gpu_fails_cleanly():
