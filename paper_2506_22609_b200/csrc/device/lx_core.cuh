@@ -139,6 +139,18 @@ __device__ __forceinline__ void setbit(BB<W>& a, int c) {
 #pragma unroll
     for (int i = 0; i < W; i++) a.w[i] |= (word == (u32)i) ? bit : 0u;
 }
+// set bit c in b when to_b, else in a (one LOP3 per word per board)
+template <int W>
+__device__ __forceinline__ void place_bit(BB<W>& a, BB<W>& b, int c, bool to_b) {
+    const u32 word = (u32)c >> 5, bit = 1u << (c & 31);
+    const u32 m = to_b ? 0xffffffffu : 0u;
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+        const u32 v = (word == (u32)i) ? bit : 0u;
+        a.w[i] |= v & ~m;
+        b.w[i] |= v & m;
+    }
+}
 template <int W>
 __device__ __forceinline__ void clearbit(BB<W>& a, int c) {
     const u32 word = (u32)c >> 5, bit = 1u << (c & 31);
@@ -220,6 +232,12 @@ struct Mirror {
     static __device__ __forceinline__ u32* slot() {
         __shared__ u32 buf[2 * W * LX_MIRROR_STRIDE];
         return buf + threadIdx.x;
+    }
+    // one player's plane only (readers of that plane need nothing else)
+    static __device__ __forceinline__ void store_plane(int player, const BB<W>& p) {
+        u32* m = slot();
+#pragma unroll
+        for (int i = 0; i < W; i++) m[(player * W + i) * LX_MIRROR_STRIDE] = p.w[i];
     }
     static __device__ __forceinline__ void store(const BB<W>& p0, const BB<W>& p1) {
         u32* m = slot();

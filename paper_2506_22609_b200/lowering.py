@@ -583,7 +583,7 @@ class GameLowering(MoveLoweringMixin):
         const int side = {side};
         if (!(s.last_dest >= 0 && s.last_mover == mover)) return false;
         const int c = cell_bit(s.last_dest);
-        M::store(s.own0, s.own1);
+        M::store_plane(side, side ? s.own1 : s.own0);   // only the player's stones are probed
         if (!M::probe(side, c)) return false;
         const int r = c / {self.emb_cols};
         const int col = c - r * {self.emb_cols};
@@ -1407,7 +1407,7 @@ class GameLowering(MoveLoweringMixin):
                 t = self.piece_ids[ph.mechanic.piece]
                 if self.piece_mode == "planes" and t >= 1:
                     place_planes.append(f"        if (phase == {pi}) {{ BBW pl = {self._plane(t)}; "
-                                        f"pl = pl | oh; {self._plane_set(t, 'pl')} }}")
+                                        f"pl = pl | lx::onehot<W>(cell_bit(cell)); {self._plane_set(t, 'pl')} }}")
             place_planes = "\n".join(place_planes)
         elif self.mech_kind == 1:
             mech_code = self.movement_code(phases) + "\n" + self.movement_stubs()
@@ -1472,6 +1472,7 @@ class GameLowering(MoveLoweringMixin):
         conn_rebuild = self._conn_rebuild_code()
         self.ngc = {0: 1, 1: len(getattr(self, "groups", ())) or 1,
                     2: len(self.grid[2]) if self.grid else 1}[self.mech_kind]
+        place_code = "        lx::place_bit(s.own0, s.own1, cell_bit(cell), side != 0);   // branchless"
         if self.mech_kind == 0:
             mech_code = f"""    static constexpr int MECH = 0;
     static __device__ __forceinline__ BBW legal(const St& s) {{
@@ -1486,9 +1487,7 @@ class GameLowering(MoveLoweringMixin):
     }}
     static __device__ __forceinline__ void write_place(St& s, int cell, int mover, int phase) {{
         const int side = {owner};
-        const BBW oh = lx::onehot<W>(cell_bit(cell));   // branchless: no warp split on the mover
-        s.own0 = lx::sel(side != 0, s.own0 | oh, s.own0);
-        s.own1 = lx::sel(side != 0, s.own1, s.own1 | oh);
+{place_code}
         s.last_kind = 0; s.last_dest = cell; s.last_source = -1; s.last_mover = side;
         s.ldbp0 = side ? s.ldbp0 : cell;
         s.ldbp1 = side ? cell : s.ldbp1;
