@@ -1174,17 +1174,18 @@ class GameLowering(MoveLoweringMixin):
                         f"            const BBW t0 = {self.em.const(self.slot_info[k][1][0])};")
                 store = self._slot_set(k, "R")
                 cond = f"side == {sd}"
+            flood = (f"                BBW f = a;                       // grow inside the side's stones outside R\n"
+                     f"                BBW g = (f | {dil_f}) & free_;\n"
+                     f"                while (!lx::equal(g, f)) {{\n"
+                     f"                    f = g;\n"
+                     f"                    g = (f | {dil_f}) & free_;\n"
+                     f"                }}")
             out.append(f"""{head}
             const BBW a = lx::onehot<W>(cell_bit(cell));
             if (({cond}) && lx::any((a & t0) | (({dil_a}) & R))) {{
                 const BBW mine = side ? s.own1 : s.own0;
                 const BBW free_ = lx::andnot(mine, R);
-                BBW f = a;                               // grow inside the side's stones outside R
-                BBW g = (f | {dil_f}) & free_;
-                while (!lx::equal(g, f)) {{
-                    f = g;
-                    g = (f | {dil_f}) & free_;
-                }}
+{flood}
                 R = R | f;
                 {store}
             }}
