@@ -293,25 +293,32 @@ class B200Game:
         torch = _torch()
         n = len(parents)
         A = self.codec.size
-        host = np.empty(4 * n, dtype=np.int64)
+        nb = 4 * n + n + (n * A if masks else 0)
+        bufs = getattr(self, "_xbufs", None)        # pinned + device staging, reused
+        if bufs is None or bufs[0].numel() < 4 * n or bufs[2].numel() < nb:
+            cap_in, cap_out = max(4 * n, 4096), max(nb, 1 << 16)
+            bufs = (torch.empty(cap_in, dtype=torch.int64).pin_memory(),
+                    torch.empty(cap_in, dtype=torch.int64, device="cuda"),
+                    torch.empty(cap_out, dtype=torch.uint8).pin_memory(),
+                    torch.empty(cap_out, dtype=torch.uint8, device="cuda"))
+            self._xbufs = bufs
+        pin_in, dev_in, pin_out, dev_out = bufs
+        host = pin_in.numpy()
         host[:n] = parents
         host[n:2 * n] = actions
         host[2 * n:3 * n] = children
-        host[3 * n:] = np.asarray(seeds, dtype=np.uint64).view(np.int64)
-        dev_in = torch.from_numpy(host).pin_memory().to("cuda", non_blocking=True)
-        nb = 4 * n + n + (n * A if masks else 0)
-        out = torch.empty(nb, dtype=torch.uint8, device="cuda")
-        info = out[:4 * n]
-        rolled = out[4 * n:5 * n]
-        mk = out[5 * n:] if masks else None
+        host[3 * n:4 * n] = np.asarray(seeds, dtype=np.uint64).view(np.int64)
+        dev_in[:4 * n].copy_(pin_in[:4 * n], non_blocking=True)
         p = dev_in.data_ptr()
+        o = dev_out.data_ptr()
         native.check(native.lib().lx_expand(
             self.handle, pool_words.data_ptr(), int(cap), p, p + 8 * n, p + 16 * n, n, p + 24 * n,
-            int(max_turns), info.data_ptr(), rolled.data_ptr(),
-            mk.data_ptr() if mk is not None else None, self._stream()))
-        h = out.cpu().numpy()
-        return (h[:4 * n].view(np.int32), h[4 * n:5 * n].view(np.int8),
-                h[5 * n:].reshape(n, A).astype(bool) if masks else None)
+            int(max_turns), o, o + 4 * n, (o + 5 * n) if masks else None, self._stream()))
+        pin_out[:nb].copy_(dev_out[:nb], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h = pin_out.numpy()
+        return (h[:4 * n].view(np.int32).copy(), h[4 * n:5 * n].view(np.int8).copy(),
+                h[5 * n:nb].reshape(n, A).astype(bool) if masks else None)
 
     def truncate_rows(self, state, rows):
         """Mark rows terminated + truncated with a draw outcome in place (the
