@@ -475,6 +475,246 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
 // rollout from it drawing with seeds[i] (0 draw / stuck / cap, 1 P1, 2 P2)
 // in rolled[i] (else -1).
 #if LX_IN_GROUP(3)
+namespace lx {
+
+// ---- device MCTS (one thread per search tree) --------------------------------
+// The reference's UCB1 search (agents._Search, agents.py:84-310) per tree:
+// forced prefix of root expansions, then iterations of selection / one-child
+// expansion / uniform-random rollout / backpropagation, then the best root
+// child.  Trees are independent, so one thread running its tree's iterations
+// in order reproduces the reference's lockstep batches exactly.  Node states
+// live in a pool (row = tree * nmax + node); node records and action lists
+// in a per-tree arena.  UCB arithmetic is IEEE double with no contraction
+// (--fmad=false) and log(N) from a host table, so every comparison matches
+// the reference's Python floats.
+struct MctsNode {
+    int N, to_move, term, outcome, stuck, nacts, nexp, acts;   // acts: arena offset (-1: unbuilt)
+    double W;
+};
+
+template <class G>
+__device__ __forceinline__ int mcts_legal(const typename G::St& s, short* out) {
+    int n = 0;
+    if (s.term) return 0;
+    if constexpr (G::MECH == 0) {
+        const BB<G::W> legal = G::legal(s);
+#pragma unroll
+        for (int w = 0; w < G::W; w++) {
+            u32 b = legal.w[w];
+            while (b) { const int x = 32 * w + __ffs(b) - 1; b &= b - 1u; out[n++] = (short)G::bit_cell(x); }
+        }
+    } else {
+        G::enum_moves(s, [&](int a) { out[n++] = (short)a; });
+    }
+    if (n == 0 && G::PASS >= 0 && G::force_pass(s.phase)) out[n++] = (short)G::PASS;
+    return n;
+}
+
+}  // namespace lx
+
+// status[t]: 0 ok, 1 arena or path capacity exceeded (the caller falls back)
+extern "C" __global__ void __launch_bounds__(32) lx_mcts(
+        const u32* roots, i64 n, const u64* keys, const int* budgets, double c,
+        int rollout_max_turns, const double* logs, int nlogs, u32* pool, i64 pool_rows, int nmax,
+        unsigned char* arena, i64 arena_bytes, i64* actions_out, int* status) {
+    const i64 t = lx::gtid();
+    if (t >= n) return;
+    using lx::MctsNode;
+    typedef Game::St St;
+    constexpr int MAXPATH = 256;
+    MctsNode* nodes = reinterpret_cast<MctsNode*>(arena + t * arena_bytes);
+    short* acts = reinterpret_cast<short*>(nodes + nmax);
+    const i64 acap = (arena_bytes - (i64)nmax * (i64)sizeof(MctsNode)) / 4;   // shorts: acts + kids
+    short* kids = acts + acap;
+    i64 aused = 0;
+    status[t] = 0;
+    const u64 key = keys[t];
+    const int budget = budgets[t];
+    const u64 k0 = lx::mix64(lx::HASH_SEED ^ key);
+    const u64 k_order = lx::mix64(k0 ^ 0xA11ull), k_roll = lx::mix64(k0 ^ 0x5011ull),
+              k_best = lx::mix64(k0 ^ 0x7Eull);
+    const i64 base = t * (i64)nmax;
+    int nnodes = 0;
+    bool overflow = false;
+
+    auto meta = [&](MctsNode& nd, const St& s) {
+        nd.N = 0; nd.W = 0.0; nd.to_move = s.cur; nd.term = s.term; nd.outcome = s.outcome;
+        nd.nacts = 0; nd.nexp = 0; nd.acts = -1;
+    };
+    // untried order: legal actions sorted by hash_key(key, 0xA11, a), ties by a
+    auto build = [&](MctsNode& nd, const St& s) {
+        short* out = acts + aused;
+        if (aused + Game::A + 1 > acap) { overflow = true; nd.acts = (int)aused; nd.nacts = 0; return; }
+        int m = lx::mcts_legal<Game>(s, out);
+        for (int i = 1; i < m; i++) {                    // insertion sort by (hash, action)
+            const short a = out[i];
+            const u64 h = lx::mix64(k_order ^ (u64)(i64)a);
+            int j = i - 1;
+            while (j >= 0) {
+                const u64 hj = lx::mix64(k_order ^ (u64)(i64)out[j]);
+                if (hj < h || (hj == h && out[j] <= a)) break;
+                out[j + 1] = out[j];
+                j--;
+            }
+            out[j + 1] = a;
+        }
+        int u = 0;                                       // drop duplicates (adjacent after sort)
+        for (int i = 0; i < m; i++)
+            if (u == 0 || out[u - 1] != out[i]) out[u++] = out[i];
+        nd.acts = (int)aused;
+        nd.nacts = u;
+        aused += u;
+    };
+    auto value_for = [](int player, int outcome) -> double {
+        if (outcome == 0) return 0.0;
+        return outcome == player + 1 ? 1.0 : -1.0;
+    };
+    int path[MAXPATH];
+    auto backprop = [&](int len, int outcome) {
+        nodes[path[0]].N += 1;
+        for (int i = 1; i < len; i++) {
+            nodes[path[i]].N += 1;
+            nodes[path[i]].W += value_for(nodes[path[i - 1]].to_move, outcome);
+        }
+    };
+    // child of `parent` by its next untried action; returns the backed-up value
+    auto expand = [&](int parent, int action, int& child, u64 rkey, bool do_roll) -> int {
+        St s;
+        lx::load_state<Game>(s, pool, pool_rows, base + parent);
+        if (!s.term) lx::apply_step<Game>(s, action);
+        child = nnodes++;
+        lx::store_state<Game>(s, pool, pool_rows, base + child);
+        MctsNode& nd = nodes[child];
+        meta(nd, s);
+        int cnt = 0;
+        if (!s.term) {
+            cnt = lx::legal_count<Game>(s);
+            if (cnt == 0 && Game::PASS >= 0 && Game::force_pass(s.phase)) cnt = 1;
+        }
+        nd.stuck = !s.term && cnt == 0;
+        kids[nodes[parent].acts + nodes[parent].nexp] = (short)child;
+        nodes[parent].nexp += 1;
+        if (s.term || cnt == 0 || !do_roll) return s.outcome;
+        s.seed = rkey;
+        s.ncached = 0;
+        const u64 smix = lx::seed_mix(s.seed);
+        while (!s.term && (int)s.mc < rollout_max_turns) {
+            int hint;
+            const int a = lx::sample_action<Game>(s, smix, hint);
+            if (a < 0) break;
+            lx::apply_step<Game>(s, a, hint);
+        }
+        return s.term && !s.trunc ? s.outcome : 0;
+    };
+
+    {   // root
+        St s;
+        lx::load_state<Game>(s, roots, n, t);
+        lx::store_state<Game>(s, pool, pool_rows, base);
+        nnodes = 1;
+        meta(nodes[0], s);
+        build(nodes[0], s);
+        nodes[0].stuck = nodes[0].nacts == 0;
+    }
+    MctsNode& root = nodes[0];
+    int nodes_created = 0;
+    // forced prefix: the first min(budget, branching) root children, rollouts
+    // keyed by the node count after the whole batch is attached
+    int start_it = 0;
+    if (!root.term && !root.stuck) {
+        const int k = budget < root.nacts ? budget : root.nacts;
+        const u64 rk = lx::mix64(k_roll ^ (u64)k);
+        int first = nnodes;
+        for (int j = 0; j < k; j++) {
+            int child;
+            expand(0, acts[root.acts + j], child, rk, false);
+        }
+        nodes_created = k;
+        for (int j = 0; j < k; j++) {             // rollouts + backprop in attach order
+            const int child = first + j;
+            MctsNode& nd = nodes[child];
+            int outcome = nd.outcome;
+            if (!nd.term && !nd.stuck) {
+                St s;
+                lx::load_state<Game>(s, pool, pool_rows, base + child);
+                s.seed = rk;
+                s.ncached = 0;
+                const u64 smix = lx::seed_mix(s.seed);
+                while (!s.term && (int)s.mc < rollout_max_turns) {
+                    int hint;
+                    const int a = lx::sample_action<Game>(s, smix, hint);
+                    if (a < 0) break;
+                    lx::apply_step<Game>(s, a, hint);
+                }
+                outcome = s.term && !s.trunc ? s.outcome : 0;
+            }
+            path[0] = 0; path[1] = child;
+            backprop(2, outcome);
+        }
+        start_it = k;
+    }
+    for (int it = start_it; it < budget && !overflow; it++) {
+        int node = 0, len = 1;
+        path[0] = 0;
+        while (true) {
+            MctsNode& nd = nodes[node];
+            if (nd.term || nd.stuck) { backprop(len, nd.term ? nd.outcome : 0); break; }
+            if (nd.acts < 0) {
+                St s;
+                lx::load_state<Game>(s, pool, pool_rows, base + node);
+                build(nd, s);
+                if (overflow) break;
+                if (nd.nacts == 0 && nd.nexp == 0) { nd.stuck = 1; continue; }
+            }
+            if (nd.nexp < nd.nacts) {
+                if (nnodes >= nmax || len + 1 >= MAXPATH) { overflow = true; break; }
+                nodes_created += 1;
+                int child;
+                const int outcome = expand(node, acts[nd.acts + nd.nexp], child,
+                                           lx::mix64(k_roll ^ (u64)nodes_created), true);
+                path[len++] = child;
+                backprop(len, outcome);
+                break;
+            }
+            // UCB1 over the expanded children; ties -> smallest action
+            const double log_n = logs[nd.N < nlogs ? nd.N : nlogs - 1];
+            int best = -1, best_a = 0;
+            double best_s = 0.0;
+            for (int j = 0; j < nd.nexp; j++) {
+                const MctsNode& ch = nodes[kids[nd.acts + j]];
+                const double sc = ch.W / (double)ch.N + c * sqrt(log_n / (double)ch.N);
+                const int a = acts[nd.acts + j];
+                if (best < 0 || sc > best_s || (sc == best_s && a < best_a)) {
+                    best = kids[nd.acts + j]; best_s = sc; best_a = a;
+                }
+            }
+            if (len >= MAXPATH) { overflow = true; break; }
+            node = best;
+            path[len++] = node;
+        }
+    }
+    if (overflow) { status[t] = 1; actions_out[t] = -1; return; }
+    // best root child: (N, mean value, seeded draw), insertion order, strict >
+    i64 best_a = -1;
+    if (root.nexp == 0) {
+        best_a = root.nacts > 0 ? acts[root.acts] : -1;
+    } else {
+        int bN = -1;
+        double bQ = 0.0, bU = 0.0;
+        for (int j = 0; j < root.nexp; j++) {
+            const MctsNode& ch = nodes[kids[root.acts + j]];
+            const int a = acts[root.acts + j];
+            const double q = ch.W / (double)(ch.N > 1 ? ch.N : 1);
+            const double u = lx::key_uniform(lx::mix64(k_best ^ (u64)(i64)a));
+            const bool better = bN < 0 || ch.N > bN || (ch.N == bN && (q > bQ || (q == bQ && u > bU)));
+            if (better) { bN = ch.N; bQ = q; bU = u; best_a = a; }
+        }
+    }
+    actions_out[t] = best_a;
+}
+#endif
+
+#if LX_IN_GROUP(3)
 extern "C" __global__ void __launch_bounds__(128) lx_expand(u32* pool, i64 cap, const i64* parents,
                                                             const i64* actions,
                                                             const i64* children, i64 n,

@@ -320,6 +320,34 @@ class B200Game:
         return (h[:4 * n].view(np.int32).copy(), h[4 * n:5 * n].view(np.int8).copy(),
                 h[5 * n:nb].reshape(n, A).astype(bool) if masks else None)
 
+    def mcts(self, roots, keys, budgets, exploration, rollout_max_turns):
+        """One MCTS decision per root row on the device (lx_mcts, one thread
+        per tree).  Returns (actions int64, ok bool) host arrays; rows with
+        ok False exceeded a capacity and must be searched on the host."""
+        import math
+        torch = _torch()
+        n = roots.batch_size
+        budgets = np.asarray(budgets, dtype=np.int32)
+        nmax = int(budgets.max()) + 2
+        A = self.codec.size
+        node_bytes = 40                                   # lx::MctsNode
+        arena_bytes = nmax * node_bytes + 4 * (A + 1 + nmax * min(A, 256))
+        arena_bytes = (arena_bytes + 15) // 16 * 16
+        logs = torch.tensor([0.0] + [math.log(k) for k in range(1, nmax + 2)],
+                            dtype=torch.float64, device="cuda")
+        keys_t = _u64_tensor(keys, n)
+        bud_t = torch.as_tensor(budgets).to("cuda")
+        pool = torch.empty((self._nq, n * nmax, 4), dtype=torch.int32, device="cuda")
+        arena = torch.empty(n * arena_bytes, dtype=torch.uint8, device="cuda")
+        acts = torch.empty(n, dtype=torch.int64, device="cuda")
+        status = torch.empty(n, dtype=torch.int32, device="cuda")
+        native.check(native.lib().lx_mcts(
+            self.handle, roots.words.data_ptr(), n, keys_t.data_ptr(), bud_t.data_ptr(),
+            float(exploration), int(rollout_max_turns), logs.data_ptr(), int(logs.numel()),
+            pool.data_ptr(), n * nmax, nmax, arena.data_ptr(), arena_bytes, acts.data_ptr(),
+            status.data_ptr(), self._stream()))
+        return acts.cpu().numpy(), status.cpu().numpy() == 0
+
     def truncate_rows(self, state, rows):
         """Mark rows terminated + truncated with a draw outcome in place (the
         reference's stuck / turn-cap handling, engine.py:156-160,

@@ -41,7 +41,7 @@ class RefState(ctypes.Structure):
 EXPORTS = ("lx_version", "lx_last_error", "lx_game_create", "lx_compile_only", "lx_cache_key",
            "lx_game_info_get", "lx_game_destroy", "lx_init", "lx_legal", "lx_sample",
            "lx_step", "lx_random_step", "lx_rollout", "lx_export", "lx_import", "lx_observe",
-           "lx_env_step", "lx_expand")
+           "lx_env_step", "lx_expand", "lx_mcts")
 
 
 def build_native():
@@ -77,6 +77,8 @@ def lib():
     L.lx_rollout.argtypes = [vp, vp, i64, i32, i32, u64, vp, i64, vp, vp, vp, vp, i32,
                              ctypes.POINTER(i64), vp]
     L.lx_expand.argtypes = [vp, vp, i64, vp, vp, vp, i64, vp, ctypes.c_int, vp, vp, vp, vp]
+    L.lx_mcts.argtypes = [vp, vp, i64, vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.c_int,
+                          vp, i64, ctypes.c_int, vp, i64, vp, vp, vp]
     L.lx_export.argtypes = [vp, vp, i64, ctypes.POINTER(RefState), vp]
     L.lx_import.argtypes = [vp, vp, i64, ctypes.POINTER(RefState), vp]
     L.lx_observe.argtypes = [vp, vp, i64, i32, vp, vp]

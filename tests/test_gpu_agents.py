@@ -111,3 +111,20 @@ def test_gavel_on_generated_programs(prog):
     rep = evaluation.evaluate_game(prog["text"], evaluation.EvalConfig(**GAVEL["config"]))
     got = {k: (float.hex(v) if isinstance(v, float) else v) for k, v in rep.as_dict().items()}
     assert got == prog["report"]
+
+
+@pytest.mark.parametrize("name", ["connect_four", "reversi", "english_draughts", "hex"])
+def test_device_search_equals_host_search(name):
+    """lx_mcts (one thread per tree) and the host tree search make the same
+    decisions on a batch of mid-game positions."""
+    g = game(name)
+    st = g.init(12, seed=41)
+    for _ in range(6):
+        g.step_into(st, lx.engine.random_actions(g, st), rows=~st.terminated, verify=False)
+    rows = ~st.terminated
+    budgets = np.full(12, 24, dtype=np.int64)
+    salt = np.full(12, np.uint64(9), dtype=np.uint64)
+    search = agents._Search(g, 1.4142135623730951, 60)
+    dev = search.run(st, rows, budgets, salt, device=True)
+    host = search.run(st, rows, budgets, salt, device=False)
+    assert np.array_equal(dev, host)
