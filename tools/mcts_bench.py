@@ -3,7 +3,7 @@ path vs the unmodified reference (baseline/_ref) on the same seeds, plus a
 check that both produce identical MatchStats.
 
     python tools/mcts_bench.py [--game connect_four] [--games 16] [--strong 100]
-                               [--weak 50] [--no-reference]
+                               [--weak 50] [--no-reference] [--gavel --matches 100]
 
 Prints one JSON line: wall seconds and MCTS iterations/s of each side.
 """
@@ -23,6 +23,9 @@ p.add_argument("--strong", type=int, default=100)
 p.add_argument("--weak", type=int, default=50)
 p.add_argument("--seed", type=int, default=0)
 p.add_argument("--no-reference", action="store_true")
+p.add_argument("--gavel", action="store_true",
+               help="time evaluation.evaluate_game (GAVEL report) instead of one match")
+p.add_argument("--matches", type=int, default=100)
 a = p.parse_args()
 
 text = open(os.path.join(ROOT, "paper_2506_22609_b200", "games", f"{a.game}.ldx")).read()
@@ -41,6 +44,28 @@ def iterations(st):
 import torch  # noqa: E402
 import paper_2506_22609_b200 as lx  # noqa: E402
 from paper_2506_22609_b200 import agents  # noqa: E402
+
+if a.gavel:
+    from paper_2506_22609_b200 import evaluation  # noqa: E402
+    cfg = dict(matches=a.matches, strong_iterations=a.strong, weak_iterations=a.weak, seed=a.seed)
+    lx.load_game(text).native                          # CUDA context + NVRTC cache warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = evaluation.evaluate_game(text, evaluation.EvalConfig(**cfg)).as_dict()
+    t_mine = time.perf_counter() - t0
+    out = {"game": a.game, "gavel": cfg, "b200": {"seconds": t_mine}, "report": rep}
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not a.no_reference and os.path.isdir(os.path.join(ref_dir, "boardlang")):
+        sys.path.insert(0, ref_dir)
+        from boardlang import evaluation as revaluation  # noqa: E402
+        t0 = time.perf_counter()
+        rrep = revaluation.evaluate_game(text, revaluation.EvalConfig(**cfg)).as_dict()
+        t_ref = time.perf_counter() - t0
+        out["reference"] = {"seconds": t_ref, "cores": 1}
+        out["identical_report"] = rrep == rep
+        out["speedup"] = t_ref / t_mine
+    print(json.dumps(out))
+    sys.exit(0)
 
 g = lx.load_game(text)
 strong = agents.MctsPolicy(agents.MctsConfig(iterations=a.strong, seed=a.seed * 2 + 1))
