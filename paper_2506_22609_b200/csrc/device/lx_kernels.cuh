@@ -144,7 +144,7 @@ __device__ __forceinline__ void write_mask_moves(unsigned char* __restrict__ mas
 // The native runtime compiles the kernels in groups, one NVRTC program per
 // group in parallel (LX_GROUP = group id; unset: every kernel):
 //   0 init / rollout / export / import   1 legal / sample / observe
-//   2 verify / step / random_step        3 expand (MCTS)   4 env_step
+//   2 verify / step / random_step        3 expand (MCTS)   4 env_step   5 mcts
 #ifndef LX_GROUP
 #define LX_GROUP -1
 #endif
@@ -474,7 +474,7 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
 // when it is live and has a legal action, the outcome of one uniform-random
 // rollout from it drawing with seeds[i] (0 draw / stuck / cap, 1 P1, 2 P2)
 // in rolled[i] (else -1).
-#if LX_IN_GROUP(3)
+#if LX_IN_GROUP(5)
 namespace lx {
 
 // ---- device MCTS (one thread per search tree) --------------------------------
@@ -493,7 +493,7 @@ struct MctsNode {
 };
 
 template <class G>
-__device__ __forceinline__ int mcts_legal(const typename G::St& s, short* out) {
+__device__ __forceinline__ int mcts_legal(const typename G::St& s, int* out) {
     int n = 0;
     if (s.term) return 0;
     if constexpr (G::MECH == 0) {
@@ -501,13 +501,30 @@ __device__ __forceinline__ int mcts_legal(const typename G::St& s, short* out) {
 #pragma unroll
         for (int w = 0; w < G::W; w++) {
             u32 b = legal.w[w];
-            while (b) { const int x = 32 * w + __ffs(b) - 1; b &= b - 1u; out[n++] = (short)G::bit_cell(x); }
+            while (b) { const int x = 32 * w + __ffs(b) - 1; b &= b - 1u; out[n++] = G::bit_cell(x); }
         }
     } else {
-        G::enum_moves(s, [&](int a) { out[n++] = (short)a; });
+        G::enum_moves(s, [&](int a) { out[n++] = a; });
     }
-    if (n == 0 && G::PASS >= 0 && G::force_pass(s.phase)) out[n++] = (short)G::PASS;
+    if (n == 0 && G::PASS >= 0 && G::force_pass(s.phase)) out[n++] = G::PASS;
     return n;
+}
+
+// one uniform-random rollout from s drawing with `seed` (agents._rollout):
+// 0 draw / cap / stuck, 1 P1, 2 P2.  Out of line: the MCTS kernel calls it
+// from two places and inlining the rules twice doubles its compile time.
+template <class G>
+__device__ __noinline__ int mcts_playout(typename G::St& s, u64 seed, int max_turns) {
+    s.seed = seed;
+    s.ncached = 0;
+    const u64 smix = seed_mix(seed);
+    while (!s.term && (int)s.mc < max_turns) {
+        int hint;
+        const int a = sample_action<G>(s, smix, hint);
+        if (a < 0) break;                          // stuck: scored as a draw
+        apply_step<G>(s, a, hint);
+    }
+    return s.term && !s.trunc ? s.outcome : 0;
 }
 
 }  // namespace lx
@@ -523,9 +540,9 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
     typedef Game::St St;
     constexpr int MAXPATH = 256;
     MctsNode* nodes = reinterpret_cast<MctsNode*>(arena + t * arena_bytes);
-    short* acts = reinterpret_cast<short*>(nodes + nmax);
-    const i64 acap = (arena_bytes - (i64)nmax * (i64)sizeof(MctsNode)) / 4;   // shorts: acts + kids
-    short* kids = acts + acap;
+    int* acts = reinterpret_cast<int*>(nodes + nmax);
+    const i64 acap = (arena_bytes - (i64)nmax * (i64)sizeof(MctsNode)) / 8;   // ints: acts + kids
+    int* kids = acts + acap;
     i64 aused = 0;
     status[t] = 0;
     const u64 key = keys[t];
@@ -543,11 +560,11 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
     };
     // untried order: legal actions sorted by hash_key(key, 0xA11, a), ties by a
     auto build = [&](MctsNode& nd, const St& s) {
-        short* out = acts + aused;
+        int* out = acts + aused;
         if (aused + Game::A + 1 > acap) { overflow = true; nd.acts = (int)aused; nd.nacts = 0; return; }
         int m = lx::mcts_legal<Game>(s, out);
         for (int i = 1; i < m; i++) {                    // insertion sort by (hash, action)
-            const short a = out[i];
+            const int a = out[i];
             const u64 h = lx::mix64(k_order ^ (u64)(i64)a);
             int j = i - 1;
             while (j >= 0) {
@@ -592,19 +609,10 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
             if (cnt == 0 && Game::PASS >= 0 && Game::force_pass(s.phase)) cnt = 1;
         }
         nd.stuck = !s.term && cnt == 0;
-        kids[nodes[parent].acts + nodes[parent].nexp] = (short)child;
+        kids[nodes[parent].acts + nodes[parent].nexp] = child;
         nodes[parent].nexp += 1;
         if (s.term || cnt == 0 || !do_roll) return s.outcome;
-        s.seed = rkey;
-        s.ncached = 0;
-        const u64 smix = lx::seed_mix(s.seed);
-        while (!s.term && (int)s.mc < rollout_max_turns) {
-            int hint;
-            const int a = lx::sample_action<Game>(s, smix, hint);
-            if (a < 0) break;
-            lx::apply_step<Game>(s, a, hint);
-        }
-        return s.term && !s.trunc ? s.outcome : 0;
+        return lx::mcts_playout<Game>(s, rkey, rollout_max_turns);
     };
 
     {   // root
@@ -637,16 +645,7 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
             if (!nd.term && !nd.stuck) {
                 St s;
                 lx::load_state<Game>(s, pool, pool_rows, base + child);
-                s.seed = rk;
-                s.ncached = 0;
-                const u64 smix = lx::seed_mix(s.seed);
-                while (!s.term && (int)s.mc < rollout_max_turns) {
-                    int hint;
-                    const int a = lx::sample_action<Game>(s, smix, hint);
-                    if (a < 0) break;
-                    lx::apply_step<Game>(s, a, hint);
-                }
-                outcome = s.term && !s.trunc ? s.outcome : 0;
+                outcome = lx::mcts_playout<Game>(s, rk, rollout_max_turns);
             }
             path[0] = 0; path[1] = child;
             backprop(2, outcome);

@@ -331,7 +331,7 @@ class B200Game:
         nmax = int(budgets.max()) + 2
         A = self.codec.size
         node_bytes = 40                                   # lx::MctsNode
-        arena_bytes = nmax * node_bytes + 4 * (A + 1 + nmax * min(A, 256))
+        arena_bytes = nmax * node_bytes + 8 * (A + 1 + nmax * min(A, 256))
         arena_bytes = (arena_bytes + 15) // 16 * 16
         logs = torch.tensor([0.0] + [math.log(k) for k in range(1, nmax + 2)],
                             dtype=torch.float64, device="cuda")

@@ -128,3 +128,25 @@ def test_device_search_equals_host_search(name):
     dev = search.run(st, rows, budgets, salt, device=True)
     host = search.run(st, rows, budgets, salt, device=False)
     assert np.array_equal(dev, host)
+
+
+def test_device_search_on_generated_programs():
+    """Device and host MCTS agree on programs from the reference's generator
+    (movement, mixed phases, passes, transient masks ...)."""
+    with open(os.path.join(GOLDEN, "fuzz.json")) as f:
+        progs = json.load(f)["programs"][::57][:4]
+    for prog in progs:
+        g = lx.load_game(prog["text"])
+        st = g.init(6, seed=5)
+        for _ in range(3):
+            live = ~st.terminated
+            a = lx.engine.random_actions(g, st)
+            if (a[live] < 0).any():
+                break
+            g.step_into(st, a, rows=live, verify=False)
+        rows = ~st.terminated
+        budgets = np.full(6, 12, dtype=np.int64)
+        salt = np.full(6, np.uint64(3), dtype=np.uint64)
+        search = agents._Search(g, 1.4142135623730951, 30)
+        assert np.array_equal(search.run(st, rows, budgets, salt, device=True),
+                              search.run(st, rows, budgets, salt, device=False)), prog["index"]

@@ -28,7 +28,7 @@ def test_every_header_symbol_is_exported():
 def test_nvrtc_compiles_config_games_for_sm100a():
     keys = precompile(prune=False)
     for k in keys.values():
-        for g in range(5):                     # one cubin per kernel group
+        for g in range(6):                     # one cubin per kernel group
             path = os.path.join(native.CACHE_DIR, f"{k}-g{g}.cubin")
             with open(path, "rb") as f:
                 head = f.read(64)
