@@ -7,6 +7,7 @@ python bench.py --game english_draughts --steps 20 > gpurun_out/bench_draughts.j
 python bench.py --steps 3 --warmup 1 --no-extras > gpurun_out/b_plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 1 --no-extras > gpurun_out/ncu_launch.log 2>&1; echo "launches rc=$?"
 NO_LAUNCHES=1 GAMES="connect_four:1048576 tic_tac_toe:1048576 hex:131072 reversi:262144 pente:65536 gomoku:65536 yavalath:262144 english_draughts:262144 dai_hasami_shogi:131072 wolf_and_sheep:262144 gridworld:1048576" bash tools/profile_all.sh
 python tools/mcts_bench.py --game connect_four --games 16 > gpurun_out/mcts_c4.json 2>&1
+python tools/mcts_bench.py --gavel --game connect_four --matches 24 > gpurun_out/gavel_c4.json 2>&1
 python tools/mcts_bench.py --game reversi --games 8 --strong 50 --weak 25 > gpurun_out/mcts_rev.json 2>&1
 python tools/mcts_bench.py --game tic_tac_toe --games 32 > gpurun_out/mcts_ttt.json 2>&1
 cat gpurun_out/mcts_*.json
