@@ -233,11 +233,13 @@ struct Mirror {
         __shared__ u32 buf[2 * W * LX_MIRROR_STRIDE];
         return buf + threadIdx.x;
     }
-    // one player's plane only (readers of that plane need nothing else)
-    static __device__ __forceinline__ void store_plane(int player, const BB<W>& p) {
-        u32* m = slot();
+    // one player's plane only (readers of that plane need nothing else);
+    // word-wise select, no board copy (a selected BB<W> spills on big boards)
+    static __device__ __forceinline__ void store_plane(int player, const BB<W>& p0,
+                                                       const BB<W>& p1) {
+        u32* m = slot() + player * W * LX_MIRROR_STRIDE;
 #pragma unroll
-        for (int i = 0; i < W; i++) m[(player * W + i) * LX_MIRROR_STRIDE] = p.w[i];
+        for (int i = 0; i < W; i++) m[i * LX_MIRROR_STRIDE] = player ? p1.w[i] : p0.w[i];
     }
     static __device__ __forceinline__ void store(const BB<W>& p0, const BB<W>& p1) {
         u32* m = slot();

@@ -583,7 +583,7 @@ class GameLowering(MoveLoweringMixin):
         const int side = {side};
         if (!(s.last_dest >= 0 && s.last_mover == mover)) return false;
         const int c = cell_bit(s.last_dest);
-        M::store_plane(side, side ? s.own1 : s.own0);   // only the player's stones are probed
+        M::store_plane(side, s.own0, s.own1);   // only the player's stones are probed
         if (!M::probe(side, c)) return false;
         const int r = c / {self.emb_cols};
         const int col = c - r * {self.emb_cols};
