@@ -167,7 +167,7 @@ struct LxRefPtrs {               // reference GameState field pointers (state.py
     short* last_source;          // (B,) int16
     short* last_dest;            // (B,) int16
     short* last_dest_by_player;  // (B, 2) int16
-    short* comp_labels;          // (B, 1, C) int16     or null
+    short* comp_labels;          // (B, P, C) int16     or null (P connectivity plans)
     signed char* phase;          // (B,) int8           or null
     short* must_move;            // (B,) int16          or null
     signed char* turn_pos;       // (B,) int8           or null
@@ -856,7 +856,7 @@ extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B
         p.last_dest_by_player[2 * i] = (short)s.ldbp0;
         p.last_dest_by_player[2 * i + 1] = (short)s.ldbp1;
     }
-    if (p.comp_labels) Game::labels(s, p.comp_labels + i * Game::C);
+    if (p.comp_labels) Game::labels(s, p.comp_labels + i * Game::CONN_PLANS * Game::C);
     if (p.phase) p.phase[i] = (signed char)s.phase;
     if (p.must_move) p.must_move[i] = (short)s.must_move;
     if (p.turn_pos) p.turn_pos[i] = (signed char)s.pos;

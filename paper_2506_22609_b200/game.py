@@ -543,7 +543,7 @@ class B200Game:
             for k in ("hopped_mask", "captured_mask", "promoted_mask"):
                 f[k] = ((B, C), torch.bool)
         if L.connectivity:
-            f["comp_labels"] = ((B, 1, C), torch.int16)
+            f["comp_labels"] = ((B, L.connectivity, C), torch.int16)
         if L.phase:
             f["phase"] = ((B,), torch.int8)
         if L.turn_pos:

@@ -221,8 +221,6 @@ class GameLowering(MoveLoweringMixin):
                        "phase": self.phase_mult, "turn_pos": self.turn_pos}
         self._anchor_candidates = cands
         self._last_action_base = last_action
-        if len(self.conn_plans) > 1:
-            _fail("more than one connectivity direction plan is not lowered yet")
         # action codec (reference codec.py:58-69)
         base = {0: self.C, 1: self.C * self.C}.get(self.mech_kind)
         if base is None:
@@ -940,12 +938,16 @@ class GameLowering(MoveLoweringMixin):
         stones = self.piece_filter(node.piece, self.stones(self.side(node.player)))
         L = node.length
         name = f"line_anchor_{self.em.fresh('a')}"
+        extra = ""
         if node.exclude is not None:
-            # a window through the anchor avoiding excluded cells <=> a run of
-            # >= L owned non-excluded cells through the anchor
+            ex = self.em.const(self._line_excluded(node))
             if node.exact:
-                _fail("exact anchored line with exclude: is not lowered yet")
-            stones = f"lx::andnot({stones}, {self.em.const(self._line_excluded(node))})"
+                # the window is the maximal run itself: exactly L cells, none excluded
+                extra = f" && !lx::any((e | a) & {ex})"
+            else:
+                # a window avoiding excluded cells <=> a run of >= L owned
+                # non-excluded cells through the anchor
+                stones = f"lx::andnot({stones}, {ex})"
         lines = []
         # exact lines need the maximal run through the anchor to be exactly L:
         # grow L steps each way and compare (reference exprs.py:525-533)
@@ -956,7 +958,7 @@ class GameLowering(MoveLoweringMixin):
             lines.append("            BBW e = a;")
             for _ in range(steps):
                 lines.append(f"            e = (e | {self.nb(d, 'e')} | {self.nb(OPPOSITE[d], 'e')}) & b;")
-            lines.append(f"            hit = hit || lx::popc(e | a) {test};")
+            lines.append(f"            hit = hit || (lx::popc(e | a) {test}{extra});")
             lines.append("        }")
         body = "\n".join(lines)
         self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const St& s, int mover, const BBW& b) {{
@@ -1439,18 +1441,18 @@ class GameLowering(MoveLoweringMixin):
                 cond = f"pos == {key}" if self.turn_pos else f"mover == {key}"
                 adv.append(f"        if (phase == {pi} && {cond}) {{ np = {nplayer}; "
                            f"nphase = {nphase}; npos = {npos}; return; }}")
-        conn = ""
-        if self.conn_plans:
-            plan = self.conn_plans[0]
+        conn = []
+        for pi_, plan in enumerate(self.conn_plans):   # comp_labels[:, plan, :]
             dil = " | ".join(self.nb(d, "f") for d in plan)
-            conn = f"""        const BBW occ[2] = {{s.own0, s.own1}};
+            conn.append(f"""        {{
+        short* lab = out + {pi_} * C;
         BBW done = lx::bb_zero<W>();
         for (int c = 0; c < C; c++) {{                    // ascending cell id = min label
             const int cb = cell_bit(c);
             const bool o0 = lx::test(s.own0, cb), o1 = lx::test(s.own1, cb);
-            if (!o0 && !o1) {{ out[c] = -1; continue; }}
+            if (!o0 && !o1) {{ lab[c] = -1; continue; }}
             if (lx::test(done, cb)) continue;
-            const BBW mine = o0 ? occ[0] : occ[1];
+            const BBW mine = lx::sel(o1, s.own0, s.own1);
             BBW f = lx::onehot<W>(cb);
             while (true) {{
                 const BBW g = (f | {dil}) & mine;
@@ -1463,11 +1465,13 @@ class GameLowering(MoveLoweringMixin):
                 u32 bits = f.w[i];
                 while (bits) {{
                     const int b = __ffs(bits) - 1;
-                    out[bit_cell(32 * i + b)] = (short)c;
+                    lab[bit_cell(32 * i + b)] = (short)c;
                     bits &= bits - 1u;
                 }}
             }}
-        }}"""
+        }}
+        }}""")
+        conn = "\n".join(conn)
         fp = " || ".join(f"phase == {p}" for p in fp_cases) or "false"
         conn_update = self._conn_update_code()
         conn_rebuild = self._conn_rebuild_code()
@@ -1526,6 +1530,7 @@ struct Game {{
     static constexpr int NB = {self.NB};                       // bit slots (embedded grid)
     typedef lx::BB<W> BBW;
     static constexpr int NGC = {self.ngc};                     // cached move-group totals
+    static constexpr int CONN_PLANS = {max(len(self.conn_plans), 1)};           // comp_labels planes
     typedef lx::State<W, NX, NGC> St;
 {self._bitmap_code()}
 @@CONSTS@@

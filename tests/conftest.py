@@ -73,7 +73,7 @@ def ref_allocator(info):
             s["last_dest"] = np.full(B, -1, np.int16)
             s["last_dest_by_player"] = np.full((B, 2), -1, np.int16)
         if L["connectivity"]:
-            s["comp_labels"] = np.full((B, 1, C), -1, np.int16)
+            s["comp_labels"] = np.full((B, L["connectivity"], C), -1, np.int16)
         if L["transient_masks"]:
             for k in ("hopped_mask", "captured_mask", "promoted_mask"):
                 s[k] = np.zeros((B, C), bool)

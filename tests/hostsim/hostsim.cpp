@@ -56,7 +56,7 @@ static void export_one(const St& s, int64_t i, const RefOut* p) {
         p->last_dest_by_player[2 * i] = (int16_t)s.ldbp0;
         p->last_dest_by_player[2 * i + 1] = (int16_t)s.ldbp1;
     }
-    if (p->comp_labels) Game::labels(s, (short*)(p->comp_labels + i * Game::C));
+    if (p->comp_labels) Game::labels(s, (short*)(p->comp_labels + i * Game::CONN_PLANS * Game::C));
     if (p->phase) p->phase[i] = (int8_t)s.phase;
     if (p->must_move) p->must_move[i] = (int16_t)s.must_move;
     if (p->turn_pos) p->turn_pos[i] = (int8_t)s.pos;

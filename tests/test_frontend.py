@@ -122,11 +122,14 @@ def test_lowering_words_bit_order():
         (end (if (connected "s" ((edge top) (edge bottom)) direction:orthogonal) (mover win))
              (if (connected "s" ((edge left) (edge right))) (mover win)))))""",
      "two connectivity plans"),
+    ("""(game "Tri" (players 2) (equipment (board (square 5)) (pieces ("s" both)))
+        (rules (play (repeat (P1 P2) (place "s" (destination (empty)))))
+        (end (if (connected "s" ((edge top) (edge bottom) (edge left))) (mover win)))))""",
+     "three-target connected"),
 ])
-def test_unsupported_raises_compile_error(text, what):
-    with pytest.raises(CompileError) as e:
-        lowering.lower_game(syntax.parse_game(text))
-    assert e.value.stage == "lower"
+def test_formerly_unsupported_constructs_lower(text, what):
+    low = lowering.lower_game(syntax.parse_game(text))
+    assert "struct Game" in low.source, what
 
 
 def test_reference_unsupported_constructs_raise_like_the_reference():

@@ -1,8 +1,9 @@
 #!/bin/bash
-# Run on the GPU box (gpurun): plain run then ncu --set full of lx_rollout for
+# Run on the GPU box (gpurun): plain run then ncu --set full of lx_rollout (at the
+# bench batch, 2^22 envs, so per-env-step counts match the bench workload) for
 # each config game, SASS source pages exported, plus the bench launch list.
 mkdir -p gpurun_out
-for gb in ${GAMES:-connect_four:1048576 tic_tac_toe:1048576 hex:131072 reversi:262144 pente:65536}; do
+for gb in ${GAMES:-connect_four:4194304 tic_tac_toe:4194304 hex:4194304 reversi:4194304 pente:4194304}; do
   g=${gb%%:*}; b=${gb##*:}
   timeout 300 python tools/ncu_rollout.py --game $g --batch $b > gpurun_out/plain_$g.json 2>&1 &&
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:lx_rollout -s 1 -c 1 \
