@@ -117,6 +117,18 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU arm
+def cpu_model():
+    """Host CPU model name (BASELINE.md section 2 asks for it beside core counts)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_rate(game, batch_total, seconds, threads, max_turns):
     """Oracle port (plain C, all host threads) on a bounded sample of the same
     workload: the first envs of episode 10000, repeated until ~seconds."""
@@ -160,6 +172,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": config(args, ws),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "cpu_model": cpu_model(),
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -488,6 +501,7 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
     threads = os.cpu_count() or 1
     r, steps, dt, n = cpu_rate(args.game, B_total, args.cpu_seconds, threads, args.max_turns)
     out["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": threads, "kind": "port",
+                           "cpu_model": cpu_model(),
                            "sample": f"{steps} env steps, first {n} envs of episode 10000, "
                                      f"{dt:.1f}s on {threads} threads"}
     return out
