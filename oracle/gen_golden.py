@@ -334,6 +334,39 @@ def gavel_fixtures(n_valid=10, n_invalid=4):
         json.dump({"config": cfg, "programs": out}, fh, indent=0, sort_keys=True)
 
 
+def fuzz_mask_fixtures(stride=10):
+    """Per-ply legal-mask hashes and sampled actions of B=4 trajectories
+    (seed 3, 60-ply cap) for every `stride`-th fuzz program: exercises the
+    mask writers and verified steps, not just final states."""
+    import hashlib
+    from boardlang import rng as rrng
+    with open(os.path.join(OUT, "fuzz.json")) as fh:
+        progs = json.load(fh)["programs"][::stride]
+    out = []
+    for prog in progs:
+        g = boardlang.load_game(prog["text"])
+        st = g.init(batch_size=4, seed=3)
+        rows = [[] for _ in range(4)]
+        for _ in range(60):
+            if st.terminated.all():
+                break
+            m = g.legal_mask(st)
+            u = rrng.uniform(st.seeds, st.move_count.astype(np.uint64))
+            a = g.sample_actions(st, u)
+            live = ~st.terminated
+            if (a[live] < 0).any():
+                break
+            for i in np.nonzero(live)[0]:
+                h = hashlib.blake2b(np.packbits(m[i]).tobytes(), digest_size=8).hexdigest()
+                rows[i].append([h, int(a[i])])
+            g.step_into(st, a, rows=live, verify=True)
+        out.append({"sampler": prog.get("sampler"), "index": prog["index"], "rows": rows,
+                    "digest": st.digest()})
+    with open(os.path.join(OUT, "fuzz_masks.json"), "w") as fh:
+        json.dump({"stride": stride, "programs": out}, fh, indent=0, sort_keys=True)
+    print("wrote fuzz_masks.json", len(out))
+
+
 def validate_fixtures(per_corpus=150):
     """Validation reports of generated programs, valid or not (validate.py,
     raised as ValidationFailure by load_game)."""
@@ -356,6 +389,9 @@ def validate_fixtures(per_corpus=150):
 
 
 if __name__ == "__main__":
+    if "--fuzz-masks" in sys.argv:
+        fuzz_mask_fixtures()
+        sys.exit(0)
     if "--gavel" in sys.argv:
         gavel_fixtures()
         sys.exit(0)

@@ -68,3 +68,55 @@ def test_fuzz_device_matches_reference():
             assert int(np.asarray(po.turns_taken).sum()) == run["turns"], prog["index"]
         checked += 1
     assert checked == len(PROGRAMS[::every])
+
+
+with open(os.path.join(GOLDEN, "fuzz_masks.json")) as f:
+    MASKS = json.load(f)
+_TEXT = {(tuple(p.get("sampler") or [7, 5]), p["index"]): p["text"] for p in PROGRAMS}
+
+
+def _mask_hash(row):
+    import hashlib
+    return hashlib.blake2b(np.packbits(np.asarray(row, dtype=bool)).tobytes(),
+                           digest_size=8).hexdigest()
+
+
+@pytest.mark.parametrize("rec", MASKS["programs"][::3],
+                         ids=lambda r: f"s{(r.get('sampler') or [7])[0]}-{r['index']}")
+def test_fuzz_hostsim_masks_match_reference(rec):
+    """Per-ply legal masks and sampled actions (reference fuzz_masks.json)."""
+    from hostsim.hostsim import HostGame
+    text = _TEXT[(tuple(rec.get("sampler") or [7, 5]), rec["index"])]
+    hg = HostGame(lowering.lower_game(syntax.parse_game(text)))
+    seeds = rng.spawn_seeds(3, 4)
+    for i in range(4):
+        want = rec["rows"][i]
+        m, a = hg.masks(int(seeds[i]), max_plies=60)
+        assert len(a) >= len(want)
+        for t, (h, act) in enumerate(want):
+            assert _mask_hash(m[t]) == h, (i, t)
+            assert int(a[t]) == act, (i, t)
+
+
+@pytest.mark.gpu
+def test_fuzz_device_masks_match_reference():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_22609_b200 as lx
+    every = 1 if os.environ.get("LX_FUZZ_ALL") else 6
+    for rec in MASKS["programs"][::every]:
+        g = lx.load_game(_TEXT[(tuple(rec.get("sampler") or [7, 5]), rec["index"])])
+        st = g.init(4, seed=3)
+        t = 0
+        while t < 60 and not st.terminated.all():
+            m = g.legal_mask(st)
+            a = lx.engine.random_actions(g, st)
+            live = ~st.terminated
+            if (a[live] < 0).any():
+                break
+            for i in np.nonzero(live)[0]:
+                assert [_mask_hash(m[i]), int(a[i])] == rec["rows"][i][t], (rec["index"], i, t)
+            g.step_into(st, a, rows=live, verify=True)
+            t += 1
+        assert st.digest() == rec["digest"], rec["index"]

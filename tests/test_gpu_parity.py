@@ -224,3 +224,35 @@ def test_ttt_outcome_counts(golden_meta):
     want = golden_meta["kat"]["ttt_10000_seed11"]
     f = lx.engine.playout_random(game("tic_tac_toe"), seed=11, batch_size=10_000).final
     assert f.digest() == want["digest"]
+
+
+def test_ttt_exhaustive_census():
+    """Every tic-tac-toe game by breadth-first expansion on the device
+    (reference test_acceptance.py:84-111): the published census 255168 games,
+    131184 P1 wins, 77904 P2 wins, 46080 draws."""
+    g = game("tic_tac_toe")
+    st = g.init(1, seed=0)
+    totals = np.zeros(4, dtype=np.int64)
+    while st.batch_size:
+        mask = g.legal_mask(st)
+        counts = mask.sum(axis=1)
+        rows, acts = np.nonzero(mask)
+        st = st.rows(rows)
+        g.step_into(st, acts.astype(np.int64), verify=False)
+        m = g.meta(st)
+        done = m["terminated"]
+        totals += [done.sum(), (m["outcome"][done] == 1).sum(), (m["outcome"][done] == 2).sum(),
+                   (m["outcome"][done] == 0).sum()]
+        st = st.rows(np.nonzero(~done)[0]) if (~done).any() else st.rows([])
+    assert tuple(int(x) for x in totals) == (255168, 131184, 77904, 46080)
+
+
+def test_connect_four_opening_chi_square():
+    """1e5 uniform openings (reference test_agents.py:28-41)."""
+    g = game("connect_four")
+    n = 100_000
+    a = lx.engine.random_actions(g, g.init(n, seed=77))
+    vals, cnt = np.unique(a, return_counts=True)
+    assert vals.tolist() == list(range(35, 42))
+    exp = n / 7
+    assert float(((cnt - exp) ** 2 / exp).sum()) < 22.46
