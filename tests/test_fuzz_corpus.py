@@ -47,6 +47,18 @@ def test_fuzz_hostsim_matches_reference(prog):
         assert steps == run["turns"]
 
 
+def _fuzz_part(default_stride):
+    """LX_FUZZ_ALL=1: the whole corpus; LX_FUZZ_ALL=k/n: programs k, k+n, ...
+    (the corpus in n GPU calls); else a stride sample."""
+    spec = os.environ.get("LX_FUZZ_ALL")
+    if not spec:
+        return PROGRAMS[::default_stride]
+    if "/" in spec:
+        k, n = (int(x) for x in spec.split("/"))
+        return PROGRAMS[k::n]
+    return PROGRAMS
+
+
 @pytest.mark.gpu
 def test_fuzz_device_matches_reference():
     """A stride-30 sample (NVRTC compiles each program in ~7 s; the whole
@@ -55,9 +67,9 @@ def test_fuzz_device_matches_reference():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2506_22609_b200 as lx
-    every = 1 if os.environ.get("LX_FUZZ_ALL") else 30
+    part = _fuzz_part(30)
     checked = 0
-    for prog in PROGRAMS[::every]:
+    for prog in part:
         if lowered(prog) is None:
             continue
         g = lx.load_game(prog["text"])
@@ -67,7 +79,7 @@ def test_fuzz_device_matches_reference():
             assert po.final.digest() == run["digest"], prog["index"]
             assert int(np.asarray(po.turns_taken).sum()) == run["turns"], prog["index"]
         checked += 1
-    assert checked == len(PROGRAMS[::every])
+    assert checked == len(part)
 
 
 with open(os.path.join(GOLDEN, "fuzz_masks.json")) as f:
