@@ -234,12 +234,20 @@ struct Mirror {
         return buf + threadIdx.x;
     }
     // one player's plane only (readers of that plane need nothing else);
-    // word-wise select, no board copy (a selected BB<W> spills on big boards)
+    // big boards select word by word (a selected BB<W> copy spills); small
+    // boards select the board (C4: 7% faster than the word-wise form)
     static __device__ __forceinline__ void store_plane(int player, const BB<W>& p0,
                                                        const BB<W>& p1) {
-        u32* m = slot() + player * W * LX_MIRROR_STRIDE;
+        if constexpr (W <= 2) {
+            const BB<W> p = player ? p1 : p0;
+            u32* m = slot();
 #pragma unroll
-        for (int i = 0; i < W; i++) m[i * LX_MIRROR_STRIDE] = player ? p1.w[i] : p0.w[i];
+            for (int i = 0; i < W; i++) m[(player * W + i) * LX_MIRROR_STRIDE] = p.w[i];
+        } else {
+            u32* m = slot() + player * W * LX_MIRROR_STRIDE;
+#pragma unroll
+            for (int i = 0; i < W; i++) m[i * LX_MIRROR_STRIDE] = player ? p1.w[i] : p0.w[i];
+        }
     }
     static __device__ __forceinline__ void store(const BB<W>& p0, const BB<W>& p1) {
         u32* m = slot();
