@@ -366,7 +366,7 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
     # double-buffered over three streams (H2D, compute, D2H), so step i+1's
     # upload and step i's download overlap step i's / i+1's rollout; all the
     # copies stay inside the timed region.
-    K = max(3, min(args.steps, 10))
+    K = max(3, min(args.steps, 30))          # 30 steps: pipeline fill/drain < 3 %
     WU = 2
     n_it = K + WU
     seeds_h = [torch.from_numpy(rng.spawn_seeds(rng.episode_seed(0, B_total, 20000 + e), B)
@@ -441,6 +441,8 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
         rl.update({"achieved": ach / 1e9, "frac": ach / peak_alu,
                    "traffic": prof["dram_bytes_per_launch"] / prof["env_steps_in_launch"],
                    "traffic_unit": "DRAM bytes per env step (ncu)",
+                   "traffic_bytes_per_launch": prof["dram_bytes_per_launch"],
+                   "traffic_profile_batch": prof.get("batch"),
                    "issue": {"achieved": iss / 1e9, "peak": peak_issue / 1e9,
                              "frac": iss / peak_issue},
                    "ncu_alu_pipe_pct": prof.get("alu_pipe_elapsed_pct"),
