@@ -257,6 +257,19 @@ struct Mirror {
             m[(W + i) * LX_MIRROR_STRIDE] = p1.w[i];
         }
     }
+    // remove `cell` from `player`'s mirrored plane (a probed capture collects
+    // its cells here with LDS/LOP/STS per cell instead of a W-way register
+    // select per cell; the caller diffs the plane against its registers)
+    static __device__ __forceinline__ void clear(int player, int cell) {
+        slot()[(player * W + (cell >> 5)) * LX_MIRROR_STRIDE] &= ~(1u << (cell & 31));
+    }
+    static __device__ __forceinline__ BB<W> load(int player) {
+        const u32* m = slot() + player * W * LX_MIRROR_STRIDE;
+        BB<W> r;
+#pragma unroll
+        for (int i = 0; i < W; i++) r.w[i] = m[i * LX_MIRROR_STRIDE];
+        return r;
+    }
     // is `cell` occupied by `player` (0/1)?
     static __device__ __forceinline__ bool probe(int player, int cell) {
         const u32 w = slot()[(player * W + (cell >> 5)) * LX_MIRROR_STRIDE];
@@ -329,5 +342,129 @@ struct State {
     int ntot[NGC];
     u64 seed;
 };
+
+#if defined(__CUDA_ARCH__)
+// ---------------------------------------------------------------------------
+// Warp-cooperative flood (connectivity reach sets, reference connectivity.py
+// place_update).  A sequential flood costs the warp the LONGEST flood of its
+// lanes (~5.5 dilations per ply on Hex 11x11, ~54 instructions each, while
+// the mean lane needs 0.4).  Here one flood is spread over a group of G lanes,
+// lane i of the group holding word i of the bitboard: a dilation is 4 funnel
+// shifts + 4 shuffles per lane instead of 4 words x 6 shifts, and 32/G floods
+// run side by side.  The fixed point is the same set as the sequential loop.
+
+// word i of a W-word bitboard held by one lane of a group
+template <int W>
+struct LW {
+    u32 v;
+    int i;
+};
+template <int W>
+__device__ constexpr int lw_group() { return W <= 1 ? 1 : W <= 2 ? 2 : W <= 4 ? 4 : W <= 8 ? 8 : W <= 16 ? 16 : 32; }
+
+template <int W>
+__device__ __forceinline__ u32 word_of(const BB<W>& m, int i) {
+    u32 r = m.w[0];
+#pragma unroll
+    for (int k = 1; k < W; k++) r = (i == k) ? m.w[k] : r;
+    return r;
+}
+template <int W>
+__device__ __forceinline__ LW<W> operator|(const LW<W>& a, const LW<W>& b) { return LW<W>{a.v | b.v, a.i}; }
+template <int W>
+__device__ __forceinline__ LW<W> operator&(const LW<W>& a, const LW<W>& b) { return LW<W>{a.v & b.v, a.i}; }
+template <int W>
+__device__ __forceinline__ LW<W> operator&(const LW<W>& a, const BB<W>& m) {
+    return LW<W>{a.v & word_of<W>(m, a.i), a.i};
+}
+
+// gather (bit x = a bit (x + S)) on the lane-word view: words i+q and i+q+1
+// (S > 0) or i-q and i-q-1 (S < 0) come from the group's neighbouring lanes.
+// Only for walk helpers, which AND the result with the direction's validity
+// mask: a masked-in bit's source cell is on the board, so the words a shuffle
+// fetches from outside the group (it then returns the lane's own word) only
+// reach masked-out bits and need no zeroing.
+template <int W, int S>
+__device__ __forceinline__ LW<W> gather(const LW<W>& a) {
+    constexpr int G = lw_group<W>();
+    if constexpr (S == 0) {
+        return a;
+    } else if constexpr (S > 0) {
+        constexpr int q = S / 32;
+        constexpr unsigned s = (unsigned)(S % 32);
+        const u32 lo = q ? __shfl_down_sync(0xffffffffu, a.v, q, G) : a.v;
+        u32 r = lo;
+        if constexpr (s != 0) {
+            const u32 hi = __shfl_down_sync(0xffffffffu, a.v, q + 1, G);
+            r = __funnelshift_r(lo, hi, s);
+        }
+        return LW<W>{r, a.i};
+    } else {
+        constexpr int q = (-S) / 32;
+        constexpr unsigned s = (unsigned)((-S) % 32);
+        const u32 hi = q ? __shfl_up_sync(0xffffffffu, a.v, q, G) : a.v;
+        u32 r = hi;
+        if constexpr (s != 0) {
+            const u32 lo = __shfl_up_sync(0xffffffffu, a.v, q + 1, G);
+            r = __funnelshift_l(lo, hi, s);
+        }
+        return LW<W>{r, a.i};
+    }
+}
+
+__device__ __forceinline__ int lane_id() {
+    u32 l;
+    asm("mov.u32 %0, %%laneid;" : "=r"(l));
+    return (int)l;
+}
+
+// All 32 lanes call this (the caller checks __activemask() == full).  Lanes
+// with `need` get f = the component of f's cells inside `free_` (f ⊆ free_):
+// the fixed point of f <- (f | dil(f)) & free_.  Floods are handed to lane
+// groups in lane order, 32/G per round; the words travel through a per-warp
+// shared-memory slot row (word k of the r-th flood at slot r*G + k, so each
+// lane reads its own slot), which keeps the hand-off off the ALU pipe.
+template <int W, class Dil>
+__device__ __forceinline__ void coop_flood(bool need, const BB<W>& free_, BB<W>& f, Dil dil) {
+    constexpr int G = lw_group<W>();
+    constexpr int NGRP = 32 / G;
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ u32 lx_flood_buf[32][2][32];        // [warp of the block][free|f][slot]
+    const int lane = lane_id();
+    u32 (&buf)[2][32] = lx_flood_buf[(threadIdx.x >> 5) & 31];
+    const int grp = lane / G, idx = lane % G;
+    unsigned pending = __ballot_sync(FULL, need);
+    while (pending) {
+        const int rank = __popc(pending & ((1u << lane) - 1u));
+        const bool mine = ((pending >> lane) & 1u) && rank < NGRP;
+        __syncwarp(FULL);
+        if (mine) {
+#pragma unroll
+            for (int k = 0; k < W; k++) {
+                buf[0][rank * G + k] = free_.w[k];
+                buf[1][rank * G + k] = f.w[k];
+            }
+        }
+        __syncwarp(FULL);
+        const bool act = grp < __popc(pending) && idx < W;
+        LW<W> x{act ? buf[1][lane] : 0u, idx};
+        const LW<W> fre{act ? buf[0][lane] : 0u, idx};
+        while (true) {
+            const LW<W> g = (x | dil(x)) & fre;
+            const bool ch = g.v != x.v;
+            x = g;
+            if (!__any_sync(FULL, ch)) break;
+        }
+        __syncwarp(FULL);
+        buf[1][lane] = x.v;
+        __syncwarp(FULL);
+        if (mine) {
+#pragma unroll
+            for (int k = 0; k < W; k++) f.w[k] = buf[1][rank * G + k];
+        }
+        pending &= ~__ballot_sync(FULL, mine);
+    }
+}
+#endif
 
 }  // namespace lx

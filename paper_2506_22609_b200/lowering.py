@@ -155,7 +155,11 @@ class GameLowering(MoveLoweringMixin):
         name = f"walk_{d}_{k}"
         mask = self.em.const(self._walk_ok(d, k))
         self.em.helper(name, f"    static __device__ __forceinline__ BBW {name}(const BBW& x) "
-                             f"{{ return lx::gather<W, {S}>(x) & {mask}; }}")
+                             f"{{ return lx::gather<W, {S}>(x) & {mask}; }}\n"
+                             f"#if defined(__CUDA_ARCH__)\n"
+                             f"    static __device__ __forceinline__ lx::LW<W> {name}(const lx::LW<W>& x) "
+                             f"{{ return lx::gather<W, {S}>(x) & {mask}; }}\n"
+                             f"#endif")
         return f"{name}({expr})"
 
     def nb(self, d, expr):
@@ -471,7 +475,15 @@ class GameLowering(MoveLoweringMixin):
         n_len = node.length
         name = f"custodial_probe_{self.em.fresh('c')}"
         lines = []
-        for d in self.custodial_dirs(node):
+        dirs = self.custodial_dirs(node)
+        # captured cells are removed from the mirrored target plane as they are
+        # found (result = registers minus mirror) when no direction probes a
+        # cell another direction captures: k*S_e != j*S_d for 1 <= k <= n+1,
+        # 1 <= j <= n; otherwise cells are set in a register bitboard
+        steps = {d: self._shift[d] for d in dirs}
+        in_mirror = all(k * steps[e] != j * steps[d] for d in dirs for e in dirs if d != e
+                        for k in range(1, n_len + 2) for j in range(1, n_len + 1))
+        for d in dirs:
             S = self._shift[d]
             # branch-free: all probes issue (clamped when off-board), one rare branch
             lines.append(f"        {{ const bool ok = {self._max_steps(d)} >= {n_len + 1};")
@@ -479,9 +491,11 @@ class GameLowering(MoveLoweringMixin):
             conds.append(f"M::probe_if(ok, side, c + {(n_len + 1) * S})")
             lines.append("        if (" + " & ".join(conds) + ") {")
             for k in range(1, n_len + 1):
-                lines.append(f"            lx::setbit(out, c + {k * S});")
+                lines.append(f"            M::clear(tg, c + {k * S});" if in_mirror else
+                             f"            lx::setbit(out, c + {k * S});")
             lines.append("        } }")
         body = "\n".join(lines)
+        ret = ("lx::andnot(lx::sel(tg != 0, s.own0, s.own1), M::load(tg))" if in_mirror else "out")
         self.em.helper(name, f"""    static __device__ __forceinline__ BBW {name}(const St& s, int mover) {{
         typedef lx::Mirror<W> M;
         const int side = {side};
@@ -493,7 +507,7 @@ class GameLowering(MoveLoweringMixin):
         const int r = c / {self.emb_cols};
         const int col = c - r * {self.emb_cols};
 {body}
-        return out;
+        return {ret};
     }}""")
         return f"{name}(s, mover)"
 
@@ -983,7 +997,7 @@ class GameLowering(MoveLoweringMixin):
                 raise UnsupportedConstruct(f"{type(bad).__name__} is not static")
         return targets
 
-    def _dilate(self, plan, var):
+    def _dilate(self, plan, var, ty="BBW"):
         """Expression: cells with a plan-direction neighbour in `var`.
 
         Directions that are the composition of two others (nbr_d = nbr_b
@@ -1009,15 +1023,18 @@ class GameLowering(MoveLoweringMixin):
         if not comp:
             return " | ".join(self.nb(d, var) for d in plan)
         tmp = {d: f"{var}_{d}" for d in base}
-        decl = " ".join(f"const BBW {tmp[d]} = {self.nb(d, var)};" for d in base)
-        terms = []
+        terms, used = [], set()
         for a in base:
             inner = [tmp[b] for d, (a2, b) in comp.items() if a2 == a]
             if inner:
+                used.update(inner)
                 terms.append(self.nb(a, f"({var} | {' | '.join(sorted(set(inner)))})"))
             else:
+                used.add(tmp[a])
                 terms.append(tmp[a])
-        return f"([&]() {{ {decl} return BBW({' | '.join(terms)}); }}())"
+        decl = " ".join(f"const {ty} {tmp[d]} = {self.nb(d, var)};" for d in base
+                        if tmp[d] in used)
+        return f"([&]() {{ {decl} return {ty}({' | '.join(terms)}); }}())"
 
     def _conn_tracking(self):
         """Decide which (connected node, side) pairs get an incrementally
@@ -1176,18 +1193,32 @@ class GameLowering(MoveLoweringMixin):
                         f"            const BBW t0 = {self.em.const(self.slot_info[k][1][0])};")
                 store = self._slot_set(k, "R")
                 cond = f"side == {sd}"
-            flood = (f"                BBW f = a;                       // grow inside the side's stones outside R\n"
-                     f"                BBW g = (f | {dil_f}) & free_;\n"
+            dil_lw = self._dilate(plan, "x", ty="lx::LW<W>")
+            flood = (f"                BBW g = (f | {dil_f}) & free_;\n"
                      f"                while (!lx::equal(g, f)) {{\n"
                      f"                    f = g;\n"
                      f"                    g = (f | {dil_f}) & free_;\n"
                      f"                }}")
+            # grow inside the side's stones outside R; a converged full warp
+            # floods cooperatively (lx::coop_flood), else each lane alone
+            coop = (f"#if defined(__CUDA_ARCH__)\n"
+                    f"            if (__activemask() == 0xffffffffu) {{\n"
+                    f"                lx::coop_flood<W>(need, free_, f, [&](const lx::LW<W>& x) {{ return {dil_lw}; }});\n"
+                    f"                solo = false;\n"
+                    f"            }}\n"
+                    f"#endif") if os.environ.get("LX_COOP_FLOOD", "1") != "0" else ""
             out.append(f"""{head}
             const BBW a = lx::onehot<W>(cell_bit(cell));
-            if (({cond}) && lx::any((a & t0) | (({dil_a}) & R))) {{
-                const BBW mine = side ? s.own1 : s.own0;
-                const BBW free_ = lx::andnot(mine, R);
+            const bool need = ({cond}) && lx::any((a & t0) | (({dil_a}) & R));
+            const BBW mine = side ? s.own1 : s.own0;
+            const BBW free_ = lx::andnot(mine, R);
+            BBW f = a;
+            bool solo = true;
+{coop}
+            if (need) {{
+                if (solo) {{
 {flood}
+                }}
                 R = R | f;
                 {store}
             }}

@@ -256,3 +256,24 @@ def test_connect_four_opening_chi_square():
     assert vals.tolist() == list(range(35, 42))
     exp = n / 7
     assert float(((cnt - exp) ** 2 / exp).sum()) < 22.46
+
+
+def test_hex_cooperative_flood_matches_per_lane_flood(monkeypatch):
+    """Hex reach sets grown by the warp-cooperative flood (lx::coop_flood,
+    full warps) and by the per-lane flood (LX_COOP_FLOOD=0 lowering) give
+    identical final states at full size, and both match the oracle on a
+    sample; partial warps (odd batch) take the per-lane path."""
+    import os
+    path = os.path.join(lx.game.GAMES_DIR, "hex.ldx")
+    with open(path) as f:
+        text = f.read()
+    coop = lx.load_game(text)
+    monkeypatch.setenv("LX_COOP_FLOOD", "0")
+    solo = lx.load_game(text)
+    assert coop.lowered_key() != solo.lowered_key()
+    for B, seed in ((1 << 18, 3), (1000, 11)):
+        a = lx.engine.playout_random(coop, seed=seed, batch_size=B).final.digest()
+        b = lx.engine.playout_random(solo, seed=seed, batch_size=B).final.digest()
+        assert a == b, (B, seed)
+    want, _ = O.OracleGame("hex").playout(1000, seed=11)
+    assert a == O.digest(want)
