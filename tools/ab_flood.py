@@ -34,15 +34,16 @@ for name, g in games.items():
         g.rollout(seed=rng.episode_seed(0, B, e), out=out, batch_size=B, truncate=False,
                   check=False, stats=stats)
     torch.cuda.synchronize()
-    stats.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(a.reps)]
     e0.record()
-    for e in range(a.reps):
+    for e in range(a.reps):         # lx_rollout overwrites its stats vector
         g.rollout(seed=rng.episode_seed(0, B, 10000 + e), out=out, batch_size=B, truncate=False,
-                  check=False, stats=stats)
+                  check=False, stats=per[e])
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    stats = sum(per)
     steps = int(stats[0].item())
     res[name] = {"key": g.lowered_key(), "ms_per_episode": ms / a.reps,
                  "env_steps_per_s": steps / (ms / 1e3), "stats": stats.cpu().tolist()}
