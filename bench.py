@@ -477,18 +477,20 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
     for _ in range(3):
         est = env.step_(est, env.random_actions(est))
     torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    t_s = t_e = 0.0
+    # events queued back to back with no per-ply synchronize: the host stays
+    # ahead of the device, so each interval is device time, not launch latency
+    # of an idle GPU
     plies = 16
-    for _ in range(plies):
-        ev[0].record()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * plies + 1)]
+    ev[0].record()
+    for p in range(plies):
         acts = env.random_actions(est)
-        ev[1].record()
+        ev[2 * p + 1].record()
         est = env.step_(est, acts)
-        ev[2].record()
-        torch.cuda.synchronize()
-        t_s += ev[0].elapsed_time(ev[1])
-        t_e += ev[1].elapsed_time(ev[2])
+        ev[2 * p + 2].record()
+    torch.cuda.synchronize()
+    t_s = sum(ev[2 * p].elapsed_time(ev[2 * p + 1]) for p in range(plies))
+    t_e = sum(ev[2 * p + 1].elapsed_time(ev[2 * p + 2]) for p in range(plies))
     nq, A = game.info["nq"], game.action_space_size
     b_env = 2 * nq * 16 + 8 + A + 8 + 6      # state r/w, action, mask, rewards, flags
     gbs = b_env * B / (t_e / plies / 1e3) / 1e9

@@ -38,17 +38,18 @@ for name in a.games.split(","):
         acts = env.random_actions(st)
         st = env.step_(st, acts)
     torch.cuda.synchronize()
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    t_sample = t_step = 0.0
-    for _ in range(a.plies):
-        e[0].record()
+    # events back to back, one synchronize at the end (a per-ply synchronize
+    # would put the host's launch latency on an idle GPU into each interval)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2 * a.plies + 1)]
+    e[0].record()
+    for p in range(a.plies):
         acts = env.random_actions(st)
-        e[1].record()
+        e[2 * p + 1].record()
         st = env.step_(st, acts)
-        e[2].record()
-        torch.cuda.synchronize()
-        t_sample += e[0].elapsed_time(e[1])
-        t_step += e[1].elapsed_time(e[2])
+        e[2 * p + 2].record()
+    torch.cuda.synchronize()
+    t_sample = sum(e[2 * p].elapsed_time(e[2 * p + 1]) for p in range(a.plies))
+    t_step = sum(e[2 * p + 1].elapsed_time(e[2 * p + 2]) for p in range(a.plies))
     nq, A = env.game.info["nq"], env.num_actions
     b_sample = B * (nq * 16 + 8)
     b_step = B * (2 * nq * 16 + 8 + A + 8 + 6)
