@@ -1532,9 +1532,14 @@ class GameLowering(MoveLoweringMixin):
     }}
 {self.placement_stubs()}"""
         L = self.layout
-        # rollout block shape: 2 x 256 threads per SM (<= 128 registers) won a
-        # B200 sweep for every config game incl. Pente (128x3..5 and 256x2 tried)
-        r_threads, r_minb = 256, 2
+        # rollout block shape: 256 threads; resident blocks per SM by board
+        # size, from a B200 A/B at 2^22 envs over all 11 corpus games (same
+        # stats; profiles/r1n_ab_minb_*.json): 4 on <= 16-cell boards (TTT
+        # +2.3 %, gridworld +3.2 %), 3 up to 4 words (Wolf and Sheep +9.6 %,
+        # Yavalath +8 %, draughts +3.7 %, Hex +2.3 %, C4/Reversi/DHS within
+        # noise), 2 on the big boards (Pente -5.8 % at 3, Gomoku even)
+        r_threads = 256
+        r_minb = 4 if self.C <= 16 else (3 if self.W <= 4 else 2)
         r_threads = int(os.environ.get("LX_ROLLOUT_THREADS", r_threads))     # tuning overrides
         r_minb = int(os.environ.get("LX_ROLLOUT_MINB", r_minb))
         # batched game-over handling (lx_kernels.cuh): worth it for short games
