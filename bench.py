@@ -324,9 +324,11 @@ def main():
     value = tot[0] / (ms_max / 1000.0)
 
     extras = {}
+    if not args.no_extras:
+        extras["e2e"] = measure_e2e(args, game, rng, B, B_total, first, ws)
     if rank == 0 and not args.no_extras:
-        extras = measure_extras(args, game, lx, rng, B, B_total, value, ms_max / args.steps,
-                                clk.summary().get("sm_mhz"), tot)
+        extras.update(measure_extras(args, game, lx, rng, B, B_total, value, ms_max / args.steps,
+                                     clk.summary().get("sm_mhz"), tot))
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup,
@@ -355,11 +357,14 @@ def native_rollout(game, state, B, max_turns, seed, first, stats, work):
         game._stream()))
 
 
-def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, totals):
-    """e2e through the public API, the HBM-bound step kernel, roofline data,
-    and the CPU baseline (rank 0, N=1 sizes)."""
+def measure_e2e(args, game, rng, B, B_total, first, ws):
+    """e2e through the public API on every rank (each on its own env shard,
+    global indices [first, first + B)): Σ env steps over ranks ÷ max over
+    ranks of the host wall time of the timed steps, barrier on both sides."""
     import torch
-    out = {}
+    import torch.distributed as dist
+
+    from paper_2506_22609_b200 import shard
     # ---- e2e: every step copies its episode's per-env seeds host -> device
     # (pinned), runs the fused rollout through the public API and copies the
     # per-env outcomes + the step's stats device -> host.  Steps are
@@ -369,7 +374,7 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
     K = max(3, min(args.steps, 30))          # 30 steps: pipeline fill/drain < 3 %
     WU = 2
     n_it = K + WU
-    seeds_h = [torch.from_numpy(rng.spawn_seeds(rng.episode_seed(0, B_total, 20000 + e), B)
+    seeds_h = [torch.from_numpy(rng.spawn_seeds(rng.episode_seed(0, B_total, 20000 + e), B, first)
                                 .view("int64")).pin_memory() for e in range(n_it)]
     seeds_d = [torch.empty(B, dtype=torch.int64, device="cuda") for _ in range(2)]
     outc_d = [torch.empty(B, dtype=torch.int8, device="cuda") for _ in range(2)]
@@ -408,16 +413,33 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
     for it in range(WU):
         step(it)
     torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for it in range(WU, n_it):
         step(it)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        dist.barrier()
     steps = sum(int(stats_h[it][0]) for it in range(WU, n_it))
-    out["e2e"] = {"value": steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * 8,
-                  "d2h_bytes_per_step": B + 64, "steps_timed": K,
-                  "path": "B200Game.rollout(seeds=host->device) + outcomes/stats device->host, "
-                          "double-buffered over H2D / compute / D2H streams"}
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    n = torch.tensor([steps], dtype=torch.int64, device="cuda")
+    shard.max_over_ranks(t)
+    shard.reduce_stats(n)
+    return {"value": int(n.item()) / float(t.item()), "unit": UNIT,
+            "h2d_bytes_per_step": B * 8 * ws, "d2h_bytes_per_step": (B + 64) * ws,
+            "steps_timed": K,
+            "path": "B200Game.rollout(seeds=host->device) + outcomes/stats device->host, "
+                    "double-buffered over H2D / compute / D2H streams, every rank on its "
+                    "own shard, max wall time over ranks"}
+
+
+def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, totals):
+    """The HBM-bound step kernel, roofline data, the PGX env path and the CPU
+    baseline (rank 0, N=1 sizes)."""
+    import torch
+    out = {}
 
     # ---- roofline of the fused rollout kernel: integer ALU pipe bound.
     # Per-env-step instruction counts come from the ncu capture of this exact
@@ -474,13 +496,13 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
     # ---- PGX-style API path (LudaxEnvironment): lx_sample + lx_env_step per ply
     env = lx.LudaxEnvironment(game, auto_reset=True)
     est = env.init(seed=2, batch_size=B)
-    for _ in range(3):
+    for _ in range(16):
         est = env.step_(est, env.random_actions(est))
     torch.cuda.synchronize()
     # events queued back to back with no per-ply synchronize: the host stays
     # ahead of the device, so each interval is device time, not launch latency
     # of an idle GPU
-    plies = 16
+    plies = 64
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * plies + 1)]
     ev[0].record()
     for p in range(plies):
