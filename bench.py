@@ -490,7 +490,9 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
                           "ms_per_ply": ms, "env_steps_per_s_upper": B / (ms / 1e3),
                           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak_hbm,
                                        "unit": "GB/s", "frac": gbs / peak_hbm,
-                                       "traffic": None,
+                                       "traffic": step_traffic(game, "lx_random_step", B),
+                                       "traffic_unit": "DRAM bytes per launch (ncu, scaled "
+                                                       "to this batch)",
                                        "bytes_per_env_ply": 2 * game.info["nq"] * 16}}
 
     # ---- PGX-style API path (LudaxEnvironment): lx_sample + lx_env_step per ply
@@ -521,7 +523,9 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
         "env_steps_per_s": B / ((t_s + t_e) / plies / 1e3), "plies_timed": plies,
         "kernel": "lx_env_step",
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak_hbm, "unit": "GB/s",
-                     "frac": gbs / peak_hbm, "traffic": None, "bytes_per_env_step": b_env}}
+                     "frac": gbs / peak_hbm, "traffic": step_traffic(game, "lx_env_step", B),
+                     "traffic_unit": "DRAM bytes per launch (ncu, scaled to this batch)",
+                     "bytes_per_env_step": b_env}}
 
     # ---- CPU baseline (oracle port, all host threads, bounded sample)
     threads = os.cpu_count() or 1
@@ -554,6 +558,22 @@ def load_profile(game):
     # count; say so instead of dropping the roofline
     prof["stale"] = bool(prof.get("cubin_key")) and prof["cubin_key"] != game.lowered_key()
     return prof
+
+
+def step_traffic(game, kernel, B):
+    """DRAM bytes of one launch of a per-ply kernel at batch B, from the
+    committed ncu --set full capture (profiles/step_<game>.json, written by
+    tools/ncu_summary.py from tools/ncu_step.py); None when absent or when it
+    was taken on another build of this game."""
+    path = os.path.join(ROOT, "profiles", f"step_{game.info['name'].replace(' ', '_')}.json")
+    try:
+        with open(path) as f:
+            prof = json.load(f)
+        if prof.get("cubin_key") != game.lowered_key():
+            return None
+        return prof["kernels"][kernel]["dram_bytes_per_env"] * B
+    except Exception:
+        return None
 
 
 if __name__ == "__main__":

@@ -56,6 +56,40 @@ def raw(rep):
     return res
 
 
+def step_summaries(a):
+    """gpurun_out/step_<game>.json (tools/ncu_step.py) + stepprof_<game>_<kernel>.ncu-rep
+    -> profiles/<tag>_step_<game>.json and profiles/step_<Game>.json (read by bench.py
+    for the `traffic` of the HBM-bound per-ply kernels)."""
+    for fn in sorted(os.listdir(a.src)):
+        if not (fn.startswith("step_") and fn.endswith(".json")):
+            continue
+        with open(os.path.join(a.src, fn)) as f:
+            info = json.loads(f.read().strip().splitlines()[-1])
+        game, B = info["game"], info["batch"]
+        out = {"game": game, "batch": B, "cubin_key": info["cubin_key"], "kernels": {}}
+        for k in ("lx_random_step", "lx_sample", "lx_env_step"):
+            rep = os.path.join(a.src, f"stepprof_{game}_{k}.ncu-rep")
+            if not os.path.exists(rep):
+                continue
+            m = raw(rep)
+            dram = m.get("dram_read", 0) + m.get("dram_write", 0)
+            out["kernels"][k] = {
+                "duration_ns": m["duration_ns"], "dram_read": m.get("dram_read", 0),
+                "dram_write": m.get("dram_write", 0), "dram_bytes_per_env": dram / B,
+                "dram_gbs_under_ncu": dram / m["duration_ns"],
+                "registers": m.get("registers"), "grid": m.get("grid"),
+                "source": f"ncu --set full, {os.path.basename(rep)} (serialised, cold cache)"}
+            print(game, k, f"{dram / B:.1f} DRAM B/env", f"{dram / m['duration_ns']:.0f} GB/s")
+        from paper_2506_22609_b200.game import GAMES_DIR
+        from paper_2506_22609_b200.syntax import parse_game
+        with open(os.path.join(GAMES_DIR, f"{game}.ldx")) as f:
+            gname = parse_game(f.read()).name.replace(" ", "_")
+        for path in (os.path.join(a.out, f"{a.tag}_step_{game}.json"),
+                     os.path.join(a.out, f"step_{gname}.json")):
+            with open(path, "w") as f:
+                json.dump(out, f, indent=1, sort_keys=True)
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("src")
@@ -63,6 +97,9 @@ def main():
     p.add_argument("--out", default="profiles")
     a = p.parse_args()
     os.makedirs(a.out, exist_ok=True)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    step_summaries(a)
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from paper_2506_22609_b200.game import GAMES_DIR

@@ -17,3 +17,14 @@ if [ -z "$NO_LAUNCHES" ]; then
       --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 1 --no-extras > gpurun_out/ncu_launch.log 2>&1
   echo "launches rc=$?"
 fi
+# per-ply HBM-bound kernels (bench.py `traffic` of step_kernel / env_step_api)
+for gb in ${STEP_GAMES:-}; do
+  g=${gb%%:*}; b=${gb##*:}
+  timeout 300 python tools/ncu_step.py --game $g --batch $b > gpurun_out/step_$g.json 2>&1 || continue
+  for k in lx_random_step lx_sample lx_env_step; do
+    timeout 300 ncu --set full --clock-control none -k regex:"^$k\$" -s 2 -c 1 \
+        -o gpurun_out/stepprof_${g}_$k python tools/ncu_step.py --game $g --batch $b \
+        > gpurun_out/ncu_step_${g}_$k.log 2>&1
+    echo "$g $k rc=$?"
+  done
+done
