@@ -527,7 +527,9 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
                      "traffic_unit": "DRAM bytes per launch (ncu, scaled to this batch)",
                      "bytes_per_env_step": b_env}}
 
-    # ---- CPU baseline (oracle port, all host threads, bounded sample)
+    # ---- CPU baseline (oracle port, all host threads, bounded sample): N=1 only
+    if B_total != B:
+        return out
     threads = os.cpu_count() or 1
     r, steps, dt, n = cpu_rate(args.game, B_total, args.cpu_seconds, threads, args.max_turns)
     out["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": threads, "kind": "port",
