@@ -1,0 +1,6 @@
+# r1s: final round-1 check on the committed tree: GPU suite, smoke, bench both arms.
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -8 gpurun_out/smoke.log
+python bench.py > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; tail -c 800 gpurun_out/bench_c4.json
+python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 600 gpurun_out/bench_ref.json
