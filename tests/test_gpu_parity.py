@@ -277,3 +277,32 @@ def test_hex_cooperative_flood_matches_per_lane_flood(monkeypatch):
         assert a == b, (B, seed)
     want, _ = O.OracleGame("hex").playout(1000, seed=11)
     assert a == O.digest(want)
+
+
+# full BASELINE size (2^22 envs per GPU) for every corpus game: the fused
+# rollout's per-env outcome and ply count, spot-checked window by window
+# against the oracle replaying the same env indices (seeds = spawn(seed, i),
+# reference rng.py:45-54) -- head, a seeded interior window and the tail
+FULL_B = 1 << 22
+SPOT_W = {"tic_tac_toe": 16384, "connect_four": 8192, "hex": 2048, "reversi": 2048,
+          "pente": 1024, "gomoku": 1024, "yavalath": 2048, "english_draughts": 1024,
+          "dai_hasami_shogi": 512, "wolf_and_sheep": 2048, "gridworld": 16384}
+
+
+@pytest.mark.parametrize("name", list(SPOT_W))
+def test_full_size_rollout_windows_match_oracle(name):
+    g = game(name)
+    W = SPOT_W[name]
+    out = torch.empty(FULL_B, dtype=torch.int8, device="cuda")
+    turns = torch.empty(FULL_B, dtype=torch.int32, device="cuda")
+    _, st = g.rollout(batch_size=FULL_B, seed=4242, store=False, outcomes=out, turns=turns)
+    st = st.cpu().tolist()
+    assert st[5] == FULL_B and st[1] + st[2] + st[3] == FULL_B
+    mid = int(np.random.default_rng(7).integers(W, FULL_B - 2 * W))
+    og = O.OracleGame(name)
+    for off in (0, mid, FULL_B - W):
+        want, _ = og.playout(seeds=O.spawn_seeds(4242, W, first=off), threads=8)
+        got_o = out[off:off + W].cpu().numpy()
+        got_t = turns[off:off + W].cpu().numpy()
+        assert np.array_equal(got_o, want["outcome"]), (name, off)
+        assert np.array_equal(got_t, want["move_count"]), (name, off)
