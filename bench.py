@@ -1,4 +1,4 @@
-"""Benchmark: env steps/s of uniform-random rollouts (Connect Four 6x7).
+"""Benchmark: env steps/s of uniform-random rollouts, every BASELINE config.
 
 Metric and protocol follow the reference benchmark (reference:
 pkg/src/boardlang/evaluation.py:197-233): one step of this bench = one
@@ -7,12 +7,21 @@ position with per-env seeds spawn(hash_key(0, B_total, e), global index),
 played with uniform legal actions until every env has terminated (cap 200
 plies); env steps = live envs advanced by one ply, summed.
 
+The headline line is configs[1] (Connect Four, 2^22 envs per GPU).  At N=1
+the line also carries ``per_config``: every BASELINE.json config measured in
+the same run -- Tic-Tac-Toe at B=1024 (configs[0], the reference's CPU-sized
+case) and at 2^22, Connect Four, Hex, Reversi and Pente at 2^22 -- each with
+its own timed episodes, roofline, e2e leg, CPU baseline and an oracle
+parity check of the benchmarked episode's final states.
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--game G]
   python bench.py --impl reference ...      # CPU reference arm (oracle port)
 
 Under torchrun each rank plays its own slice [rank*B, (rank+1)*B) of the
 global env index space (weak scaling, no collective on the hot path); one
-NCCL all-reduce of the stats after the timed region.
+all-reduce (MAX) of the device time and one (SUM) of the stats after the
+timed region.  ``run_distributed`` holds that flow; the GPU arm and the CPU
+test stub (tests/test_bench_dist.py, gloo world size 2) both run through it.
 """
 
 from __future__ import annotations
@@ -37,8 +46,21 @@ GAME_FILES = {"connect_four": "Connect Four 6x7", "tic_tac_toe": "Tic-Tac-Toe",
               "dai_hasami_shogi": "Dai Hasami Shogi 9x9", "wolf_and_sheep": "Wolf and Sheep 8x8",
               "gridworld": "Frozen Lake gridworld 4x4"}
 
+# BASELINE.json configs measured at N=1: (label, game, batch, timed steps,
+# envs of the benchmarked episode replayed by the oracle).  The parity sample
+# is every env where the oracle finishes in seconds on the box's host cores
+# (TTT, C4), else a 2^20 prefix of the same episode.
+PER_CONFIG = (
+    ("configs[0]", "tic_tac_toe", 1024, 400, 1024),
+    ("configs[0]@2^22", "tic_tac_toe", 1 << 22, 20, 1 << 22),
+    ("configs[1]", "connect_four", 1 << 22, 20, 1 << 22),
+    ("configs[2]", "hex", 1 << 22, 20, 1 << 20),
+    ("configs[3]", "reversi", 1 << 22, 20, 1 << 20),
+    ("configs[4]", "pente", 1 << 22, 20, 1 << 20),
+)
 
-def parse():
+
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=400)
@@ -50,8 +72,13 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU time of the bounded CPU-baseline sample")
     p.add_argument("--no-extras", action="store_true",
-                   help="skip the e2e / step-kernel / cpu-baseline legs")
-    return p.parse_args()
+                   help="skip the e2e / step-kernel / cpu-baseline / per-config legs")
+    p.add_argument("--no-per-config", action="store_true",
+                   help="headline config only (skip the per_config block)")
+    p.add_argument("--parity-scale", type=float, default=1.0,
+                   help="scale the per-config oracle parity samples (quick runs)")
+    p.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)   # CPU test arm
+    return p.parse_args(argv)
 
 
 def dist_env():
@@ -69,12 +96,15 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, enabled=True):
         self.index = index
         self.rows = []
         self._proc = None
+        self.enabled = enabled
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -176,13 +206,16 @@ def run_reference(args):
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    ref = numpy_reference_rate(args.game, seconds=3.0, max_turns=args.max_turns)
-    if ref:
-        line["reference_numpy"] = ref
-    mp = numpy_reference_mp(args.game, seconds=6.0, max_turns=args.max_turns)
-    if mp:
-        line["reference_numpy_all_cores"] = mp
+    if not args.no_extras:
+        line["reference_numpy"] = numpy_reference_rate(args.game, seconds=3.0,
+                                                       max_turns=args.max_turns)
+        line["reference_numpy_all_cores"] = numpy_reference_mp(args.game, seconds=6.0,
+                                                               max_turns=args.max_turns)
     print(json.dumps(line), flush=True)
+
+
+def _ref_dir():
+    return os.path.join(ROOT, "baseline", "_ref")
 
 
 def _mp_worker(args):
@@ -190,8 +223,7 @@ def _mp_worker(args):
     _run_episode on its own episodes until `seconds` of loop time."""
     game, wid, seconds, max_turns, batch = args
     os.environ["OMP_NUM_THREADS"] = "1"
-    ref_dir = os.path.join(ROOT, "baseline", "_ref")
-    sys.path.insert(0, ref_dir)
+    sys.path.insert(0, _ref_dir())
     import numpy as np
     import boardlang
     from boardlang import evaluation, rng as rrng
@@ -212,8 +244,8 @@ def numpy_reference_mp(game, seconds, max_turns, batch=1024):
     os.cpu_count() forked workers, OMP_NUM_THREADS=1, each timing its own
     _run_episode loop (evaluation.py:197-211) on independent B=1024 episodes;
     rate = sum of steps / max worker loop time.  Context only."""
-    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "boardlang")):
-        return None
+    if not os.path.isdir(os.path.join(_ref_dir(), "boardlang")):
+        return {"error": "baseline/_ref is not staged (build() installs it from /root/reference)"}
     try:
         import multiprocessing as mp
         n = os.cpu_count() or 1
@@ -232,9 +264,9 @@ def numpy_reference_rate(game, seconds, max_turns, batch=1024):
     """For context only: the unmodified reference (pip-installed into
     baseline/_ref) timed through its own _run_episode (evaluation.py:197-211),
     one process, B=1024, on the same game program."""
-    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    ref_dir = _ref_dir()
     if not os.path.isdir(os.path.join(ref_dir, "boardlang")):
-        return None
+        return {"error": "baseline/_ref is not staged (build() installs it from /root/reference)"}
     try:
         sys.path.insert(0, ref_dir)
         import numpy as np
@@ -258,77 +290,41 @@ def numpy_reference_rate(game, seconds, max_turns, batch=1024):
             sys.path.remove(ref_dir)
 
 
-def config(args, ws):
-    return {"workload": f"{GAME_FILES[args.game]} uniform-random rollouts, "
-                        f"{args.batch} envs per GPU, full episodes (cap {args.max_turns} plies)",
-            "game": args.game, "batch_per_gpu": args.batch,
-            "global_batch": args.batch * ws, "max_turns": args.max_turns,
+def config(args, ws, game=None, batch=None):
+    game = game or args.game
+    batch = batch or args.batch
+    return {"workload": f"{GAME_FILES[game]} uniform-random rollouts, "
+                        f"{batch} envs per GPU, full episodes (cap {args.max_turns} plies)",
+            "game": game, "batch_per_gpu": batch,
+            "global_batch": batch * ws, "max_turns": args.max_turns,
             "parallelism": f"env-shard x{ws}",
-            "l2": "final states written each step (48-128 B/env, > 126 MB L2 at 2^22 envs)"}
+            "l2": "final states written each step (32-128 B/env: > 126 MB L2 at 2^22 envs); "
+                  "the rollout reads no input but its seeds, so there is nothing to flush"}
 
 
-# ------------------------------------------------------------------ GPU arm
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
-    import torch
-    import torch.distributed as dist
-
-    import paper_2506_22609_b200 as lx
-    from paper_2506_22609_b200 import rng, shard
-
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    game = lx.load_config_game(args.game)
-    B, B_total = args.batch, args.batch * ws
-    first, _ = shard.shard_range(rank, ws, B)
-    state = game.empty_state(B)
-    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
-    work = torch.zeros(4, dtype=torch.int64, device="cuda")
-    acc = torch.zeros(8, dtype=torch.int64, device="cuda")
-    stream = torch.cuda.current_stream()
-
-    def episode(e):
-        # fresh envs from the episode seed, final states stored to `state`
-        seed = rng.episode_seed(0, B_total, e)
-        native_rollout(game, state, B, args.max_turns, seed, first, stats, work)
-        acc.add_(stats)
-
+# ------------------------------------------------------------------ shared distributed flow
+def run_distributed(args, arm):
+    """Warm-up, barrier, K timed episodes, max-over-ranks time, summed stats,
+    e2e leg on every rank, rank-0 extras, one JSON line from rank 0.  `arm`
+    is the GPU arm (below) or the CPU stub of tests/test_bench_dist.py."""
+    ws, rank = arm.world_size, arm.rank
     for w in range(args.warmup):
-        episode(w)
-    torch.cuda.synchronize()
-    acc.zero_()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for e in range(args.steps):
-            episode(10_000 + e)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    tot = acc.clone()
-    shard.max_over_ranks(t)
-    shard.reduce_stats(tot)
-    if ws > 1:
-        dist.barrier()
-    ms_max = float(t.item())
-    tot = tot.cpu().tolist()
+        arm.episode(w)
+    arm.reset_totals()
+    arm.barrier()
+    arm.sync()
+    with arm.clock_sampler() as clk:
+        ms = arm.timed(lambda: [arm.episode(10_000 + e) for e in range(args.steps)])
+    ms_max = arm.max_over_ranks(ms)
+    tot = arm.reduced_totals()
+    arm.barrier()
     value = tot[0] / (ms_max / 1000.0)
-
     extras = {}
     if not args.no_extras:
-        extras["e2e"] = measure_e2e(args, game, rng, B, B_total, first, ws)
+        extras["e2e"] = arm.e2e()
     if rank == 0 and not args.no_extras:
-        extras.update(measure_extras(args, game, lx, rng, B, B_total, value, ms_max / args.steps,
-                                     clk.summary().get("sm_mhz"), tot))
+        extras.update(arm.extras(value, ms_max / args.steps, clk.summary().get("sm_mhz"), tot))
+    line = None
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup,
@@ -336,14 +332,112 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "u32",
                 "data": "synthetic (seeded random play from the start position)",
                 "config": config(args, ws), "clocks": clk.summary(),
-                "gpu_launches": args.steps,
+                "gpu_launches": args.steps * arm.launches_per_episode,
                 "totals": {"env_steps": tot[0], "p1_wins": tot[1], "p2_wins": tot[2],
                            "draws": tot[3], "truncated": tot[4], "envs": tot[5]},
                 "mean_plies": tot[0] / max(tot[5], 1)}
         line.update(extras)
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
+    arm.barrier()
+    arm.close()
+    return line
+
+
+# ------------------------------------------------------------------ GPU arm
+class GpuArm:
+    launches_per_episode = 1           # one lx_rollout per episode
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        import paper_2506_22609_b200 as lx
+        from paper_2506_22609_b200 import rng, shard
+        self.torch, self.dist, self.lx, self.rng, self.shard = torch, dist, lx, rng, shard
+        self.args = args
+        self.world_size, self.rank, self.local = dist_env()
+        torch.cuda.set_device(self.local)
+        if self.world_size > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        self.game = lx.load_config_game(args.game)
+        self.B = args.batch
+        self.B_total = args.batch * self.world_size
+        self.first, _ = shard.shard_range(self.rank, self.world_size, self.B)
+        self.state = self.game.empty_state(self.B)
+        self.stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+        self.work = torch.zeros(4, dtype=torch.int64, device="cuda")
+        self.acc = torch.zeros(8, dtype=torch.int64, device="cuda")
+        self.last_episode = None
+
+    # -- flow hooks --
+    def episode(self, e):
+        seed = self.rng.episode_seed(0, self.B_total, e)
+        native_rollout(self.game, self.state, self.B, self.args.max_turns, seed, self.first,
+                       self.stats, self.work)
+        self.acc.add_(self.stats)
+        self.last_episode = e
+
+    def reset_totals(self):
+        self.torch.cuda.synchronize()
+        self.acc.zero_()
+
+    def barrier(self):
+        if self.world_size > 1:
+            self.dist.barrier()
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+    def clock_sampler(self):
+        return ClockSampler(self.local)
+
+    def timed(self, fn):
+        torch = self.torch
+        stream = torch.cuda.current_stream()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1)
+
+    def max_over_ranks(self, ms):
+        t = self.torch.tensor([ms], dtype=self.torch.float64, device="cuda")
+        self.shard.max_over_ranks(t)
+        return float(t.item())
+
+    def reduced_totals(self):
+        tot = self.acc.clone()
+        self.shard.reduce_stats(tot)
+        return tot.cpu().tolist()
+
+    def e2e(self):
+        return measure_e2e(self.args, self.game, self.rng, self.B, self.B_total, self.first,
+                           self.world_size)
+
+    def extras(self, value, ms_step, clock_mhz, totals):
+        out = measure_extras(self.args, self.game, self.lx, self.rng, self.B, self.B_total,
+                             value, ms_step, clock_mhz, totals)
+        if self.B_total == self.B and not self.args.no_per_config:
+            out["per_config"] = measure_per_config(self, value, ms_step, totals, out)
+        return out
+
+    def close(self):
+        if self.world_size > 1:
+            self.dist.destroy_process_group()
+
+
+def main(argv=None):
+    args = parse(argv)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if args.stub:                                      # CPU test arm (gloo)
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from bench_stub import StubArm
+        run_distributed(args, StubArm(args))
+        return
+    run_distributed(args, GpuArm(args))
 
 
 def native_rollout(game, state, B, max_turns, seed, first, stats, work):
@@ -357,7 +451,7 @@ def native_rollout(game, state, B, max_turns, seed, first, stats, work):
         game._stream()))
 
 
-def measure_e2e(args, game, rng, B, B_total, first, ws):
+def measure_e2e(args, game, rng, B, B_total, first, ws, steps=None):
     """e2e through the public API on every rank (each on its own env shard,
     global indices [first, first + B)): Σ env steps over ranks ÷ max over
     ranks of the host wall time of the timed steps, barrier on both sides."""
@@ -371,7 +465,7 @@ def measure_e2e(args, game, rng, B, B_total, first, ws):
     # double-buffered over three streams (H2D, compute, D2H), so step i+1's
     # upload and step i's download overlap step i's / i+1's rollout; all the
     # copies stay inside the timed region.
-    K = max(3, min(args.steps, 30))          # 30 steps: pipeline fill/drain < 3 %
+    K = steps if steps is not None else max(3, min(args.steps, 30))
     WU = 2
     n_it = K + WU
     seeds_h = [torch.from_numpy(rng.spawn_seeds(rng.episode_seed(0, B_total, 20000 + e), B, first)
@@ -422,9 +516,9 @@ def measure_e2e(args, game, rng, B, B_total, first, ws):
     e2e_s = time.perf_counter() - t0
     if ws > 1:
         dist.barrier()
-    steps = sum(int(stats_h[it][0]) for it in range(WU, n_it))
+    steps_done = sum(int(stats_h[it][0]) for it in range(WU, n_it))
     t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    n = torch.tensor([steps], dtype=torch.int64, device="cuda")
+    n = torch.tensor([steps_done], dtype=torch.int64, device="cuda")
     shard.max_over_ranks(t)
     shard.reduce_stats(n)
     return {"value": int(n.item()) / float(t.item()), "unit": UNIT,
@@ -435,26 +529,26 @@ def measure_e2e(args, game, rng, B, B_total, first, ws):
                     "own shard, max wall time over ranks"}
 
 
-def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, totals):
-    """The HBM-bound step kernel, roofline data, the PGX env path and the CPU
-    baseline (rank 0, N=1 sizes)."""
-    import torch
-    out = {}
-
-    # ---- roofline of the fused rollout kernel: integer ALU pipe bound.
-    # Per-env-step instruction counts come from the ncu capture of this exact
-    # cubin (profiles/rollout_<Game>.json, keyed by the NVRTC cache key);
-    # achieved = count x live env steps/s; peak = pipe rate x SMs x clock.
+def rollout_roofline(game, value, totals, clock_mhz):
+    """Roofline of the fused rollout kernel: integer ALU pipe bound.
+    Per-env-step instruction counts come from the ncu capture of this exact
+    cubin (profiles/rollout_<Game>.json, keyed by the NVRTC cache key);
+    achieved = count x live env steps/s; peak = pipe rate x SMs x clock."""
     prof = load_profile(game)
     clk_mhz = float(clock_mhz or 1965.0)
-    sms = 148
-    peak_alu = sms * 4 * 0.5 * clk_mhz * 1e6          # ALU pipe: 0.5 warp-inst/clk/SMSP
+    sms = int((prof or {}).get("sms") or 148)
+    # ALU pipe peak per SM per cycle from ncu (sm__inst_executed_pipe_alu
+    # .avg.peak_sustained: 4 SMSP x 0.5 warp-inst/clk) when the capture has it
+    per_sm = float((prof or {}).get("alu_peak_per_sm_cycle") or 2.0)
+    src = ("ncu sm__inst_executed_pipe_alu.avg.peak_sustained"
+           if (prof or {}).get("alu_peak_per_sm_cycle") else "4 SMSP x 0.5/clk pipe rate")
+    peak_alu = sms * per_sm * clk_mhz * 1e6
     peak_issue = sms * 4 * 1.0 * clk_mhz * 1e6        # issue: 1 warp-inst/clk/SMSP
     mean_plies = totals[0] / max(totals[5], 1)
     rl = {"bound": "int_alu", "unit": "Gwarp-inst/s", "kernel": "lx_rollout",
           "peak": peak_alu / 1e9,
-          "peak_source": f"{sms} SMs x 4 SMSP x 0.5 ALU warp-inst/clk (B300_MICROARCH.md pipe "
-                         f"rates) x {clk_mhz:.0f} MHz measured SM clock",
+          "peak_source": f"{sms} SMs x {per_sm:g} ALU warp-inst/clk/SM ({src}) x "
+                         f"{clk_mhz:.0f} MHz SM clock sampled in the run",
           "achieved": None, "frac": None, "traffic": None,
           "algorithmic_bytes_per_env_step": game.info["nq"] * 16 / mean_plies}
     if prof:
@@ -465,14 +559,22 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
                    "traffic_unit": "DRAM bytes per env step (ncu)",
                    "traffic_bytes_per_launch": prof["dram_bytes_per_launch"],
                    "traffic_profile_batch": prof.get("batch"),
+                   "alu_warp_inst_per_env_step": prof["alu_warp_inst_per_env_step"],
                    "issue": {"achieved": iss / 1e9, "peak": peak_issue / 1e9,
                              "frac": iss / peak_issue},
                    "ncu_alu_pipe_pct": prof.get("alu_pipe_elapsed_pct"),
                    "inst_source": prof.get("source"), "cubin_key": prof.get("cubin_key"),
                    "profile_stale": prof.get("stale", False)})
-    out["roofline"] = rl
+    return rl
 
-    # ---- HBM-bound per-ply step kernel (PGX-style API path)
+
+def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, totals):
+    """The HBM-bound step kernel, roofline data, the PGX env path and the CPU
+    baseline (rank 0, N=1 sizes)."""
+    import torch
+    out = {"roofline": rollout_roofline(game, value, totals, clock_mhz)}
+
+    # ---- HBM-bound per-ply step kernel (CompiledGame.random_actions + step_into)
     st = game.init(B, seed=1)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -494,38 +596,7 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
                                        "traffic_unit": "DRAM bytes per launch (ncu, scaled "
                                                        "to this batch)",
                                        "bytes_per_env_ply": 2 * game.info["nq"] * 16}}
-
-    # ---- PGX-style API path (LudaxEnvironment): lx_sample + lx_env_step per ply
-    env = lx.LudaxEnvironment(game, auto_reset=True)
-    est = env.init(seed=2, batch_size=B)
-    for _ in range(16):
-        est = env.step_(est, env.random_actions(est))
-    torch.cuda.synchronize()
-    # events queued back to back with no per-ply synchronize: the host stays
-    # ahead of the device, so each interval is device time, not launch latency
-    # of an idle GPU
-    plies = 64
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * plies + 1)]
-    ev[0].record()
-    for p in range(plies):
-        acts = env.random_actions(est)
-        ev[2 * p + 1].record()
-        est = env.step_(est, acts)
-        ev[2 * p + 2].record()
-    torch.cuda.synchronize()
-    t_s = sum(ev[2 * p].elapsed_time(ev[2 * p + 1]) for p in range(plies))
-    t_e = sum(ev[2 * p + 1].elapsed_time(ev[2 * p + 2]) for p in range(plies))
-    nq, A = game.info["nq"], game.action_space_size
-    b_env = 2 * nq * 16 + 8 + A + 8 + 6      # state r/w, action, mask, rewards, flags
-    gbs = b_env * B / (t_e / plies / 1e3) / 1e9
-    out["env_step_api"] = {
-        "path": "LudaxEnvironment.random_actions + step_ (auto_reset), device tensors",
-        "env_steps_per_s": B / ((t_s + t_e) / plies / 1e3), "plies_timed": plies,
-        "kernel": "lx_env_step",
-        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak_hbm, "unit": "GB/s",
-                     "frac": gbs / peak_hbm, "traffic": step_traffic(game, "lx_env_step", B),
-                     "traffic_unit": "DRAM bytes per launch (ncu, scaled to this batch)",
-                     "bytes_per_env_step": b_env}}
+    out["env_step_api"] = measure_env_api(args, game, lx, B)
 
     # ---- CPU baseline (oracle port, all host threads, bounded sample): N=1 only
     if B_total != B:
@@ -539,12 +610,152 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
     return out
 
 
+def measure_env_api(args, game, lx, B):
+    """PGX-style API path (LudaxEnvironment): one fused launch per ply
+    (uniform-random action sampled in the step kernel, auto-reset), device
+    tensors, output buffers reused; bool mask and bit-packed mask variants."""
+    import torch
+    peak_hbm = measured_hbm()
+    res = {}
+    for fmt in ("bool", "bits"):
+        env = lx.LudaxEnvironment(game, auto_reset=True, mask_format=fmt)
+        est = env.init(seed=2, batch_size=B)
+        for _ in range(16):
+            est = env.step_(est, env.RANDOM)
+        torch.cuda.synchronize()
+        plies = 64
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(plies):
+            est = env.step_(est, env.RANDOM)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / plies
+        b_env = env.bytes_per_env_step()
+        gbs = b_env * B / (ms / 1e3) / 1e9
+        res[fmt] = {"env_steps_per_s": B / (ms / 1e3), "ms_per_ply": ms,
+                    "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak_hbm,
+                                 "unit": "GB/s", "frac": gbs / peak_hbm,
+                                 "traffic": step_traffic(game, "lx_env_step", B, fmt),
+                                 "traffic_unit": "DRAM bytes per launch (ncu, scaled to "
+                                                 "this batch)",
+                                 "bytes_per_env_step": b_env}}
+    return {"path": "LudaxEnvironment.step_(state, RANDOM) (auto_reset): action sampled, "
+                    "applied, rewards / flags / next legal mask written in one lx_env_step "
+                    "launch per ply; device tensors, output buffers reused",
+            "kernel": "lx_env_step", "plies_timed": 64,
+            "env_steps_per_s": res["bool"]["env_steps_per_s"],
+            "roofline": res["bool"]["roofline"], "bits_mask": res["bits"]}
+
+
+# ------------------------------------------------------------------ per-config block
+def time_config(arm, game, B, steps, warmup, max_turns):
+    """Timed episodes of one config on this GPU (N=1): returns (ms, totals,
+    final-state buffer of the last timed episode, its episode id)."""
+    torch, rng = arm.torch, arm.rng
+    state = game.empty_state(B)
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    work = torch.zeros(4, dtype=torch.int64, device="cuda")
+    acc = torch.zeros(8, dtype=torch.int64, device="cuda")
+
+    def ep(e):
+        native_rollout(game, state, B, max_turns, rng.episode_seed(0, B, e), 0, stats, work)
+        acc.add_(stats)
+    for w in range(warmup):
+        ep(w)
+    torch.cuda.synchronize()
+    acc.zero_()
+    with ClockSampler(arm.local, enabled=B >= (1 << 20)) as clk:
+        ms = arm.timed(lambda: [ep(10_000 + e) for e in range(steps)])
+    return ms, acc.cpu().tolist(), state, 10_000 + steps - 1, clk.summary()
+
+
+def parity_check(name, game, state, B, episode, n, max_turns):
+    """Every field of the first n final states of the benchmarked episode
+    (exported to the reference GameState layout by lx_export) against the
+    CPU oracle replaying the same env seeds; also the oracle's rate on that
+    sample (the config's cpu_baseline).  The bench episodes do not truncate
+    (reference _run_episode); the cap's truncation is applied to both sides
+    the way engine.playout_random does (engine.py:156-160)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2506_22609_b200.game import DeviceState
+    n = min(n, B)
+    sub = DeviceState(game, state.words[:, :n].contiguous(), n) if n < B else state
+    got = game._export(sub)
+    cap = ~got["terminated"]
+    got["terminated"] = got["terminated"] | cap
+    got["truncated"] = got["truncated"] | cap
+    got["outcome"] = np.where(cap, 0, got["outcome"]).astype(np.int8)
+    og = O.OracleGame(name)
+    threads = os.cpu_count() or 1
+    seeds = O.spawn_seeds(O.hash_key3(0, B, episode), n)
+    st = og.init(n, seeds=seeds)
+    t0 = time.perf_counter()
+    want, steps = og.playout(state=st, max_turns=max_turns, threads=threads)
+    dt = time.perf_counter() - t0
+    bad = np.zeros(n, bool)
+    fields = []
+    for k, v in want.items():
+        if k not in got:
+            continue
+        fields.append(k)
+        a, b = np.asarray(got[k]).reshape(n, -1), np.asarray(v).reshape(n, -1)
+        bad |= (a != b).any(axis=1)
+    first_bad = int(np.argmax(bad)) if bad.any() else None
+    return ({"envs_checked": n, "of_batch": B, "episode": episode, "mismatches": int(bad.sum()),
+             "first_mismatch_row": first_bad, "fields": fields,
+             "checker": "oracle/ludax_oracle.c (C restatement pinned to reference fixtures)"},
+            {"value": steps / dt, "unit": UNIT, "cores": threads, "kind": "port",
+             "cpu_model": cpu_model(),
+             "sample": f"the first {n} envs of benchmarked episode {episode} replayed by the "
+                       f"oracle port for the parity check: {steps} env steps, {dt:.1f}s on "
+                       f"{threads} threads"})
+
+
+def measure_per_config(arm, value, ms_step, totals, head_extras):
+    """Every BASELINE.json config at N=1 (see PER_CONFIG)."""
+    args = arm.args
+    out = []
+    for label, name, B, steps, n_par in PER_CONFIG:
+        n_par = max(1, int(n_par * args.parity_scale))
+        entry = {"config": label, "game": name, "batch": B}
+        if name == args.game and B == args.batch:
+            # the headline: its timed episodes, e2e and roofline are the line's own
+            game, state, episode = arm.game, arm.state, arm.last_episode
+            entry.update({"steps": args.steps, "ms_per_step": ms_step, "value": value,
+                          "mean_plies": totals[0] / max(totals[5], 1),
+                          "roofline": head_extras.get("roofline"), "e2e": "headline e2e",
+                          "clocks": "headline clocks"})
+        else:
+            game = arm.lx.load_config_game(name)
+            ms, tot, state, episode, clk = time_config(arm, game, B, steps, 3, args.max_turns)
+            val = tot[0] / (ms / 1000.0)
+            entry.update({"steps": steps, "warmup": 3, "ms_per_step": ms / steps, "value": val,
+                          "mean_plies": tot[0] / max(tot[5], 1),
+                          "totals": {"env_steps": tot[0], "p1_wins": tot[1], "p2_wins": tot[2],
+                                     "draws": tot[3], "envs": tot[5]},
+                          "clocks": clk,
+                          "roofline": rollout_roofline(game, val, tot, clk.get("sm_mhz")),
+                          "e2e": measure_e2e(args, game, arm.rng, B, B, 0, 1,
+                                             steps=min(steps, 12))})
+        entry["unit"] = UNIT
+        entry["workload"] = (f"{GAME_FILES[name]} uniform-random rollouts, {B} envs, "
+                             f"full episodes (cap {args.max_turns} plies)")
+        par, cpu = parity_check(name, game, state, B, episode, n_par, args.max_turns)
+        entry["parity"] = par
+        entry["cpu_baseline"] = cpu
+        out.append(entry)
+    return out
+
+
 def measured_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"])
     except Exception:
-        return 6650.0
+        return 6553.3
 
 
 def load_profile(game):
@@ -562,7 +773,7 @@ def load_profile(game):
     return prof
 
 
-def step_traffic(game, kernel, B):
+def step_traffic(game, kernel, B, variant=None):
     """DRAM bytes of one launch of a per-ply kernel at batch B, from the
     committed ncu --set full capture (profiles/step_<game>.json, written by
     tools/ncu_summary.py from tools/ncu_step.py); None when absent or when it
@@ -573,7 +784,8 @@ def step_traffic(game, kernel, B):
             prof = json.load(f)
         if prof.get("cubin_key") != game.lowered_key():
             return None
-        return prof["kernels"][kernel]["dram_bytes_per_env"] * B
+        key = kernel if variant in (None, "bool") else f"{kernel}:{variant}"
+        return prof["kernels"][key]["dram_bytes_per_env"] * B
     except Exception:
         return None
 

@@ -36,14 +36,21 @@ extern "C" {
 typedef struct lx_game lx_game;
 
 /* Static facts of a compiled game (reference CompiledGame.describe,
-   compiler.py:628-650, plus the device state layout). */
+   compiler.py:628-650, plus the device state layout), read from the
+   generated unit's lx_facts constant at lx_game_create: a C caller sizes
+   every buffer from these alone. */
 typedef struct {
     int32_t num_cells;          /* C */
     int32_t num_actions;        /* A: C, C*C (movement) or #directions (gridworld), +1 pass; ActionCodec.size (codec.py:58-69) */
     int32_t pass_index;         /* -1 when the game has no pass action */
     int32_t board_words;        /* W: 32-bit words per player bitboard */
-    int32_t state_quads;        /* NQ: 16-byte quads per env in HBM */
-    int32_t num_sms;            /* SMs of the device the module is loaded on */
+    int32_t state_quads;        /* NQ: 16-byte quads per env in HBM; a batch of B envs is NQ*B*16 bytes */
+    int32_t state_bytes;        /* 16 * NQ: device bytes per env */
+    int32_t private_words;      /* NX: piece-type planes + rule-private words per env */
+    int32_t mechanics;          /* 0 placement, 1 movement, 2 gridworld */
+    int32_t mask_words;         /* ceil(A / 32): u32 words per bit-packed mask row */
+    int32_t device;             /* CUDA device ordinal the handle is bound to */
+    int32_t num_sms;            /* SMs of that device */
     int32_t rollout_blocks;     /* persistent grid of lx_rollout (SMs x blocks/SM) */
     int32_t rollout_threads;    /* block size of lx_rollout */
 } lx_game_info;
@@ -72,11 +79,18 @@ int lx_version(void);
 const char *lx_last_error(void);
 
 /* Compile (or fetch from cache_dir) the generated translation unit and load
-   it on the current CUDA context.  Replaces CompiledGame.__init__
-   (compiler.py:200-286).  `source` is the lowering's output; headers are
-   resolved from include_dir; cubins are cached as <cache_dir>/<key>.cubin. */
+   it on the calling thread's current CUDA context (the device selected with
+   cudaSetDevice / torch.cuda.set_device / lx_bind_device; no current context
+   is an LX_ECUDA error).  The handle is bound to that device: calls made
+   while another device is current fail with LX_EINVALID -- create one handle
+   per device.  Replaces CompiledGame.__init__ (compiler.py:200-286).
+   `source` is the lowering's output; headers are resolved from include_dir;
+   cubins are cached as <cache_dir>/<key>-g<group>.cubin. */
 int lx_game_create(const char *source, const char *name, const char *include_dir,
                    const char *cache_dir, lx_game **out);
+/* Make device `ordinal`'s primary context current on the calling thread
+   (for C callers that do not use the CUDA runtime). */
+int lx_bind_device(int ordinal);
 /* Compile to <cache_dir>/<key>.cubin only (no GPU needed); *key_out gets the
    cache key (>= 65 bytes). */
 int lx_compile_only(const char *source, const char *name, const char *include_dir,
@@ -93,14 +107,26 @@ int lx_init(const lx_game *g, void *state, int64_t B, const uint64_t *seeds, uin
             int64_t first_index, void *stream);
 
 /* CompiledGame.legal_mask / legal_counts (compiler.py:394-428):
-   mask (B, A) uint8 or NULL, counts (B,) int64 or NULL. */
-int lx_legal(const lx_game *g, const void *state, int64_t B, uint8_t *mask, int64_t *counts,
-             void *stream);
+   mask (B, A) uint8 or NULL, counts (B,) int64 or NULL; mover (B,) int8 or
+   NULL: legality for that player instead of each row's current player (the
+   reference's `mover=` argument), in the row's own phase. */
+int lx_legal(const lx_game *g, const void *state, int64_t B, const int8_t *mover, uint8_t *mask,
+             int64_t *counts, void *stream);
 
 /* CompiledGame.sample_actions (compiler.py:430-446): u (B,) float64 draws, or
-   NULL to draw uniform(seed, move_count) on device (engine.random_actions). */
-int lx_sample(const lx_game *g, const void *state, int64_t B, const double *u,
+   NULL to draw uniform(seed, move_count) on device (engine.random_actions);
+   mover as in lx_legal. */
+int lx_sample(const lx_game *g, const void *state, int64_t B, const int8_t *mover, const double *u,
               int64_t *actions, void *stream);
+
+/* Mark rows (B,) uint8 (NULL = all) that are still live terminated +
+   truncated draws in place (engine.playout_random's cap, engine.py:156-160;
+   agents.py:430-435). */
+int lx_truncate(const lx_game *g, void *state, int64_t B, const uint8_t *rows, void *stream);
+
+/* Replace every row's RNG seed with seeds (B,) uint64 (device) in place
+   (the MCTS rollout re-keying, agents.py:229-233). */
+int lx_set_seeds(const lx_game *g, void *state, int64_t B, const uint64_t *seeds, void *stream);
 
 /* CompiledGame.step_into (compiler.py:456-580), in place on rows (B,) uint8
    (NULL = all) & ~terminated.  verify != 0 checks every live row first and
@@ -157,17 +183,38 @@ int lx_rollout(const lx_game *g, void *state, int64_t B, int max_turns, int mode
                int8_t *outcomes, int32_t *turns, int check, int64_t *stuck_row, void *stream);
 
 /* PGX-style environment step (LudaxEnvironment.step; BASELINE north star),
-   one launch: apply actions (B,) int64 to live rows (NULL = refresh outputs
-   only), rewards (B, 2) float32 for the terminating ply from the outcome
-   (engine.py:79-87), truncate at max_turns (> 0), auto_reset finished rows
-   with seeds hash_key(seed, 0xE9) (engine.py:58-65), then write the next
-   state's legal mask (B, A) uint8, terminated / truncated (B,) uint8 and
-   current player (B,) int32.  Any output may be NULL. */
-int lx_env_step(const lx_game *g, void *state, int64_t B, const int64_t *actions, int max_turns,
-                int auto_reset, uint8_t *mask, float *rewards, uint8_t *terminated,
-                uint8_t *truncated, int32_t *player, void *stream);
+   one launch per ply.  flags (LX_ENV_*):
+     STEP       apply one ply to live rows (else only refresh the outputs)
+     RANDOM     sample a uniform legal action per live row from its own
+                (seed, move_count) stream in the kernel (engine.random_actions,
+                engine.py:72-75); written to `actions` when non-NULL.  Without
+                RANDOM, actions (B,) int64 are read.
+     AUTO_RESET re-initialise finished rows with seed hash_key(seed, 0xE9)
+                (engine.reset_rows, engine.py:58-65); the terminating ply's
+                terminated / truncated / rewards are still reported
+     MASK_BITS  mask is (B, ceil(A/32)) uint32 bit rows (action a = bit a%32
+                of word a/32) instead of (B, A) uint8
+   rewards (B, 2) float32: the terminating ply's outcome (engine.py:79-87),
+   0 otherwise; games reaching max_turns (> 0) end as truncated draws.  An
+   illegal given action (engine.step -> IllegalAction, mechanics.py:503-510)
+   is not applied: the row terminates with the PGX penalty (mover -1,
+   opponent +1, outcome = opponent win); a RANDOM row with no legal action
+   and no pass (EmptyMask, engine.py:142-147) ends as a truncated draw.
+   Either way *bad_row (device int64, or NULL) receives the lowest such row,
+   -1 when none.  Then the next state's legal mask, terminated / truncated
+   (B,) uint8 and current player (B,) int32 are written.  Any output may be
+   NULL. */
+#define LX_ENV_AUTO_RESET 1
+#define LX_ENV_RANDOM 2
+#define LX_ENV_MASK_BITS 4
+#define LX_ENV_STEP 8
+int lx_env_step(const lx_game *g, void *state, int64_t B, int64_t *actions, int max_turns,
+                int flags, void *mask, float *rewards, uint8_t *terminated, uint8_t *truncated,
+                int32_t *player, int64_t *bad_row, void *stream);
 
-/* device state <-> reference GameState arrays (device pointers) */
+/* device state <-> reference GameState arrays (device pointers).  Export:
+   board_owner / board_piece may both be NULL (scalar fields only); any
+   other field NULL is skipped. */
 int lx_export(const lx_game *g, const void *state, int64_t B, const lx_ref_state *ref,
               void *stream);
 int lx_import(const lx_game *g, void *state, int64_t B, const lx_ref_state *ref, void *stream);

@@ -11,7 +11,8 @@
 //   [0, W)        P1 stones        [W, 2W)       P2 stones
 //   [2W, 2W+NX)   piece-type planes (games with several piece types), then
 //                 rule-private words (e.g. edge-connected stone sets)
-//   then 8 meta words (see pack/unpack in lx_rules.cuh), zero padding to NQ*4.
+//   then the seed, scores and packed meta bit fields (lx::Layout in
+//   lx_rules.cuh), zero padding to NQ*4.
 #pragma once
 
 #include "lx_rules.cuh"
@@ -49,16 +50,13 @@ __device__ __forceinline__ i64 gtid() { return (i64)blockIdx.x * blockDim.x + th
 // 4 mask bits -> 4 bytes of 0/1
 __device__ __forceinline__ u32 spread4(u32 x) { return ((x & 0xfu) * 0x00204081u) & 0x01010101u; }
 
-// Warp-cooperative write of the (B, A) uint8 legal mask for the warp's 32
-// consecutive envs: each lane stages its row as a bit vector (cells, then the
-// pass column) in shared memory; the warp's rows form one contiguous block of
-// 32*A bytes in global memory, written with coalesced 16-byte stores.  Every
-// lane of the warp must call it (rows >= B pass valid = false).
+// Stage the lane's legal-mask row as a bit vector in cell order (cells, then
+// the pass column) in a per-warp shared-memory block of 32 rows x STRIDE
+// words; returns the block.  Every lane of the warp must call it.
 template <class G>
-__device__ __forceinline__ void write_mask_rows(unsigned char* __restrict__ mask, i64 B, i64 i,
-                                                bool valid, const BB<G::W>& legal,
-                                                bool pass_bit) {
-    constexpr int A = G::A, NW = (G::A + 31) / 32, STRIDE = NW + 1;
+__device__ __forceinline__ const u32* stage_mask_rows(bool valid, const BB<G::W>& legal,
+                                                      bool pass_bit) {
+    constexpr int NW = (G::A + 31) / 32, STRIDE = NW + 1;
     __shared__ u32 stage[(256 / 32) * 32 * STRIDE];
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     u32* mine = stage + (warp * 32 + lane) * STRIDE;
@@ -79,12 +77,26 @@ __device__ __forceinline__ void write_mask_rows(unsigned char* __restrict__ mask
     }
     mine[NW] = 0u;
     __syncwarp();
+    return stage + warp * 32 * STRIDE;
+}
+
+// Warp-cooperative write of the (B, A) uint8 legal mask for the warp's 32
+// consecutive envs: the rows staged as bit vectors (stage_mask_rows) form
+// one contiguous block of 32*A bytes in global memory, written with
+// coalesced 16-byte stores.  Every lane of the warp must call it (rows >= B
+// pass valid = false).
+template <class G>
+__device__ __forceinline__ void write_mask_rows(unsigned char* __restrict__ mask, i64 B, i64 i,
+                                                bool valid, const BB<G::W>& legal,
+                                                bool pass_bit) {
+    constexpr int A = G::A, NW = (G::A + 31) / 32, STRIDE = NW + 1;
+    const u32* rows = stage_mask_rows<G>(valid, legal, pass_bit);
+    const unsigned lane = threadIdx.x & 31u;
     const i64 i0 = i - lane;
     const i64 left = B - i0;
     const int nrows = left < 32 ? (int)left : 32;
     const int bytes = nrows * A;
     unsigned char* base = mask + i0 * (i64)A;
-    const u32* rows = stage + warp * 32 * STRIDE;
     for (int p0 = (int)lane * 16; p0 < bytes; p0 += 32 * 16) {
         const int nb = bytes - p0 < 16 ? bytes - p0 : 16;
         u32 v = 0u;
@@ -106,6 +118,23 @@ __device__ __forceinline__ void write_mask_rows(unsigned char* __restrict__ mask
             for (int j = 0; j < nb; j++) base[p0 + j] = (v >> j) & 1u;
         }
     }
+    __syncwarp();
+}
+
+// Bit-packed legal mask: (B, NW) u32 rows, action a = bit a%32 of word a/32
+// (NW = ceil(A/32)).  The warp's 32 rows are one contiguous block of 32*NW
+// words, copied from the staged rows with coalesced 4-byte stores.
+template <class G>
+__device__ __forceinline__ void write_mask_bits(u32* __restrict__ mask, i64 B, i64 i, bool valid,
+                                                const BB<G::W>& legal, bool pass_bit) {
+    constexpr int NW = (G::A + 31) / 32, STRIDE = NW + 1;
+    const u32* rows = stage_mask_rows<G>(valid, legal, pass_bit);
+    const unsigned lane = threadIdx.x & 31u;
+    const i64 i0 = i - lane;
+    const i64 left = B - i0;
+    const int nrows = left < 32 ? (int)left : 32;
+    u32* base = mask + i0 * (i64)NW;
+    for (int k = (int)lane; k < nrows * NW; k += 32) base[k] = rows[(k / NW) * STRIDE + k % NW];
     __syncwarp();
 }
 
@@ -132,6 +161,28 @@ __device__ __forceinline__ void write_mask_moves(unsigned char* __restrict__ mas
         unsigned char* row = mask + i * (i64)A;
         if (live) G::enum_moves(s, [&](int a) { row[a] = 1; });
         if (G::PASS >= 0 && pass_bit) row[G::PASS] = 1;
+    }
+    __syncwarp();
+}
+
+// Bit-packed movement / gridworld masks: the warp zeroes its 32 contiguous
+// rows of NW words, then each lane sets the bits of its own legal actions.
+template <class G>
+__device__ __forceinline__ void write_mask_moves_bits(u32* __restrict__ mask, i64 B, i64 i,
+                                                      bool valid, const typename G::St& s,
+                                                      bool live, bool pass_bit) {
+    constexpr int NW = (G::A + 31) / 32;
+    const unsigned lane = threadIdx.x & 31u;
+    const i64 i0 = i - lane;
+    const i64 left = B - i0;
+    const int nrows = left < 32 ? (int)left : 32;
+    u32* base = mask + i0 * (i64)NW;
+    for (int k = (int)lane; k < nrows * NW; k += 32) base[k] = 0u;
+    __syncwarp();
+    if (valid) {
+        u32* row = mask + i * (i64)NW;
+        if (live) G::enum_moves(s, [&](int a) { row[a >> 5] |= 1u << (a & 31); });
+        if (G::PASS >= 0 && pass_bit) row[G::PASS >> 5] |= 1u << (G::PASS & 31);
     }
     __syncwarp();
 }
@@ -188,10 +239,45 @@ extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const 
 }
 #endif
 
+// Static facts of the game and of its device state layout, read by the
+// native runtime at lx_game_create (lx_game_info, include/ludax_b200.h).
+#if LX_IN_GROUP(0)
+extern "C" __constant__ int lx_facts[8] = {
+    Game::C, Game::A, Game::PASS, Game::W, lx::Layout<Game>::NQ, Game::NX, Game::MECH,
+    lx::Layout<Game>::NWORDS};
+
+// mark rows (uint8 (B,), null = all) that are still live terminated +
+// truncated with a draw outcome (engine.playout_random's cap, engine.py:156-160;
+// the MCTS stuck / cap handling, agents.py:430-435)
+extern "C" __global__ void __launch_bounds__(256) lx_truncate(u32* st, i64 B,
+                                                              const unsigned char* rows) {
+    const i64 i = lx::gtid();
+    if (i >= B || (rows && !rows[i])) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    if (s.term) return;
+    s.term = 1; s.trunc = 1; s.outcome = 0;
+    lx::store_state<Game>(s, st, B, i);
+}
+
+// replace every row's RNG seed (the MCTS rollout re-keying, agents.py:229-233)
+extern "C" __global__ void __launch_bounds__(256) lx_set_seeds(u32* st, i64 B, const u64* seeds) {
+    const i64 i = lx::gtid();
+    if (i >= B) return;
+    Game::St s;
+    lx::load_state<Game>(s, st, B, i);
+    s.seed = seeds[i];
+    lx::store_state<Game>(s, st, B, i);
+}
+#endif
+
 // (B, A) uint8 mask (null to skip) and (B,) int64 counts (null to skip);
-// terminated rows are all-false / zero (reference compiler.py:394-428)
+// terminated rows are all-false / zero (reference compiler.py:394-428).
+// mover (B,) int8 or null: legality for that player instead of the row's
+// current player, in the row's phase (the reference's `mover=` argument).
 #if LX_IN_GROUP(1)
 extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
+                                                           const signed char* mover,
                                                            unsigned char* mask, i64* counts) {
     const i64 i = lx::gtid();
     if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
@@ -202,6 +288,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
         if (valid) {
             Game::St s;
             lx::load_state<Game>(s, st, B, i);
+            if (mover) s.cur = mover[i];
             if (!s.term) legal = Game::legal(s);
             const int n = lx::popc(legal);
             pass_only = !s.term && n == 0 && Game::force_pass(s.phase);
@@ -213,6 +300,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
         bool live = false;
         if (valid) {
             lx::load_state<Game>(s, st, B, i);
+            if (mover) s.cur = mover[i];
             live = !s.term;
             const int n = live ? lx::legal_count<Game>(s) : 0;
             pass_only = live && n == 0 && Game::force_pass(s.phase);
@@ -223,14 +311,17 @@ extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
 }
 #endif
 
-// sampled action per row from u (when given) or from the row's own stream
+// sampled action per row from u (when given) or from the row's own stream;
+// mover as in lx_legal
 #if LX_IN_GROUP(1)
 extern "C" __global__ void __launch_bounds__(256) lx_sample(const u32* st, i64 B,
+                                                            const signed char* mover,
                                                             const double* u, i64* actions) {
     const i64 i = lx::gtid();
     if (i >= B) return;
     Game::St s;
     lx::load_state<Game>(s, st, B, i);
+    if (mover) s.cur = mover[i];
     if (s.term) { actions[i] = -1; return; }
     if (!u) { actions[i] = lx::sample_action<Game>(s, lx::seed_mix(s.seed)); return; }
     if constexpr (Game::MECH == 0) {
@@ -764,20 +855,35 @@ extern "C" __global__ void __launch_bounds__(128) lx_expand(u32* pool, i64 cap, 
 }
 #endif
 
-// PGX-style environment step (env.LudaxEnvironment.step), one launch per ply:
-// apply actions[i] to live rows (actions == null: no move, just refresh the
-// outputs), reward the terminating ply from the outcome (reference
-// engine.py:79-87: P1 win [+1,-1], P2 win [-1,+1], draw [0,0]), truncate at
-// max_turns (> 0), optionally auto-reset finished rows with seed
-// hash_key(seed, 0xE9) (engine.reset_rows, engine.py:58-65), and write the
-// legal mask / flags / player of the resulting state.
+// PGX-style environment step (env.LudaxEnvironment.step), one launch per ply.
+// flags: LX_ENV_STEP apply one ply to live rows (else only refresh outputs);
+// LX_ENV_RANDOM sample a uniform legal action in the kernel from the row's
+// own stream (engine.random_actions; written to `actions` when non-null)
+// instead of reading `actions`; LX_ENV_AUTO_RESET re-initialise finished
+// rows with seed hash_key(seed, 0xE9) (engine.reset_rows, engine.py:58-65);
+// LX_ENV_MASK_BITS write the mask as (B, ceil(A/32)) u32 bit rows instead of
+// (B, A) uint8.  Rewards of the terminating ply follow the outcome (reference
+// engine.py:79-87: P1 win [+1,-1], P2 win [-1,+1], draw [0,0]); games that
+// reach max_turns (> 0) are truncated draws.  With auto-reset the
+// terminating ply's terminated / truncated / rewards are reported while the
+// stored state, mask and player are the reset env's (PGX auto_reset).  An
+// illegal given action (reference engine.step raises IllegalAction,
+// mechanics.py:503-510) is not applied: the row ends with the PGX
+// illegal-action penalty (mover -1, opponent +1, outcome = opponent win) and
+// *bad receives the lowest such row; a random row with no legal action and
+// no pass (EmptyMask, engine.py:142-147) ends as a truncated draw and is
+// reported the same way.
+#define LX_ENV_AUTO_RESET 1
+#define LX_ENV_RANDOM 2
+#define LX_ENV_MASK_BITS 4
+#define LX_ENV_STEP 8
 #if LX_IN_GROUP(4)
-extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, const i64* actions,
-                                                              int max_turns, int auto_reset,
-                                                              unsigned char* mask, float* rewards,
+extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, i64* actions,
+                                                              int max_turns, int flags,
+                                                              void* mask, float* rewards,
                                                               unsigned char* terminated,
                                                               unsigned char* truncated,
-                                                              int* player) {
+                                                              int* player, u64* bad) {
     const i64 i = lx::gtid();
     if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
     const bool valid = i < B;
@@ -786,25 +892,50 @@ extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, co
     Game::St s;
     if (valid) {
         lx::load_state<Game>(s, st, B, i);
-        const bool was = s.term;
         float r0 = 0.f, r1 = 0.f;
-        if (!was && actions) {
-            lx::apply_step<Game>(s, (int)actions[i]);
-            if (s.term) {
-                r0 = s.outcome == 1 ? 1.f : (s.outcome == 2 ? -1.f : 0.f);
-                r1 = -r0;
-            } else if (max_turns > 0 && (int)s.mc >= max_turns) {
-                s.term = 1; s.trunc = 1; s.outcome = 0;
+        bool out_term = s.term, out_trunc = s.trunc;
+        if ((flags & LX_ENV_STEP) && !s.term) {
+            int a, hint = -1;
+            bool ok;
+            if (flags & LX_ENV_RANDOM) {
+                a = lx::sample_action<Game>(s, lx::seed_mix(s.seed), hint);
+                if (actions) actions[i] = a;
+                ok = a >= 0;
+            } else {
+                const i64 a64 = actions[i];
+                ok = lx::action_legal<Game>(s, a64);
+                a = (int)a64;
             }
+            if (ok) {
+                lx::apply_step<Game>(s, a, hint);
+                if (s.term) {
+                    r0 = s.outcome == 1 ? 1.f : (s.outcome == 2 ? -1.f : 0.f);
+                    r1 = -r0;
+                } else if (max_turns > 0 && (int)s.mc >= max_turns) {
+                    s.term = 1; s.trunc = 1; s.outcome = 0;
+                }
+            } else {
+                if (bad) atomicMin(bad, (u64)i);
+                s.term = 1;
+                if (flags & LX_ENV_RANDOM) {           // stuck: truncated draw
+                    s.trunc = 1; s.outcome = 0;
+                } else {                               // illegal: the mover loses
+                    s.outcome = 2 - s.cur;
+                    r0 = s.cur ? 1.f : -1.f;
+                    r1 = -r0;
+                }
+            }
+            out_term = s.term;
+            out_trunc = s.trunc;
+            if ((flags & LX_ENV_AUTO_RESET) && s.term) {
+                const u64 seed = lx::mix64(lx::seed_mix(s.seed) ^ 0xE9ull);
+                lx::init_state<Game>(s, seed);
+            }
+            lx::store_state<Game>(s, st, B, i);
         }
-        if (auto_reset && s.term && actions) {
-            const u64 seed = lx::mix64(lx::seed_mix(s.seed) ^ 0xE9ull);
-            lx::init_state<Game>(s, seed);
-        }
-        if (actions) lx::store_state<Game>(s, st, B, i);
         if (rewards) reinterpret_cast<float2*>(rewards)[i] = make_float2(r0, r1);
-        if (terminated) terminated[i] = (unsigned char)s.term;
-        if (truncated) truncated[i] = (unsigned char)s.trunc;
+        if (terminated) terminated[i] = (unsigned char)out_term;
+        if (truncated) truncated[i] = (unsigned char)out_trunc;
         if (player) player[i] = s.cur;
         live = !s.term;
         if constexpr (Game::MECH == 0) {
@@ -815,8 +946,17 @@ extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, co
         }
     }
     if (mask) {
-        if constexpr (Game::MECH == 0) lx::write_mask_rows<Game>(mask, B, i, valid, legal, pass_only);
-        else lx::write_mask_moves<Game>(mask, B, i, valid, s, live, pass_only);
+        if (flags & LX_ENV_MASK_BITS) {
+            if constexpr (Game::MECH == 0)
+                lx::write_mask_bits<Game>((u32*)mask, B, i, valid, legal, pass_only);
+            else
+                lx::write_mask_moves_bits<Game>((u32*)mask, B, i, valid, s, live, pass_only);
+        } else {
+            if constexpr (Game::MECH == 0)
+                lx::write_mask_rows<Game>((unsigned char*)mask, B, i, valid, legal, pass_only);
+            else
+                lx::write_mask_moves<Game>((unsigned char*)mask, B, i, valid, s, live, pass_only);
+        }
     }
 }
 #endif
@@ -828,20 +968,22 @@ extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B
     if (i >= B) return;
     Game::St s;
     lx::load_state<Game>(s, st, B, i);
-    signed char* own = p.board_owner + i * Game::C;
-    signed char* pc = p.board_piece + i * Game::C;
-    for (int c = 0; c < Game::C; c++) {
-        const int cb = Game::cell_bit(c);
-        const bool a = lx::test(s.own0, cb), b = lx::test(s.own1, cb);
-        own[c] = a ? 0 : (b ? 1 : -1);
-        pc[c] = (a || b) ? (signed char)Game::piece_at(s, cb) : (signed char)-1;
+    if (p.board_owner) {                       // null: scalar fields only (B200Game.meta)
+        signed char* own = p.board_owner + i * Game::C;
+        signed char* pc = p.board_piece + i * Game::C;
+        for (int c = 0; c < Game::C; c++) {
+            const int cb = Game::cell_bit(c);
+            const bool a = lx::test(s.own0, cb), b = lx::test(s.own1, cb);
+            own[c] = a ? 0 : (b ? 1 : -1);
+            pc[c] = (a || b) ? (signed char)Game::piece_at(s, cb) : (signed char)-1;
+        }
     }
-    p.current_player[i] = (signed char)s.cur;
-    p.move_count[i] = (int)s.mc;
-    p.terminated[i] = (unsigned char)s.term;
-    p.truncated[i] = (unsigned char)s.trunc;
-    p.outcome[i] = (signed char)s.outcome;
-    p.seeds[i] = s.seed;
+    if (p.current_player) p.current_player[i] = (signed char)s.cur;
+    if (p.move_count) p.move_count[i] = (int)s.mc;
+    if (p.terminated) p.terminated[i] = (unsigned char)s.term;
+    if (p.truncated) p.truncated[i] = (unsigned char)s.trunc;
+    if (p.outcome) p.outcome[i] = (signed char)s.outcome;
+    if (p.seeds) p.seeds[i] = s.seed;
     if (p.scores) { p.scores[2 * i] = s.sc0; p.scores[2 * i + 1] = s.sc1; }
     if (p.pass_streak) {
         p.pass_streak[i] = (short)s.pass_streak;

@@ -11,42 +11,104 @@
 
 namespace lx {
 
+// HBM word layout of one env (compact, per game): the boards and private
+// words, the 64-bit seed, the two int32 scores when the game keeps scores,
+// then bit fields holding only the meta the game's rules and the reference
+// StateLayout need (state.py:34-66): move_count (32 bits), current player,
+// terminated, truncated, outcome (+1), then, when present, phase, turn
+// position, pass streak (int16) + pass flags, the last action (mover +1,
+// kind +1, dest / per-player dests / source as cell index + 1) and
+// must_move (cell + 1).  Connect Four packs into 32 B (NQ = 2) instead of 48.
+__host__ __device__ constexpr int bitlen(int v) { return v <= 0 ? 0 : 1 + bitlen(v >> 1); }
+
 template <class G>
 struct Layout {
     static constexpr int W = G::W, NX = G::NX;
-    static constexpr int META = 2 * W + NX;
-    static constexpr int NWORDS = META + 8;
+    static constexpr int SEED = 2 * W + NX;                      // seed lo, hi
+    static constexpr int SCORE = SEED + 2;                       // sc0, sc1 (int32)
+    static constexpr int CB = bitlen(G::C);                      // cell index + 1
+    static constexpr int O_MC = 32 * (SCORE + (G::L_SCORES ? 2 : 0));
+    static constexpr int O_CUR = O_MC + 32;
+    static constexpr int O_TERM = O_CUR + 1, O_TRUNC = O_TERM + 1, O_OUT = O_TRUNC + 1;
+    static constexpr int B_PHASE = G::L_PHASE ? bitlen(G::NPHASE) : 0;
+    static constexpr int O_PHASE = O_OUT + 2;
+    static constexpr int B_POS = G::L_TURNPOS ? 5 : 0;
+    static constexpr int O_POS = O_PHASE + B_PHASE;
+    static constexpr int B_PASS = G::L_PASSING ? 16 : 0;
+    static constexpr int O_PASS = O_POS + B_POS;
+    static constexpr int O_PF = O_PASS + B_PASS;                 // pf0, pf1
+    static constexpr int B_LAST = G::L_LAST ? CB : 0;
+    static constexpr int O_LM = O_PF + (G::L_PASSING ? 2 : 0);   // last_mover + 1 (2 bits)
+    static constexpr int O_LK = O_LM + (G::L_LAST ? 2 : 0);      // last_kind + 1 (3 bits)
+    static constexpr int O_LD = O_LK + (G::L_LAST ? 3 : 0);      // last_dest + 1
+    static constexpr int O_L0 = O_LD + B_LAST;                   // ldbp0 + 1
+    static constexpr int O_L1 = O_L0 + B_LAST;                   // ldbp1 + 1
+    static constexpr int B_SRC = (G::L_LAST && G::MECH != 0) ? CB : 0;
+    static constexpr int O_SRC = O_L1 + B_LAST;                  // last_source + 1
+    static constexpr int B_MUST = G::L_MUSTMOVE ? CB : 0;
+    static constexpr int O_MUST = O_SRC + B_SRC;                 // must_move + 1
+    static constexpr int END = O_MUST + B_MUST;
+    static constexpr int NWORDS = (END + 31) / 32;
     static constexpr int NQ = (NWORDS + 3) / 4;
 };
 
+// bit field [OFF, OFF + BITS) of a word array (BITS <= 32)
+template <int OFF, int BITS>
+__device__ __forceinline__ u32 getf(const u32* w) {
+    constexpr int wi = OFF >> 5, sh = OFF & 31;
+    constexpr u32 mask = BITS >= 32 ? 0xffffffffu : ((1u << BITS) - 1u);
+    if constexpr (BITS == 0) {
+        return 0u;
+    } else if constexpr (sh + BITS <= 32) {
+        return (w[wi] >> sh) & mask;
+    } else {
+        return ((w[wi] >> sh) | (w[wi + 1] << (32 - sh))) & mask;
+    }
+}
+// OR v into the field (the word array starts zeroed)
+template <int OFF, int BITS>
+__device__ __forceinline__ void putf(u32* w, u32 v) {
+    constexpr int wi = OFF >> 5, sh = OFF & 31;
+    constexpr u32 mask = BITS >= 32 ? 0xffffffffu : ((1u << BITS) - 1u);
+    if constexpr (BITS > 0) {
+        v &= mask;
+        w[wi] |= v << sh;
+        if constexpr (sh + BITS > 32) w[wi + 1] |= v >> (32 - sh);
+    }
+}
+
 template <class G>
 __device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<G>::NQ * 4]) {
-    constexpr int W = G::W, M = Layout<G>::META;
+    typedef Layout<G> L;
+    constexpr int W = G::W;
 #pragma unroll
     for (int i = 0; i < W; i++) { s.own0.w[i] = w[i]; s.own1.w[i] = w[W + i]; }
 #pragma unroll
     for (int i = 0; i < G::NX; i++) s.ext[i] = w[2 * W + i];
-    s.mc = w[M];
-    const u32 f = w[M + 1];
-    s.cur = f & 1u;
-    s.term = (f >> 1) & 1u;
-    s.trunc = (f >> 2) & 1u;
-    s.outcome = (int)((f >> 3) & 3u) - 1;
-    s.phase = (f >> 5) & 7u;
-    s.last_mover = (int)((f >> 8) & 3u) - 1;
-    s.pf0 = (f >> 10) & 1u;
-    s.pf1 = (f >> 11) & 1u;
-    s.last_kind = (int)((f >> 12) & 7u) - 1;
-    s.pos = (f >> 15) & 31u;
-    s.last_dest = (short)(w[M + 2] & 0xffffu);
-    s.pass_streak = (short)(w[M + 2] >> 16);
-    s.ldbp0 = (short)(w[M + 3] & 0xffffu);
-    s.ldbp1 = (short)(w[M + 3] >> 16);
-    s.sc0 = (short)(w[M + 4] & 0xffffu);
-    s.sc1 = (short)(w[M + 4] >> 16);
-    s.seed = (u64)w[M + 5] | ((u64)w[M + 6] << 32);
-    s.last_source = (short)(w[M + 7] & 0xffffu);
-    s.must_move = (short)(w[M + 7] >> 16);
+    s.seed = (u64)w[L::SEED] | ((u64)w[L::SEED + 1] << 32);
+    s.sc0 = G::L_SCORES ? (int)w[L::SCORE] : 0;
+    s.sc1 = G::L_SCORES ? (int)w[L::SCORE + 1] : 0;
+    s.mc = getf<L::O_MC, 32>(w);
+    s.cur = (int)getf<L::O_CUR, 1>(w);
+    s.term = (int)getf<L::O_TERM, 1>(w);
+    s.trunc = (int)getf<L::O_TRUNC, 1>(w);
+    s.outcome = (int)getf<L::O_OUT, 2>(w) - 1;
+    s.phase = (int)getf<L::O_PHASE, L::B_PHASE>(w);
+    s.pos = (int)getf<L::O_POS, L::B_POS>(w);
+    s.pass_streak = G::L_PASSING ? (int)(short)getf<L::O_PASS, 16>(w) : 0;
+    s.pf0 = G::L_PASSING ? (int)getf<L::O_PF, 1>(w) : 0;
+    s.pf1 = G::L_PASSING ? (int)getf<L::O_PF + 1, 1>(w) : 0;
+    if (G::L_LAST) {
+        s.last_mover = (int)getf<L::O_LM, 2>(w) - 1;
+        s.last_kind = (int)getf<L::O_LK, 3>(w) - 1;
+        s.last_dest = (int)getf<L::O_LD, L::B_LAST>(w) - 1;
+        s.ldbp0 = (int)getf<L::O_L0, L::B_LAST>(w) - 1;
+        s.ldbp1 = (int)getf<L::O_L1, L::B_LAST>(w) - 1;
+    } else {
+        s.last_mover = -1; s.last_kind = -1; s.last_dest = -1; s.ldbp0 = -1; s.ldbp1 = -1;
+    }
+    s.last_source = L::B_SRC ? (int)getf<L::O_SRC, L::B_SRC>(w) - 1 : -1;
+    s.must_move = L::B_MUST ? (int)getf<L::O_MUST, L::B_MUST>(w) - 1 : -1;
     s.ovr = -1;
     s.samep = 0;
     s.ncached = 0;
@@ -54,24 +116,38 @@ __device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<
 
 template <class G>
 __device__ __forceinline__ void pack(const typename G::St& s, u32 (&w)[Layout<G>::NQ * 4]) {
-    constexpr int W = G::W, M = Layout<G>::META;
+    typedef Layout<G> L;
+    constexpr int W = G::W;
+#pragma unroll
+    for (int i = 2 * W + G::NX; i < L::NQ * 4; i++) w[i] = 0u;
 #pragma unroll
     for (int i = 0; i < W; i++) { w[i] = s.own0.w[i]; w[W + i] = s.own1.w[i]; }
 #pragma unroll
     for (int i = 0; i < G::NX; i++) w[2 * W + i] = s.ext[i];
-    w[M] = s.mc;
-    w[M + 1] = (u32)s.cur | ((u32)s.term << 1) | ((u32)s.trunc << 2) |
-               ((u32)(s.outcome + 1) << 3) | ((u32)s.phase << 5) |
-               ((u32)(s.last_mover + 1) << 8) | ((u32)s.pf0 << 10) | ((u32)s.pf1 << 11) |
-               ((u32)(s.last_kind + 1) << 12) | ((u32)s.pos << 15);
-    w[M + 2] = ((u32)s.last_dest & 0xffffu) | ((u32)s.pass_streak << 16);
-    w[M + 3] = ((u32)s.ldbp0 & 0xffffu) | ((u32)s.ldbp1 << 16);
-    w[M + 4] = ((u32)s.sc0 & 0xffffu) | ((u32)s.sc1 << 16);
-    w[M + 5] = (u32)s.seed;
-    w[M + 6] = (u32)(s.seed >> 32);
-    w[M + 7] = ((u32)s.last_source & 0xffffu) | ((u32)s.must_move << 16);
-#pragma unroll
-    for (int i = Layout<G>::NWORDS; i < Layout<G>::NQ * 4; i++) w[i] = 0u;
+    w[L::SEED] = (u32)s.seed;
+    w[L::SEED + 1] = (u32)(s.seed >> 32);
+    if (G::L_SCORES) { w[L::SCORE] = (u32)s.sc0; w[L::SCORE + 1] = (u32)s.sc1; }
+    putf<L::O_MC, 32>(w, s.mc);
+    putf<L::O_CUR, 1>(w, (u32)s.cur);
+    putf<L::O_TERM, 1>(w, (u32)s.term);
+    putf<L::O_TRUNC, 1>(w, (u32)s.trunc);
+    putf<L::O_OUT, 2>(w, (u32)(s.outcome + 1));
+    putf<L::O_PHASE, L::B_PHASE>(w, (u32)s.phase);
+    putf<L::O_POS, L::B_POS>(w, (u32)s.pos);
+    if (G::L_PASSING) {
+        putf<L::O_PASS, 16>(w, (u32)s.pass_streak);
+        putf<L::O_PF, 1>(w, (u32)s.pf0);
+        putf<L::O_PF + 1, 1>(w, (u32)s.pf1);
+    }
+    if (G::L_LAST) {
+        putf<L::O_LM, 2>(w, (u32)(s.last_mover + 1));
+        putf<L::O_LK, 3>(w, (u32)(s.last_kind + 1));
+        putf<L::O_LD, L::B_LAST>(w, (u32)(s.last_dest + 1));
+        putf<L::O_L0, L::B_LAST>(w, (u32)(s.ldbp0 + 1));
+        putf<L::O_L1, L::B_LAST>(w, (u32)(s.ldbp1 + 1));
+    }
+    putf<L::O_SRC, L::B_SRC>(w, (u32)(s.last_source + 1));
+    putf<L::O_MUST, L::B_MUST>(w, (u32)(s.must_move + 1));
 }
 
 // start position (reference compiler.py:329-345 _build_template + init)

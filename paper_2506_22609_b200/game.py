@@ -105,26 +105,50 @@ class StateLayout:
 
 
 class DeviceState:
-    """Batch of envs in HBM: int32 words shaped (NQ, B, 4), quad-major."""
+    """Batch of envs in HBM: int32 words shaped (NQ, B, 4), quad-major.
+
+    Reading a reference GameState field (``state.terminated``,
+    ``state.board_owner``, ... state.py:78-130) exports the device words once
+    (lx_export) into a host cache; in-place edits of those arrays -- what the
+    reference's own loops do, e.g. ``state.terminated |= truncate`` and
+    ``state.outcome[rows] = 0`` (engine.py:156-160) -- are written back to the
+    device (lx_import) before the next device call that reads the state, so
+    reference-style code sees value semantics.  Device calls that change the
+    state drop the cache.
+    """
 
     def __init__(self, game, words, batch_size):
         self.game = game
         self.words = words
         self.batch_size = batch_size
         self._host = None
+        self._snap = None
 
     # -- value semantics --
     def copy(self):
+        self.sync()
         return DeviceState(self.game, self.words.clone(), self.batch_size)
 
     def _touch(self):
         self._host = None
+        self._snap = None
+
+    def sync(self):
+        """Write host-side edits of the cached reference fields back to the
+        device (no-op when nothing was read or nothing changed)."""
+        if self._host is None:
+            return
+        if all(np.array_equal(v, self._snap[k]) for k, v in self._host.items()):
+            return
+        self.game._import_into(self, self._host)
+        self._snap = {k: v.copy() for k, v in self._host.items()}
 
     # -- reference field view --
     def host(self):
         """dict of numpy arrays in the reference GameState layout."""
         if self._host is None:
             self._host = self.game._export(self)
+            self._snap = {k: v.copy() for k, v in self._host.items()}
         return self._host
 
     def __getattr__(self, name):
@@ -150,6 +174,7 @@ class DeviceState:
         return self.words.numel() * 4
 
     def rows(self, idx):
+        self.sync()
         idx = np.atleast_1d(np.asarray(idx))
         torch = _torch()
         t = torch.as_tensor(idx, device=self.words.device, dtype=torch.long)
@@ -158,11 +183,15 @@ class DeviceState:
     @classmethod
     def concat(cls, states):
         torch = _torch()
+        for s in states:
+            s.sync()
         w = torch.cat([s.words for s in states], dim=1).contiguous()
         return cls(states[0].game, w, sum(s.batch_size for s in states))
 
     def set_rows(self, idx, other):
         torch = _torch()
+        self.sync()
+        other.sync()
         t = torch.as_tensor(np.atleast_1d(np.asarray(idx)), device=self.words.device,
                             dtype=torch.long)
         self.words[:, t] = other.words
@@ -188,16 +217,24 @@ class B200Game:
                                  lowered.info["pass_index"] >= 0,
                                  tuple(lowered.info["grid_directions"]))
         self.piece_names = tuple(p.name for p in spec.equipment.pieces)
-        self._native = None
+        self._native = {}
         self._nq = lowered.info["nq"]
 
     # -- native handle (lazy: needs the CUDA context) --
     @property
     def native(self):
-        if self._native is None:
-            _torch().cuda.current_device()
-            self._native = native.NativeGame(self.lowered.source, self.name)
-        return self._native
+        """The lx_game handle of the current device (one per device: a handle
+        is bound to the device whose context was current at creation)."""
+        dev = _torch().cuda.current_device()
+        h = self._native.get(dev)
+        if h is None:
+            i = self.lowered.info
+            h = native.NativeGame(self.lowered.source, self.name, expect={
+                "num_cells": i["C"], "num_actions": i["A"], "pass_index": i["pass_index"],
+                "board_words": i["W"], "state_quads": i["nq"], "private_words": i["NX"],
+                "mechanics": i["mechanics"], "device": dev})
+            self._native[dev] = h
+        return h
 
     @property
     def handle(self):
@@ -241,7 +278,24 @@ class B200Game:
                                  "connectivity_plans": self.layout.connectivity,
                                  "phase_index": self.layout.phase,
                                  "turn_position": self.layout.turn_pos},
+                "state_bytes": self.reference_state_bytes(),
                 "device_state_bytes": self._nq * 16}
+
+    def reference_state_bytes(self):
+        """Bytes per env of the reference GameState layout (the reference's
+        describe()["state_bytes"], compiler.py:649): the fields this game's
+        StateLayout materialises (state.py:34-130)."""
+        C, L = self.num_cells, self.layout
+        n = 2 * C + 1 + 4 + 1 + 1 + 1 + 8          # boards, player, mc, term, trunc, outcome, seed
+        n += 8 if L.scores else 0
+        n += 2 + 2 if L.passing else 0
+        n += 2 if L.must_move else 0
+        n += 1 + 1 + 2 + 2 + 4 if L.last_action else 0
+        n += 3 * C if L.transient_masks else 0
+        n += 2 * C * L.connectivity
+        n += 1 if L.phase else 0
+        n += 1 if L.turn_pos else 0
+        return n
 
     # -- allocation --
     def empty_state(self, B):
@@ -263,26 +317,26 @@ class B200Game:
         del torch
         return st
 
-    # -- per-row scalars straight from the state words (no full export) --
-    def _meta_cols(self, state):
-        M = 2 * self.info["W"] + self.info["NX"]
-        w = state.words
-        return M, (lambda k: w[k // 4, :, k % 4])
-
+    # -- per-row scalars (lx_export of the scalar fields only) --
     def meta(self, state):
-        """Host numpy view of current_player, move_count, terminated,
-        truncated, outcome and seeds (one small device->host copy)."""
+        """Host numpy arrays of current_player, move_count, terminated,
+        truncated, outcome and seeds (one export launch, no boards)."""
+        state.sync()
         torch = _torch()
-        M, col = self._meta_cols(state)
-        flat = torch.stack([col(M), col(M + 1), col(M + 5), col(M + 6)], 1).cpu().numpy()
-        flat = flat.view(np.uint32)
-        f = flat[:, 1]
-        return {"move_count": flat[:, 0].astype(np.int32),
-                "current_player": (f & 1).astype(np.int8),
-                "terminated": ((f >> 1) & 1).astype(bool),
-                "truncated": ((f >> 2) & 1).astype(bool),
-                "outcome": (((f >> 3) & 3).astype(np.int8) - 1).astype(np.int8),
-                "seeds": flat[:, 2].astype(np.uint64) | (flat[:, 3].astype(np.uint64) << np.uint64(32))}
+        B = state.batch_size
+        buf = torch.empty(B * 16, dtype=torch.uint8, device="cuda")
+        o = buf.data_ptr()
+        ref = native.RefState(current_player=o, move_count=o + B, terminated=o + 5 * B,
+                              truncated=o + 6 * B, outcome=o + 7 * B, seeds=o + 8 * B)
+        native.check(native.lib().lx_export(self.handle, state.words.data_ptr(), B,
+                                            ctypes.byref(ref), self._stream()))
+        h = buf.cpu().numpy()
+        return {"current_player": h[:B].view(np.int8).copy(),
+                "move_count": h[B:5 * B].view(np.int32).copy(),
+                "terminated": h[5 * B:6 * B].astype(bool),
+                "truncated": h[6 * B:7 * B].astype(bool),
+                "outcome": h[7 * B:8 * B].view(np.int8).copy(),
+                "seeds": h[8 * B:16 * B].view(np.uint64).copy()}
 
     def expand(self, pool_words, cap, parents, actions, children, seeds, max_turns,
                masks=True):
@@ -324,6 +378,7 @@ class B200Game:
         """One MCTS decision per root row on the device (lx_mcts, one thread
         per tree).  Returns (actions int64, ok bool) host arrays; rows with
         ok False exceeded a capacity and must be searched on the host."""
+        roots.sync()
         import math
         torch = _torch()
         n = roots.batch_size
@@ -352,43 +407,59 @@ class B200Game:
         """Mark rows terminated + truncated with a draw outcome in place (the
         reference's stuck / turn-cap handling, engine.py:156-160,
         agents.py:430-435)."""
+        state.sync()
         torch = _torch()
-        M, col = self._meta_cols(state)
-        r = torch.as_tensor(np.ascontiguousarray(rows, dtype=bool), device="cuda")
-        f = col(M + 1)
-        g = (f & ~0x1E) | 0x2 | 0x4 | (1 << 3)          # term, trunc, outcome 0 (stored +1)
-        state.words[(M + 1) // 4, :, (M + 1) % 4] = torch.where(r, g, f)
+        r = torch.as_tensor(np.ascontiguousarray(rows, dtype=np.uint8)).to("cuda")
+        native.check(native.lib().lx_truncate(self.handle, state.words.data_ptr(),
+                                              state.batch_size, r.data_ptr(), self._stream()))
         state._touch()
 
     # -- legality / sampling --
-    def legal_mask_device(self, state):
+    def _mover_tensor(self, mover, state):
+        if mover is None:
+            return None
+        torch = _torch()
+        m = mover if isinstance(mover, torch.Tensor) else torch.as_tensor(
+            np.broadcast_to(np.asarray(mover), (state.batch_size,)).astype(np.int8))
+        return m.to(device="cuda", dtype=torch.int8).reshape(-1).expand(
+            state.batch_size).contiguous()
+
+    def legal_mask_device(self, state, mover=None):
         torch = _torch()
         B = state.batch_size
+        mv = self._mover_tensor(mover, state)
         mask = torch.empty((B, self.codec.size), dtype=torch.uint8, device="cuda")
         native.check(native.lib().lx_legal(self.handle, state.words.data_ptr(), B,
+                                           mv.data_ptr() if mv is not None else None,
                                            mask.data_ptr(), None, self._stream()))
         return mask.view(torch.bool)
 
-    def legal_counts_device(self, state):
+    def legal_counts_device(self, state, mover=None):
         torch = _torch()
         B = state.batch_size
+        mv = self._mover_tensor(mover, state)
         counts = torch.empty(B, dtype=torch.int64, device="cuda")
-        native.check(native.lib().lx_legal(self.handle, state.words.data_ptr(), B, None,
+        native.check(native.lib().lx_legal(self.handle, state.words.data_ptr(), B,
+                                           mv.data_ptr() if mv is not None else None, None,
                                            counts.data_ptr(), self._stream()))
         return counts
 
     def legal_mask(self, state, mover=None):
-        """(B, A) bool numpy; all-false for terminated rows (compiler.py:411-428)."""
-        _no_mover_override(mover, state)
-        return self.legal_mask_device(state).cpu().numpy()
+        """(B, A) bool numpy; all-false for terminated rows (compiler.py:411-428).
+        ``mover``: (B,) player ids (or a scalar) whose legal actions to list
+        instead of each row's current player."""
+        state = _sync(state)
+        return self.legal_mask_device(state, mover).cpu().numpy()
 
     def legal_counts(self, state, mover=None):
-        _no_mover_override(mover, state)
-        return self.legal_counts_device(state).cpu().numpy()
+        """(B,) int64 legal action counts, pass included (compiler.py:394-409)."""
+        state = _sync(state)
+        return self.legal_counts_device(state, mover).cpu().numpy()
 
-    def sample_actions_device(self, state, u=None):
+    def sample_actions_device(self, state, u=None, mover=None):
         torch = _torch()
         B = state.batch_size
+        mv = self._mover_tensor(mover, state)
         out = torch.empty(B, dtype=torch.int64, device="cuda")
         u_t = None
         if u is not None:
@@ -396,14 +467,15 @@ class B200Game:
                 np.ascontiguousarray(u, dtype=np.float64))
             u_t = u_t.to(device="cuda", dtype=torch.float64).contiguous()
         native.check(native.lib().lx_sample(self.handle, state.words.data_ptr(), B,
+                                            mv.data_ptr() if mv is not None else None,
                                             u_t.data_ptr() if u_t is not None else None,
                                             out.data_ptr(), self._stream()))
         return out
 
     def sample_actions(self, state, u, mover=None):
         """Uniform legal action per row from a (B,) float64 draw (compiler.py:430-446)."""
-        _no_mover_override(mover, state)
-        return self.sample_actions_device(state, u).cpu().numpy()
+        state = _sync(state)
+        return self.sample_actions_device(state, u, mover).cpu().numpy()
 
     # -- stepping --
     def step(self, state, actions):
@@ -414,6 +486,7 @@ class B200Game:
 
     def step_into(self, state, actions, rows=None, verify=True):
         """In-place step on rows & ~terminated (compiler.py:456-580)."""
+        state.sync()
         torch = _torch()
         B = state.batch_size
         a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(
@@ -435,6 +508,7 @@ class B200Game:
 
     def random_step(self, state, max_turns=200, record=False):
         """One fused uniform-random ply for live rows; returns actions if record."""
+        state.sync()
         torch = _torch()
         B = state.batch_size
         out = torch.empty(B, dtype=torch.int64, device="cuda") if record else None
@@ -465,6 +539,7 @@ class B200Game:
             if store:
                 state = out if out is not None else self.empty_state(B)
         else:
+            state.sync()
             B = state.batch_size
         if store:
             mode |= 2
@@ -493,20 +568,15 @@ class B200Game:
     def with_seeds(self, state, seeds):
         """Copy of ``state`` whose rows draw from new RNG streams (the MCTS
         rollout re-keying, reference agents.py:229-233)."""
-        torch = _torch()
         out = state.copy()
         s = _u64_tensor(seeds, state.batch_size)
-        m = 2 * self.info["W"] + self.info["NX"] + 5          # seed lo word (lx_kernels.cuh)
-        lo = (s & 0xFFFFFFFF).to(torch.int64)
-        hi = ((s >> 32) & 0xFFFFFFFF).to(torch.int64)
-        lo = torch.where(lo >= 2 ** 31, lo - 2 ** 32, lo).to(torch.int32)
-        hi = torch.where(hi >= 2 ** 31, hi - 2 ** 32, hi).to(torch.int32)
-        out.words[m // 4, :, m % 4] = lo
-        out.words[(m + 1) // 4, :, (m + 1) % 4] = hi
+        native.check(native.lib().lx_set_seeds(self.handle, out.words.data_ptr(),
+                                               state.batch_size, s.data_ptr(), self._stream()))
         return out
 
     # -- observation --
     def observe_device(self, state, player):
+        state.sync()
         torch = _torch()
         B = state.batch_size
         planes = torch.empty((B, self.observation_planes, self.num_cells), dtype=torch.uint8,
@@ -556,6 +626,7 @@ class B200Game:
 
     def export_device(self, state):
         """Device tensors in the reference GameState layout (lx_export)."""
+        state.sync()
         t = self.ref_arrays(state.batch_size, "cuda")
         ref = self._ref_struct(t)
         native.check(native.lib().lx_export(self.handle, state.words.data_ptr(),
@@ -572,10 +643,10 @@ class B200Game:
             out[k] = a
         return out
 
-    def from_reference(self, arrays):
-        """DeviceState from reference-layout numpy arrays (lx_import)."""
+    def _import_into(self, state, arrays):
+        """Overwrite ``state``'s device words from reference-layout numpy
+        arrays (lx_import; Hex reach sets are rebuilt from the boards)."""
         torch = _torch()
-        B = len(arrays["seeds"])
         t = {}
         for k, v in arrays.items():
             if v is None or k not in native.REF_FIELDS:
@@ -584,17 +655,25 @@ class B200Game:
             if a.dtype == np.uint64:
                 a = a.view(np.int64)
             t[k] = torch.as_tensor(a).to("cuda")
-        st = self.empty_state(B)
+        if int(t["move_count"].max()) >= 2 ** 31 or int(t["move_count"].min()) < 0:
+            raise ValueError("move_count out of range")
         ref = self._ref_struct(t)
-        native.check(native.lib().lx_import(self.handle, st.words.data_ptr(), B,
-                                            ctypes.byref(ref), self._stream()))
+        native.check(native.lib().lx_import(self.handle, state.words.data_ptr(),
+                                            state.batch_size, ctypes.byref(ref), self._stream()))
         torch.cuda.current_stream().synchronize()
+
+    def from_reference(self, arrays):
+        """DeviceState from reference-layout numpy arrays (lx_import)."""
+        st = self.empty_state(len(arrays["seeds"]))
+        self._import_into(st, arrays)
         return st
 
 
-def _no_mover_override(mover, state):
-    if mover is not None:
-        raise NotImplementedError("legality for a non-current mover is not lowered yet")
+def _sync(state):
+    """Write host-side edits of a DeviceState's reference fields back to the
+    device before a device call reads it (see DeviceState)."""
+    state.sync()
+    return state
 
 
 def _u64_tensor(seeds, B):

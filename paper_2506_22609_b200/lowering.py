@@ -1611,11 +1611,12 @@ struct Game {{
 
 #include "lx_kernels.cuh"
 """
+        nwords = state_words(self.W, NX, self.C, L, nph, self.mech_kind)
         src = src.replace("@@CONSTS@@", em.const_defs())
         src = src.replace("@@HELPERS@@", "\n".join(em.helpers.values()))
         info = {"name": spec.name, "C": self.C, "A": self.A, "W": self.W, "NX": NX,
                 "pass_index": self.PASS, "layout": dict(self.layout),
-                "nwords": 2 * self.W + NX + 8, "nq": (2 * self.W + NX + 8 + 3) // 4,
+                "nwords": nwords, "nq": (nwords + 3) // 4,
                 "first_player": int(phases[0].order[0]), "nphase": nph,
                 "observation_planes": 2 * self.NT + 1, "mechanics": self.mech_kind,
                 "codec": {0: "placement", 1: "movement", 2: "gridworld"}[self.mech_kind],
@@ -1714,6 +1715,22 @@ struct Game {{
         if res.kind == "lose":
             return f"(1 + (1 - ({sd})))"
         return f"(1 + ({sd}))"
+
+
+def state_words(W, NX, C, layout, nphase, mech):
+    """32-bit words per env of the device state (mirror of lx::Layout in
+    csrc/device/lx_rules.cuh): boards + private words, seed, int32 scores,
+    then the packed meta bit fields the game keeps."""
+    cb = int(C).bit_length()
+    bits = 32 * (2 * W + NX + 2 + (2 if layout["scores"] else 0))
+    bits += 32 + 1 + 1 + 1 + 2                       # move_count, cur, term, trunc, outcome
+    bits += int(nphase).bit_length() if layout["phase"] else 0
+    bits += 5 if layout["turn_pos"] else 0
+    bits += 18 if layout["passing"] else 0           # pass_streak int16 + two flags
+    if layout["last_action"]:
+        bits += 2 + 3 + 3 * cb + (cb if mech != 0 else 0)
+    bits += cb if layout["must_move"] else 0
+    return (bits + 31) // 32
 
 
 def lower_game(spec):

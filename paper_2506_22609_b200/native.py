@@ -21,10 +21,10 @@ CACHE_DIR = os.path.join(PKG, "csrc", "_cubin")
 
 
 class GameInfo(ctypes.Structure):
-    _fields_ = [("num_cells", ctypes.c_int32), ("num_actions", ctypes.c_int32),
-                ("pass_index", ctypes.c_int32), ("board_words", ctypes.c_int32),
-                ("state_quads", ctypes.c_int32), ("num_sms", ctypes.c_int32),
-                ("rollout_blocks", ctypes.c_int32), ("rollout_threads", ctypes.c_int32)]
+    _fields_ = [(f, ctypes.c_int32) for f in (
+        "num_cells", "num_actions", "pass_index", "board_words", "state_quads", "state_bytes",
+        "private_words", "mechanics", "mask_words", "device", "num_sms", "rollout_blocks",
+        "rollout_threads")]
 
 
 REF_FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
@@ -38,10 +38,10 @@ class RefState(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in REF_FIELDS]
 
 
-EXPORTS = ("lx_version", "lx_last_error", "lx_game_create", "lx_compile_only", "lx_cache_key",
-           "lx_game_info_get", "lx_game_destroy", "lx_init", "lx_legal", "lx_sample",
-           "lx_step", "lx_random_step", "lx_rollout", "lx_export", "lx_import", "lx_observe",
-           "lx_env_step", "lx_expand", "lx_mcts")
+EXPORTS = ("lx_version", "lx_last_error", "lx_game_create", "lx_bind_device", "lx_compile_only",
+           "lx_cache_key", "lx_game_info_get", "lx_game_destroy", "lx_init", "lx_legal",
+           "lx_sample", "lx_truncate", "lx_set_seeds", "lx_step", "lx_random_step", "lx_rollout",
+           "lx_export", "lx_import", "lx_observe", "lx_env_step", "lx_expand", "lx_mcts")
 
 
 def build_native():
@@ -70,8 +70,11 @@ def lib():
     L.lx_cache_key.argtypes = [cs, cs, ctypes.c_char_p]
     L.lx_game_destroy.argtypes = [vp]
     L.lx_init.argtypes = [vp, vp, i64, vp, u64, i64, vp]
-    L.lx_legal.argtypes = [vp, vp, i64, vp, vp, vp]
-    L.lx_sample.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.lx_bind_device.argtypes = [i32]
+    L.lx_legal.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+    L.lx_sample.argtypes = [vp, vp, i64, vp, vp, vp, vp]
+    L.lx_truncate.argtypes = [vp, vp, i64, vp, vp]
+    L.lx_set_seeds.argtypes = [vp, vp, i64, vp, vp]
     L.lx_step.argtypes = [vp, vp, i64, vp, vp, i32, vp, ctypes.POINTER(i64), vp]
     L.lx_random_step.argtypes = [vp, vp, i64, i32, vp, vp]
     L.lx_rollout.argtypes = [vp, vp, i64, i32, i32, u64, vp, i64, vp, vp, vp, vp, i32,
@@ -82,7 +85,7 @@ def lib():
     L.lx_export.argtypes = [vp, vp, i64, ctypes.POINTER(RefState), vp]
     L.lx_import.argtypes = [vp, vp, i64, ctypes.POINTER(RefState), vp]
     L.lx_observe.argtypes = [vp, vp, i64, i32, vp, vp]
-    L.lx_env_step.argtypes = [vp, vp, i64, vp, i32, i32, vp, vp, vp, vp, vp, vp]
+    L.lx_env_step.argtypes = [vp, vp, i64, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("lx_version", "lx_last_error"):
             getattr(L, name).restype = i32
@@ -110,9 +113,10 @@ def cache_key(source):
 
 
 class NativeGame:
-    """Owns one lx_game handle (module loaded on the current CUDA context)."""
+    """Owns one lx_game handle (modules loaded on the current CUDA context,
+    i.e. bound to the current device)."""
 
-    def __init__(self, source, name):
+    def __init__(self, source, name, expect=None):
         h = ctypes.c_void_p()
         os.makedirs(CACHE_DIR, exist_ok=True)
         check(lib().lx_game_create(source.encode(), name.encode(), INCLUDE_DIR.encode(),
@@ -121,6 +125,10 @@ class NativeGame:
         info = GameInfo()
         check(lib().lx_game_info_get(self.h, ctypes.byref(info)))
         self.info = info
+        for k, v in (expect or {}).items():     # the lowering and the device unit agree
+            if getattr(info, k) != v:
+                raise RuntimeError(f"{name}: lx_game_info.{k} = {getattr(info, k)}, "
+                                   f"lowering says {v}")
 
     def __del__(self):
         try:

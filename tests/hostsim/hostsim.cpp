@@ -147,3 +147,11 @@ SIM_API int sim_transcript(uint64_t seed, int n, const int64_t* actions, uint8_t
 }
 
 }
+
+// device state layout facts (lx::Layout), checked against the lowering's
+// info["nwords"/"nq"] by the CPU suite
+extern "C" SIM_API int sim_layout(int *out) {
+    out[0] = lx::Layout<Game>::NWORDS;
+    out[1] = lx::Layout<Game>::NQ;
+    return 0;
+}

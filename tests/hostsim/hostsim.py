@@ -54,6 +54,12 @@ class HostGame:
                                        ctypes.c_void_p]
         self.info = lowered.info
 
+    def layout(self):
+        """(NWORDS, NQ) of the device state layout as lx::Layout computes it."""
+        out = (ctypes.c_int * 2)()
+        self.lib.sim_layout(out)
+        return out[0], out[1]
+
     def playout(self, seeds, max_turns=200, layout_arrays=None):
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
         arrays = layout_arrays(len(seeds))

@@ -31,6 +31,12 @@ def test_hostsim_playouts_equal_oracle(pair):
     assert O.digest(got) == O.digest(want)
 
 
+def test_state_layout_matches_lowering_info(pair):
+    """lx::Layout (device pack/unpack) and the lowering's word count agree."""
+    name, hg, og = pair
+    assert hg.layout() == (hg.info["nwords"], hg.info["nq"]), name
+
+
 def test_hostsim_masks_equal_oracle(pair):
     name, hg, og = pair
     for seed in rng.spawn_seeds(5, 6):

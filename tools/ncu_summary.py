@@ -21,6 +21,9 @@ METRICS = {
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed": "alu_pipe_elapsed_pct",
     "device__attribute_multiprocessor_count": "sms",
     "sm__inst_executed_pipe_fma.sum": "fma_warp_inst",
+    "sm__inst_executed_pipe_alu.sum": "alu_warp_inst_counted",
+    "sm__inst_executed_pipe_alu.avg.peak_sustained": "alu_peak_per_sm_cycle",
+    "sm__cycles_elapsed.avg": "sm_cycles",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
     "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pipe_pct",
@@ -67,13 +70,13 @@ def step_summaries(a):
             info = json.loads(f.read().strip().splitlines()[-1])
         game, B = info["game"], info["batch"]
         out = {"game": game, "batch": B, "cubin_key": info["cubin_key"], "kernels": {}}
-        for k in ("lx_random_step", "lx_sample", "lx_env_step"):
+        for k in ("lx_random_step", "lx_env_step", "lx_env_step_bits"):
             rep = os.path.join(a.src, f"stepprof_{game}_{k}.ncu-rep")
             if not os.path.exists(rep):
                 continue
             m = raw(rep)
             dram = m.get("dram_read", 0) + m.get("dram_write", 0)
-            out["kernels"][k] = {
+            out["kernels"][k.replace("_bits", ":bits")] = {
                 "duration_ns": m["duration_ns"], "dram_read": m.get("dram_read", 0),
                 "dram_write": m.get("dram_write", 0), "dram_bytes_per_env": dram / B,
                 "dram_gbs_under_ncu": dram / m["duration_ns"],
@@ -120,8 +123,11 @@ def main():
         steps = info["env_steps"]
         # ALU pipe: 0.5 warp-inst/clk per SMSP, 4 SMSPs per SM (B300_MICROARCH.md)
         sms = m.get("sms", 148)
-        m["alu_warp_inst"] = (m.get("alu_pipe_elapsed_pct", 0) / 100.0 * 0.5 * 4 * sms
-                              * m["sm_clock_hz"] * m["duration_ns"] / 1e9)
+        if "alu_warp_inst_counted" in m:       # direct count (ncu sm__inst_executed_pipe_alu)
+            m["alu_warp_inst"] = m["alu_warp_inst_counted"]
+        else:                                  # pipe utilisation x ncu's 0.5/clk/SMSP rate
+            m["alu_warp_inst"] = (m.get("alu_pipe_elapsed_pct", 0) / 100.0 * 0.5 * 4 * sms
+                                  * m["sm_clock_hz"] * m["duration_ns"] / 1e9)
         s = {"game": game, "batch": info["batch"], "cubin_key": info["cubin_key"],
              "env_steps_in_launch": steps, **m,
              "warp_inst_per_env_step": m["warp_inst"] / steps,

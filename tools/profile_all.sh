@@ -6,7 +6,8 @@ mkdir -p gpurun_out
 for gb in ${GAMES:-connect_four:4194304 tic_tac_toe:4194304 hex:4194304 reversi:4194304 pente:4194304}; do
   g=${gb%%:*}; b=${gb##*:}
   timeout 300 python tools/ncu_rollout.py --game $g --batch $b > gpurun_out/plain_$g.json 2>&1 &&
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:lx_rollout -s 1 -c 1 \
+  timeout 600 ncu --set full --metrics sm__inst_executed_pipe_alu.sum,sm__inst_executed_pipe_alu.avg.peak_sustained,sm__cycles_elapsed.avg \
+      --clock-control none --import-source on -k regex:lx_rollout -s 1 -c 1 \
       -o gpurun_out/prof_$g python tools/ncu_rollout.py --game $g --batch $b > gpurun_out/ncu_$g.log 2>&1
   echo "$g rc=$?"
   ncu -i gpurun_out/prof_$g.ncu-rep --page source --csv --print-source sass > gpurun_out/sass_$g.csv 2>/dev/null
@@ -21,10 +22,11 @@ fi
 for gb in ${STEP_GAMES:-}; do
   g=${gb%%:*}; b=${gb##*:}
   timeout 300 python tools/ncu_step.py --game $g --batch $b > gpurun_out/step_$g.json 2>&1 || continue
-  for k in lx_random_step lx_sample lx_env_step; do
-    timeout 300 ncu --set full --clock-control none -k regex:"^$k\$" -s 2 -c 1 \
-        -o gpurun_out/stepprof_${g}_$k python tools/ncu_step.py --game $g --batch $b \
-        > gpurun_out/ncu_step_${g}_$k.log 2>&1
-    echo "$g $k rc=$?"
+  for ks in lx_random_step:2:lx_random_step lx_env_step:3:lx_env_step lx_env_step:8:lx_env_step_bits; do
+    k=${ks%%:*}; rest=${ks#*:}; skip=${rest%%:*}; tag=${rest#*:}
+    timeout 300 ncu --set full --clock-control none -k regex:"^$k\$" -s $skip -c 1 \
+        -o gpurun_out/stepprof_${g}_$tag python tools/ncu_step.py --game $g --batch $b \
+        > gpurun_out/ncu_step_${g}_$tag.log 2>&1
+    echo "$g $tag rc=$?"
   done
 done
