@@ -388,7 +388,42 @@ def validate_fixtures(per_corpus=150):
     print("wrote validate.json", len(out), sum(o["report"] == "valid" for o in out), "valid")
 
 
+def mover_fixtures(B=24, plies=(0, 3, 7, 15)):
+    """Legality for a non-current mover (CompiledGame.legal_mask / legal_counts
+    / sample_actions with mover=, compiler.py:394-446) on reference states of
+    every corpus game: the states after k uniform-random plies, the mover
+    flipped (and, for half the rows, kept), the reference's answers."""
+    arrays = {}
+    for name in GAMES:
+        g = boardlang.load_game(open(os.path.join(GAMES_DIR, f"{name}.ldx")).read())
+        st = g.init(batch_size=B, seed=4242)
+        done = 0
+        for k in range(max(plies) + 1):
+            if k in plies:
+                mover = (1 - st.current_player).astype(np.int8)
+                mover[::2] = st.current_player[::2]
+                u = rng.uniform(st.seeds, st.move_count.astype(np.uint64))
+                pre = f"{name}__{k}__"
+                arrays.update({k: v.copy() for k, v in state_arrays(st, pre).items()})
+                arrays[pre + "mover"] = mover
+                arrays[pre + "u"] = u
+                arrays[pre + "mask"] = g.legal_mask(st, mover=mover)
+                arrays[pre + "counts"] = g.legal_counts(st, mover=mover)
+                arrays[pre + "sampled"] = g.sample_actions(st, u, mover=mover)
+                done += 1
+            live = ~st.terminated
+            if not live.any():
+                break
+            acts = engine.random_actions(g, st)
+            g.step_into(st, np.where(acts < 0, 0, acts), rows=live & (acts >= 0), verify=False)
+        print("mover fixtures", name, done)
+    np.savez_compressed(os.path.join(OUT, "mover.npz"), **arrays)
+
+
 if __name__ == "__main__":
+    if "--mover" in sys.argv:
+        mover_fixtures()
+        sys.exit(0)
     if "--fuzz-masks" in sys.argv:
         fuzz_mask_fixtures()
         sys.exit(0)

@@ -187,6 +187,39 @@ __device__ __forceinline__ void write_mask_moves_bits(u32* __restrict__ mask, i6
     __syncwarp();
 }
 
+// Coalesced (B, N)-byte row output for 128-thread blocks (lx_export,
+// lx_observe): each lane fills its row in a per-warp shared-memory stage
+// (pitch NP bytes = an odd number of words, so the 32 lanes' byte stores hit
+// 32 different banks), then the warp writes the 32 rows -- consecutive lanes
+// on consecutive bytes -- to dst + row * stride, so every store instruction
+// covers whole sectors instead of 32 rows C bytes apart.  All lanes call.
+template <int PITCH>
+struct RowStage {
+    static constexpr int NP = (((PITCH + 3) / 4) | 1) * 4;
+    static constexpr int BYTES = 4 * 32 * NP;
+    static __device__ __forceinline__ unsigned char* row() {
+        __shared__ __align__(16) unsigned char buf[BYTES];
+        return buf + ((threadIdx.x >> 5) & 3) * 32 * NP + (threadIdx.x & 31u) * NP;
+    }
+    // the first N (<= PITCH) bytes of the warp's rows [i0, i0 + 32) to dst
+    // (row pitch `stride` bytes)
+    template <int N>
+    static __device__ __forceinline__ void flush(unsigned char* __restrict__ dst, i64 stride,
+                                                 i64 B, i64 i) {
+        __syncwarp();
+        const unsigned lane = threadIdx.x & 31u;
+        const i64 i0 = i - lane;
+        const i64 left = B - i0;
+        const int nrows = left < 32 ? (int)left : 32;
+        const unsigned char* base = row() - lane * NP;
+        for (int q = (int)lane; q < nrows * N; q += 32) {
+            const int r = q / N, c = q - r * N;
+            dst[(i0 + r) * stride + c] = base[r * NP + c];
+        }
+        __syncwarp();
+    }
+};
+
 }  // namespace lx
 
 
@@ -200,6 +233,16 @@ __device__ __forceinline__ void write_mask_moves_bits(u32* __restrict__ mask, i6
 #define LX_GROUP -1
 #endif
 #define LX_IN_GROUP(g) (LX_GROUP < 0 || LX_GROUP == (g))
+
+// Envs per thread of the per-ply HBM-bound kernels (lx_random_step,
+// lx_env_step): with small states each thread loads K envs before working
+// on any of them, so K x the state bytes are in flight per thread (one
+// thread's own loads are otherwise too few to cover HBM latency once the
+// state shrinks to 32 B; placement games only).  Block b covers envs [b*256*K, (b+1)*256*K), slot
+// j of thread t is env b*256*K + j*256 + t (coalesced per slot).
+#ifndef LX_STEP_K
+#define LX_STEP_K (Game::MECH == 0 && lx::Layout<Game>::NQ <= 4 ? 2 : 1)
+#endif
 
 struct LxRefPtrs {               // reference GameState field pointers (state.py:78-130)
     signed char* board_piece;    // (B, C) int8, -1 empty
@@ -242,9 +285,9 @@ extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const 
 // Static facts of the game and of its device state layout, read by the
 // native runtime at lx_game_create (lx_game_info, include/ludax_b200.h).
 #if LX_IN_GROUP(0)
-extern "C" __constant__ int lx_facts[8] = {
+extern "C" __constant__ int lx_facts[9] = {
     Game::C, Game::A, Game::PASS, Game::W, lx::Layout<Game>::NQ, Game::NX, Game::MECH,
-    lx::Layout<Game>::NWORDS};
+    lx::Layout<Game>::NWORDS, LX_STEP_K};
 
 // mark rows (uint8 (B,), null = all) that are still live terminated +
 // truncated with a draw outcome (engine.playout_random's cap, engine.py:156-160;
@@ -378,17 +421,29 @@ extern "C" __global__ void __launch_bounds__(256) lx_step(u32* st, i64 B, const 
 #if LX_IN_GROUP(2)
 extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B, int max_turns,
                                                                  i64* actions_out) {
-    const i64 i = lx::gtid();
-    if (i >= B) return;
-    Game::St s;
-    lx::load_state<Game>(s, st, B, i);
-    if (s.term || (int)s.mc >= max_turns) { if (actions_out) actions_out[i] = -1; return; }
-    int hint;
-    const int a = lx::sample_action<Game>(s, lx::seed_mix(s.seed), hint);
-    if (actions_out) actions_out[i] = a;
-    if (a < 0) return;
-    lx::apply_step<Game>(s, a, hint);
-    lx::store_state<Game>(s, st, B, i);
+    constexpr int K = LX_STEP_K;
+    const i64 base = (i64)blockIdx.x * blockDim.x * K + threadIdx.x;
+    Game::St s[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const i64 i = base + (i64)j * blockDim.x;
+        if (i < B) lx::load_state<Game>(s[j], st, B, i);
+    }
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const i64 i = base + (i64)j * blockDim.x;
+        if (i >= B) continue;
+        if (s[j].term || (int)s[j].mc >= max_turns) {
+            if (actions_out) actions_out[i] = -1;
+            continue;
+        }
+        int hint;
+        const int a = lx::sample_action<Game>(s[j], lx::seed_mix(s[j].seed), hint);
+        if (actions_out) actions_out[i] = a;
+        if (a < 0) continue;
+        lx::apply_step<Game>(s[j], a, hint);
+        lx::store_state<Game>(s[j], st, B, i);
+    }
 }
 #endif
 
@@ -878,84 +933,111 @@ extern "C" __global__ void __launch_bounds__(128) lx_expand(u32* pool, i64 cap, 
 #define LX_ENV_MASK_BITS 4
 #define LX_ENV_STEP 8
 #if LX_IN_GROUP(4)
+namespace lx {
+// one env of lx_env_step: apply / sample, rewards, flags, auto-reset; leaves
+// the next state's legality for the mask writer in legal / pass_only / live
+template <class G>
+__device__ __forceinline__ void env_step_one(typename G::St& s, u32* st, i64 B, i64 i,
+                                             i64* actions, int max_turns, int flags,
+                                             float* rewards, unsigned char* terminated,
+                                             unsigned char* truncated, int* player, u64* bad,
+                                             bool want_mask, BB<G::W>& legal, bool& pass_only,
+                                             bool& live) {
+    float r0 = 0.f, r1 = 0.f;
+    bool out_term = s.term, out_trunc = s.trunc;
+    if ((flags & LX_ENV_STEP) && !s.term) {
+        int a, hint = -1;
+        bool ok;
+        if (flags & LX_ENV_RANDOM) {
+            a = sample_action<G>(s, seed_mix(s.seed), hint);
+            if (actions) actions[i] = a;
+            ok = a >= 0;
+        } else {
+            const i64 a64 = actions[i];
+            ok = action_legal<G>(s, a64);
+            a = (int)a64;
+        }
+        if (ok) {
+            apply_step<G>(s, a, hint);
+            if (s.term) {
+                r0 = s.outcome == 1 ? 1.f : (s.outcome == 2 ? -1.f : 0.f);
+                r1 = -r0;
+            } else if (max_turns > 0 && (int)s.mc >= max_turns) {
+                s.term = 1; s.trunc = 1; s.outcome = 0;
+            }
+        } else {
+            if (bad) atomicMin(bad, (u64)i);
+            s.term = 1;
+            if (flags & LX_ENV_RANDOM) {               // stuck: truncated draw
+                s.trunc = 1; s.outcome = 0;
+            } else {                                   // illegal: the mover loses
+                s.outcome = 2 - s.cur;
+                r0 = s.cur ? 1.f : -1.f;
+                r1 = -r0;
+            }
+        }
+        out_term = s.term;
+        out_trunc = s.trunc;
+        if ((flags & LX_ENV_AUTO_RESET) && s.term) {
+            const u64 seed = mix64(seed_mix(s.seed) ^ 0xE9ull);
+            init_state<G>(s, seed);
+        }
+        store_state<G>(s, st, B, i);
+    }
+    if (rewards) reinterpret_cast<float2*>(rewards)[i] = make_float2(r0, r1);
+    if (terminated) terminated[i] = (unsigned char)out_term;
+    if (truncated) truncated[i] = (unsigned char)out_trunc;
+    if (player) player[i] = s.cur;
+    live = !s.term;
+    if constexpr (G::MECH == 0) {
+        if (want_mask && live) legal = G::legal(s);
+        pass_only = live && !any(legal) && G::force_pass(s.phase);
+    } else {
+        if (want_mask && live) pass_only = legal_count<G>(s) == 0 && G::force_pass(s.phase);
+    }
+}
+}  // namespace lx
+
 extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, i64* actions,
                                                               int max_turns, int flags,
                                                               void* mask, float* rewards,
                                                               unsigned char* terminated,
                                                               unsigned char* truncated,
                                                               int* player, u64* bad) {
-    const i64 i = lx::gtid();
-    if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
-    const bool valid = i < B;
-    lx::BB<Game::W> legal = lx::bb_zero<Game::W>();
-    bool pass_only = false, live = false;
-    Game::St s;
-    if (valid) {
-        lx::load_state<Game>(s, st, B, i);
-        float r0 = 0.f, r1 = 0.f;
-        bool out_term = s.term, out_trunc = s.trunc;
-        if ((flags & LX_ENV_STEP) && !s.term) {
-            int a, hint = -1;
-            bool ok;
-            if (flags & LX_ENV_RANDOM) {
-                a = lx::sample_action<Game>(s, lx::seed_mix(s.seed), hint);
-                if (actions) actions[i] = a;
-                ok = a >= 0;
-            } else {
-                const i64 a64 = actions[i];
-                ok = lx::action_legal<Game>(s, a64);
-                a = (int)a64;
-            }
-            if (ok) {
-                lx::apply_step<Game>(s, a, hint);
-                if (s.term) {
-                    r0 = s.outcome == 1 ? 1.f : (s.outcome == 2 ? -1.f : 0.f);
-                    r1 = -r0;
-                } else if (max_turns > 0 && (int)s.mc >= max_turns) {
-                    s.term = 1; s.trunc = 1; s.outcome = 0;
-                }
-            } else {
-                if (bad) atomicMin(bad, (u64)i);
-                s.term = 1;
-                if (flags & LX_ENV_RANDOM) {           // stuck: truncated draw
-                    s.trunc = 1; s.outcome = 0;
-                } else {                               // illegal: the mover loses
-                    s.outcome = 2 - s.cur;
-                    r0 = s.cur ? 1.f : -1.f;
-                    r1 = -r0;
-                }
-            }
-            out_term = s.term;
-            out_trunc = s.trunc;
-            if ((flags & LX_ENV_AUTO_RESET) && s.term) {
-                const u64 seed = lx::mix64(lx::seed_mix(s.seed) ^ 0xE9ull);
-                lx::init_state<Game>(s, seed);
-            }
-            lx::store_state<Game>(s, st, B, i);
-        }
-        if (rewards) reinterpret_cast<float2*>(rewards)[i] = make_float2(r0, r1);
-        if (terminated) terminated[i] = (unsigned char)out_term;
-        if (truncated) truncated[i] = (unsigned char)out_trunc;
-        if (player) player[i] = s.cur;
-        live = !s.term;
-        if constexpr (Game::MECH == 0) {
-            if (mask && live) legal = Game::legal(s);
-            pass_only = live && !lx::any(legal) && Game::force_pass(s.phase);
-        } else {
-            if (mask && live) pass_only = lx::legal_count<Game>(s) == 0 && Game::force_pass(s.phase);
-        }
+    constexpr int K = LX_STEP_K;
+    const i64 base = (i64)blockIdx.x * blockDim.x * K + threadIdx.x;
+    Game::St s[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const i64 i = base + (i64)j * blockDim.x;
+        if (i < B) lx::load_state<Game>(s[j], st, B, i);
     }
-    if (mask) {
-        if (flags & LX_ENV_MASK_BITS) {
-            if constexpr (Game::MECH == 0)
-                lx::write_mask_bits<Game>((u32*)mask, B, i, valid, legal, pass_only);
-            else
-                lx::write_mask_moves_bits<Game>((u32*)mask, B, i, valid, s, live, pass_only);
-        } else {
-            if constexpr (Game::MECH == 0)
-                lx::write_mask_rows<Game>((unsigned char*)mask, B, i, valid, legal, pass_only);
-            else
-                lx::write_mask_moves<Game>((unsigned char*)mask, B, i, valid, s, live, pass_only);
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+        const i64 i = base + (i64)j * blockDim.x;
+        if (i - (i64)(threadIdx.x & 31u) >= B) continue;        // whole warp out (uniform)
+        const bool valid = i < B;
+        lx::BB<Game::W> legal = lx::bb_zero<Game::W>();
+        bool pass_only = false, live = false;
+        if (valid)
+            lx::env_step_one<Game>(s[j], st, B, i, actions, max_turns, flags, rewards,
+                                   terminated, truncated, player, bad, mask != nullptr, legal,
+                                   pass_only, live);
+        if (mask) {
+            if (flags & LX_ENV_MASK_BITS) {
+                if constexpr (Game::MECH == 0)
+                    lx::write_mask_bits<Game>((u32*)mask, B, i, valid, legal, pass_only);
+                else
+                    lx::write_mask_moves_bits<Game>((u32*)mask, B, i, valid, s[j], live,
+                                                    pass_only);
+            } else {
+                if constexpr (Game::MECH == 0)
+                    lx::write_mask_rows<Game>((unsigned char*)mask, B, i, valid, legal,
+                                              pass_only);
+                else
+                    lx::write_mask_moves<Game>((unsigned char*)mask, B, i, valid, s[j], live,
+                                               pass_only);
+            }
         }
     }
 }
@@ -965,19 +1047,59 @@ extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, i6
 #if LX_IN_GROUP(0)
 extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B, LxRefPtrs p) {
     const i64 i = lx::gtid();
-    if (i >= B) return;
+    if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
+    const bool valid = i < B;
     Game::St s;
-    lx::load_state<Game>(s, st, B, i);
+    if (valid) lx::load_state<Game>(s, st, B, i);
+    // one stage, wide enough for int16 label rows when they fit in 48 KB
+    constexpr bool STAGE_LABELS = Game::L_CONN && lx::RowStage<2 * Game::C>::BYTES <= 48 * 1024;
+    typedef lx::RowStage<STAGE_LABELS ? 2 * Game::C : Game::C> Rows;
+    unsigned char* r = Rows::row();
     if (p.board_owner) {                       // null: scalar fields only (B200Game.meta)
-        signed char* own = p.board_owner + i * Game::C;
-        signed char* pc = p.board_piece + i * Game::C;
-        for (int c = 0; c < Game::C; c++) {
-            const int cb = Game::cell_bit(c);
-            const bool a = lx::test(s.own0, cb), b = lx::test(s.own1, cb);
-            own[c] = a ? 0 : (b ? 1 : -1);
-            pc[c] = (a || b) ? (signed char)Game::piece_at(s, cb) : (signed char)-1;
+        if (valid)
+            for (int c = 0; c < Game::C; c++) {
+                const int cb = Game::cell_bit(c);
+                r[c] = lx::test(s.own0, cb) ? 0 : (lx::test(s.own1, cb) ? 1 : 0xff);
+            }
+        Rows::template flush<Game::C>((unsigned char*)p.board_owner, Game::C, B, i);
+        if (valid)
+            for (int c = 0; c < Game::C; c++) {
+                const int cb = Game::cell_bit(c);
+                r[c] = (lx::test(s.own0, cb) || lx::test(s.own1, cb))
+                           ? (unsigned char)Game::piece_at(s, cb) : 0xff;
+            }
+        Rows::template flush<Game::C>((unsigned char*)p.board_piece, Game::C, B, i);
+    }
+    if (p.hopped_mask) {
+        unsigned char* outs[3] = {p.hopped_mask, p.captured_mask, p.promoted_mask};
+        for (int k = 0; k < 3; k++) {
+            if (valid) {
+                unsigned char h[Game::C], cm[Game::C], pm[Game::C];
+                Game::export_transient(s, h, cm, pm);
+                const unsigned char* src = k == 0 ? h : (k == 1 ? cm : pm);
+                for (int c = 0; c < Game::C; c++) r[c] = src[c];
+            }
+            Rows::template flush<Game::C>(outs[k], Game::C, B, i);
         }
     }
+    if constexpr (Game::L_CONN) {
+        if (p.comp_labels) {                   // (B, P, C) int16 rows
+            if constexpr (STAGE_LABELS) {      // staged plan by plan
+                short lab[Game::CONN_PLANS * Game::C];
+                if (valid) Game::labels(s, lab);
+                for (int k = 0; k < Game::CONN_PLANS; k++) {
+                    short* rs = reinterpret_cast<short*>(r);
+                    if (valid)
+                        for (int c = 0; c < Game::C; c++) rs[c] = lab[k * Game::C + c];
+                    Rows::template flush<2 * Game::C>((unsigned char*)p.comp_labels + 2 * k * Game::C,
+                                                      2 * Game::CONN_PLANS * Game::C, B, i);
+                }
+            } else if (valid) {
+                Game::labels(s, p.comp_labels + i * Game::CONN_PLANS * Game::C);
+            }
+        }
+    }
+    if (!valid) return;
     if (p.current_player) p.current_player[i] = (signed char)s.cur;
     if (p.move_count) p.move_count[i] = (int)s.mc;
     if (p.terminated) p.terminated[i] = (unsigned char)s.term;
@@ -998,13 +1120,9 @@ extern "C" __global__ void __launch_bounds__(128) lx_export(const u32* st, i64 B
         p.last_dest_by_player[2 * i] = (short)s.ldbp0;
         p.last_dest_by_player[2 * i + 1] = (short)s.ldbp1;
     }
-    if (p.comp_labels) Game::labels(s, p.comp_labels + i * Game::CONN_PLANS * Game::C);
     if (p.phase) p.phase[i] = (signed char)s.phase;
     if (p.must_move) p.must_move[i] = (short)s.must_move;
     if (p.turn_pos) p.turn_pos[i] = (signed char)s.pos;
-    if (p.hopped_mask) Game::export_transient(s, p.hopped_mask + i * Game::C,
-                                              p.captured_mask + i * Game::C,
-                                              p.promoted_mask + i * Game::C);
 }
 #endif
 
@@ -1063,23 +1181,27 @@ extern "C" __global__ void __launch_bounds__(128) lx_import(u32* st, i64 B, LxRe
 extern "C" __global__ void __launch_bounds__(128) lx_observe(const u32* st, i64 B, int player,
                                                              unsigned char* planes) {
     const i64 i = lx::gtid();
-    if (i >= B) return;
+    if ((i64)(blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) >= B) return;   // whole warp out
+    const bool valid = i < B;
     Game::St s;
-    lx::load_state<Game>(s, st, B, i);
-    const lx::BB<Game::W> me = player ? s.own1 : s.own0;
-    const lx::BB<Game::W> op = player ? s.own0 : s.own1;
+    if (valid) lx::load_state<Game>(s, st, B, i);
     constexpr int T = Game::NT;
-    unsigned char* out = planes + i * (i64)((2 * T + 1) * Game::C);
-    const unsigned char mv = s.cur == player;
-    for (int t = 0; t < T; t++) {
-        const lx::BB<Game::W> tb = Game::type_bb(s, t);
-        const lx::BB<Game::W> a = me & tb, b = op & tb;
-        for (int c = 0; c < Game::C; c++) {
-            out[2 * t * Game::C + c] = lx::test(a, Game::cell_bit(c));
-            out[(2 * t + 1) * Game::C + c] = lx::test(b, Game::cell_bit(c));
+    constexpr i64 ROW = (i64)(2 * T + 1) * Game::C;
+    typedef lx::RowStage<Game::C> Rows;
+    unsigned char* r = Rows::row();
+    for (int k = 0; k < 2 * T + 1; k++) {      // plane by plane, each staged then flushed
+        if (valid) {
+            if (k == 2 * T) {
+                const unsigned char mv = s.cur == player;
+                for (int c = 0; c < Game::C; c++) r[c] = mv;
+            } else {
+                const lx::BB<Game::W> tb = Game::type_bb(s, k >> 1);
+                const lx::BB<Game::W> side = ((k & 1) ^ player) ? s.own1 : s.own0;
+                const lx::BB<Game::W> b = side & tb;
+                for (int c = 0; c < Game::C; c++) r[c] = lx::test(b, Game::cell_bit(c));
+            }
         }
+        Rows::template flush<Game::C>(planes + k * Game::C, ROW, B, i);
     }
-    for (int c = 0; c < Game::C; c++) out[2 * T * Game::C + c] = mv;
 }
 #endif
-

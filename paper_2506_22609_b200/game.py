@@ -326,17 +326,18 @@ class B200Game:
         B = state.batch_size
         buf = torch.empty(B * 16, dtype=torch.uint8, device="cuda")
         o = buf.data_ptr()
-        ref = native.RefState(current_player=o, move_count=o + B, terminated=o + 5 * B,
-                              truncated=o + 6 * B, outcome=o + 7 * B, seeds=o + 8 * B)
+        # [seeds u64 | move_count i32 | player | terminated | truncated | outcome]
+        ref = native.RefState(seeds=o, move_count=o + 8 * B, current_player=o + 12 * B,
+                              terminated=o + 13 * B, truncated=o + 14 * B, outcome=o + 15 * B)
         native.check(native.lib().lx_export(self.handle, state.words.data_ptr(), B,
                                             ctypes.byref(ref), self._stream()))
         h = buf.cpu().numpy()
-        return {"current_player": h[:B].view(np.int8).copy(),
-                "move_count": h[B:5 * B].view(np.int32).copy(),
-                "terminated": h[5 * B:6 * B].astype(bool),
-                "truncated": h[6 * B:7 * B].astype(bool),
-                "outcome": h[7 * B:8 * B].view(np.int8).copy(),
-                "seeds": h[8 * B:16 * B].view(np.uint64).copy()}
+        return {"seeds": h[:8 * B].view(np.uint64).copy(),
+                "move_count": h[8 * B:12 * B].view(np.int32).copy(),
+                "current_player": h[12 * B:13 * B].view(np.int8).copy(),
+                "terminated": h[13 * B:14 * B].astype(bool),
+                "truncated": h[14 * B:15 * B].astype(bool),
+                "outcome": h[15 * B:16 * B].view(np.int8).copy()}
 
     def expand(self, pool_words, cap, parents, actions, children, seeds, max_turns,
                masks=True):
@@ -414,6 +415,14 @@ class B200Game:
                                               state.batch_size, r.data_ptr(), self._stream()))
         state._touch()
 
+    def _device(self, state):
+        """DeviceState for a state argument: itself (host edits written back),
+        or a reference GameState-like object imported with lx_import."""
+        arrays = _foreign_arrays(state)
+        if arrays is None:
+            return _sync(state)
+        return self.from_reference(arrays)
+
     # -- legality / sampling --
     def _mover_tensor(self, mover, state):
         if mover is None:
@@ -448,12 +457,12 @@ class B200Game:
         """(B, A) bool numpy; all-false for terminated rows (compiler.py:411-428).
         ``mover``: (B,) player ids (or a scalar) whose legal actions to list
         instead of each row's current player."""
-        state = _sync(state)
+        state = self._device(state)
         return self.legal_mask_device(state, mover).cpu().numpy()
 
     def legal_counts(self, state, mover=None):
         """(B,) int64 legal action counts, pass included (compiler.py:394-409)."""
-        state = _sync(state)
+        state = self._device(state)
         return self.legal_counts_device(state, mover).cpu().numpy()
 
     def sample_actions_device(self, state, u=None, mover=None):
@@ -474,18 +483,32 @@ class B200Game:
 
     def sample_actions(self, state, u, mover=None):
         """Uniform legal action per row from a (B,) float64 draw (compiler.py:430-446)."""
-        state = _sync(state)
+        state = self._device(state)
         return self.sample_actions_device(state, u, mover).cpu().numpy()
 
     # -- stepping --
     def step(self, state, actions):
         """Pure step (compiler.py:450-454): copy, then verified step_into."""
-        out = state.copy()
+        out = self._device(state)
+        out = out.copy() if out is state else out
         self.step_into(out, actions, verify=True)
         return out
 
     def step_into(self, state, actions, rows=None, verify=True):
-        """In-place step on rows & ~terminated (compiler.py:456-580)."""
+        """In-place step on rows & ~terminated (compiler.py:456-580).  A
+        reference GameState-like argument is imported, stepped on the device
+        and its arrays overwritten in place with the result."""
+        foreign = _foreign_arrays(state)
+        if foreign is not None:
+            dev = self.from_reference(foreign)
+            self.step_into(dev, actions, rows=rows, verify=verify)
+            for k, v in dev.host().items():
+                cur = getattr(state, k, None)
+                if cur is not None:
+                    cur[...] = v
+            if hasattr(state, "_mech_cache"):
+                state._mech_cache = None
+            return
         state.sync()
         torch = _torch()
         B = state.batch_size
@@ -587,6 +610,7 @@ class B200Game:
 
     def observe(self, state, player):
         """(B, 2T+1, C) relative-owner planes + legal mask (compiler.py:611-626)."""
+        state = self._device(state)
         return (self.observe_device(state, player).cpu().numpy(),
                 self.legal_mask(state))
 
@@ -674,6 +698,20 @@ def _sync(state):
     device before a device call reads it (see DeviceState)."""
     state.sync()
     return state
+
+
+def _foreign_arrays(state):
+    """Reference-layout numpy arrays of a state object that is not a
+    DeviceState (e.g. a reference GameState built by GameState.repeat_rows /
+    concat from DeviceState fields), or None for a DeviceState."""
+    if isinstance(state, DeviceState):
+        return None
+    out = {}
+    for k in FIELDS:
+        v = getattr(state, k, None)
+        if v is not None:
+            out[k] = np.asarray(v)
+    return out
 
 
 def _u64_tensor(seeds, B):

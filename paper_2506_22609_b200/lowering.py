@@ -1567,6 +1567,7 @@ struct Game {{
     typedef lx::BB<W> BBW;
     static constexpr int NGC = {self.ngc};                     // cached move-group totals
     static constexpr int CONN_PLANS = {max(len(self.conn_plans), 1)};           // comp_labels planes
+    static constexpr bool L_CONN = {str(bool(self.conn_plans)).lower()};
     typedef lx::State<W, NX, NGC> St;
 {self._bitmap_code()}
 @@CONSTS@@
