@@ -154,18 +154,24 @@ int lx_expand(const lx_game *g, void *pool, int64_t cap, const int64_t *parents,
               const int64_t *actions, const int64_t *children, int64_t n, const uint64_t *seeds,
               int max_turns, int32_t *info, int8_t *rolled, uint8_t *masks, void *stream);
 
-/* One UCB1 MCTS decision per root state, one thread per tree (agents._Search
-   .run, agents.py:84-310: forced prefix, iterations of selection / expansion
-   / rollout / backprop, best child).  keys[t] = the tree key, budgets[t] =
-   iterations; logs[N] = log(N) as the host computes it (N < nlogs); pool:
-   pool_rows >= n * nmax env rows (node states); arena: n * arena_bytes bytes
-   (node records + action lists).  actions_out[t] = chosen action (-1: none);
-   status[t] = 1 when a capacity was exceeded (the caller searches on the
-   host instead).  Device memory throughout. */
+/* One UCB1 MCTS decision per root state (agents._Search.run, agents.py:84-310:
+   forced prefix, iterations of selection / expansion / rollout / backprop,
+   best child), one warp per tree: the lanes split each node's UCB1 scores and
+   the action-order sort; the rest runs on identical data in every lane.
+   keys[t] = the tree key, budgets[t] = iterations; logs[N] = log(N) as the
+   host computes it (N < nlogs); arena: n * arena_bytes bytes (node records,
+   action and child lists, a sort scratch of 12 * (A + 1) bytes); pool:
+   pool_rows >= n * nmax env rows (node states).  shared_bytes > 0: each
+   tree's arena (arena_bytes) and its node states (nmax * 16 * NQ) live in
+   that much dynamic shared memory instead (<= the device's opt-in limit;
+   arena / pool are then unused).  actions_out[t] = chosen action (-1:
+   none); status[t] = 1 when a capacity was exceeded (the caller searches on
+   the host instead).  Device memory throughout. */
 int lx_mcts(const lx_game *g, const void *roots, int64_t n, const uint64_t *keys,
             const int32_t *budgets, double exploration, int rollout_max_turns, const double *logs,
             int32_t nlogs, void *pool, int64_t pool_rows, int32_t nmax, void *arena,
-            int64_t arena_bytes, int64_t *actions_out, int32_t *status, void *stream);
+            int64_t arena_bytes, int64_t *actions_out, int32_t *status, int32_t shared_bytes,
+            void *stream);
 
 /* Fused register-resident rollout (engine.playout_random, engine.py:123-163;
    evaluation._run_episode, evaluation.py:197-211).

@@ -420,7 +420,32 @@ def mover_fixtures(B=24, plies=(0, 3, 7, 15)):
     np.savez_compressed(os.path.join(OUT, "mover.npz"), **arrays)
 
 
+def program_fixtures():
+    """Reference playouts of the test programs in tests/programs/ (not corpus
+    games: programs that pin one property each, e.g. big_score.ldx's scores
+    beyond int16): final-state digests, scores and outcomes."""
+    pdir = os.path.join(os.path.dirname(OUT), "programs")
+    out = {}
+    for fn in sorted(os.listdir(pdir)):
+        if not fn.endswith(".ldx"):
+            continue
+        g = boardlang.load_game(open(os.path.join(pdir, fn)).read())
+        runs = []
+        for B, seed in ((64, 3), (256, 11)):
+            f = engine.playout_random(g, seed=seed, batch_size=B, max_turns=200).final
+            runs.append({"batch": B, "seed": seed, "digest": f.digest(),
+                         "scores": f.scores.tolist() if f.scores is not None else None,
+                         "outcome": f.outcome.tolist(), "move_count": f.move_count.tolist()})
+        out[fn[:-4]] = runs
+    with open(os.path.join(OUT, "programs.json"), "w") as fh:
+        json.dump(out, fh, indent=0, sort_keys=True)
+    print("wrote programs.json", sorted(out))
+
+
 if __name__ == "__main__":
+    if "--programs" in sys.argv:
+        program_fixtures()
+        sys.exit(0)
     if "--mover" in sys.argv:
         mover_fixtures()
         sys.exit(0)

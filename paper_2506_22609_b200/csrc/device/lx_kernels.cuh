@@ -234,14 +234,18 @@ struct RowStage {
 #endif
 #define LX_IN_GROUP(g) (LX_GROUP < 0 || LX_GROUP == (g))
 
-// Envs per thread of the per-ply HBM-bound kernels (lx_random_step,
-// lx_env_step): with small states each thread loads K envs before working
-// on any of them, so K x the state bytes are in flight per thread (one
-// thread's own loads are otherwise too few to cover HBM latency once the
-// state shrinks to 32 B; placement games only).  Block b covers envs [b*256*K, (b+1)*256*K), slot
-// j of thread t is env b*256*K + j*256 + t (coalesced per slot).
+// Envs per thread of the per-ply kernels (lx_random_step, lx_env_step):
+// each thread loads K envs before working on any of them (block b covers
+// envs [b*256*K, (b+1)*256*K), slot j of thread t is env b*256*K + j*256 +
+// t).  K = 2 was measured slower on the B200 (r2d: C4 env step 52.8 -> 47.4 G
+// env steps/s with bit masks): with 32-48 B states these kernels are issue-
+// and register-bound (ncu: issue 55-65 %, math-pipe throttle the top stall,
+// occupancy limited by registers), not short of bytes in flight.
+#ifndef LX_STEP_K_OVERRIDE
+#define LX_STEP_K_OVERRIDE 1
+#endif
 #ifndef LX_STEP_K
-#define LX_STEP_K (Game::MECH == 0 && lx::Layout<Game>::NQ <= 4 ? 2 : 1)
+#define LX_STEP_K (LX_STEP_K_OVERRIDE)
 #endif
 
 struct LxRefPtrs {               // reference GameState field pointers (state.py:78-130)
@@ -475,6 +479,9 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
 #ifndef LX_REFILL_WAIT
 #define LX_REFILL_WAIT 6
 #endif
+#ifndef LX_PLY_UNROLL
+#define LX_PLY_UNROLL 1
+#endif
 #if LX_IN_GROUP(0)
 extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB)
 lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* seeds, i64 first,
@@ -573,19 +580,25 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
             waited++;
         }
         if (!__any_sync(FULL, active)) break;
-        if (playing) {
-            int hint;
-            const int a = lx::sample_action<Game>(s, smix, hint);
-            if (a < 0) {
-                atomicMin(stuck, (u64)idx);
-                playing = false;
-                pending = true;
-            } else {
-                lx::apply_step<Game>(s, a, hint);
-                n_steps++;
-                if (s.term || (int)s.mc >= max_turns) {
+        // LX_PLY_UNROLL plies per pass of the refill bookkeeping above (its
+        // ballots and branches are warp-wide overhead paid once per pass; a
+        // lane whose game ends on an earlier ply idles for the rest of it)
+#pragma unroll
+        for (int u = 0; u < LX_PLY_UNROLL; u++) {
+            if (playing) {
+                int hint;
+                const int a = lx::sample_action<Game>(s, smix, hint);
+                if (a < 0) {
+                    atomicMin(stuck, (u64)idx);
                     playing = false;
                     pending = true;
+                } else {
+                    lx::apply_step<Game>(s, a, hint);
+                    n_steps++;
+                    if (s.term || (int)s.mc >= max_turns) {
+                        playing = false;
+                        pending = true;
+                    }
                 }
             }
         }
@@ -675,22 +688,41 @@ __device__ __noinline__ int mcts_playout(typename G::St& s, u64 seed, int max_tu
 
 }  // namespace lx
 
+// One warp per search tree (block t = tree t).  The tree -- node records,
+// action lists, child lists and, when `smem` is set, the node states -- lives
+// in dynamic shared memory (else in the per-tree global arena / node pool).
+// Every lane runs the search on the same data (so control flow is uniform
+// and the per-lane registers agree); lane 0 alone writes the tree, followed
+// by __syncwarp, and the lanes split the work that is parallel: the UCB1
+// scores of a node's children (reduced to the best by (score desc, action
+// asc), the reference's order) and the rank sort of a new node's actions.
 // status[t]: 0 ok, 1 arena or path capacity exceeded (the caller falls back)
 extern "C" __global__ void __launch_bounds__(32) lx_mcts(
         const u32* roots, i64 n, const u64* keys, const int* budgets, double c,
         int rollout_max_turns, const double* logs, int nlogs, u32* pool, i64 pool_rows, int nmax,
-        unsigned char* arena, i64 arena_bytes, i64* actions_out, int* status) {
-    const i64 t = lx::gtid();
+        unsigned char* arena, i64 arena_bytes, i64* actions_out, int* status, int smem) {
+    const i64 t = blockIdx.x;
     if (t >= n) return;
+    const int lane = (int)(threadIdx.x & 31u);
+    const bool L0 = lane == 0;
+    constexpr unsigned FULL = 0xffffffffu;
     using lx::MctsNode;
     typedef Game::St St;
     constexpr int MAXPATH = 256;
-    MctsNode* nodes = reinterpret_cast<MctsNode*>(arena + t * arena_bytes);
+    constexpr int NQW = lx::Layout<Game>::NQ * 4;
+    extern __shared__ __align__(16) unsigned char lx_mcts_smem[];
+    unsigned char* ar = smem ? lx_mcts_smem : arena + t * arena_bytes;
+    MctsNode* nodes = reinterpret_cast<MctsNode*>(ar);
     int* acts = reinterpret_cast<int*>(nodes + nmax);
-    const i64 acap = (arena_bytes - (i64)nmax * (i64)sizeof(MctsNode)) / 8;   // ints: acts + kids
+    // ints: acts + kids, then (A + 1) u64 sort keys and (A + 1) ints of sort output
+    const i64 sort_bytes = (i64)(Game::A + 1) * 12;
+    const i64 acap = (arena_bytes - (i64)nmax * (i64)sizeof(MctsNode) - sort_bytes) / 8;
     int* kids = acts + acap;
+    u64* hk = reinterpret_cast<u64*>(kids + acap);
+    int* sorted = reinterpret_cast<int*>(hk + (Game::A + 1));
+    u32* sstates = reinterpret_cast<u32*>(ar + arena_bytes);   // smem: node states after the arena
     i64 aused = 0;
-    status[t] = 0;
+    if (L0) status[t] = 0;
     const u64 key = keys[t];
     const int budget = budgets[t];
     const u64 k0 = lx::mix64(lx::HASH_SEED ^ key);
@@ -700,32 +732,69 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
     int nnodes = 0;
     bool overflow = false;
 
-    auto meta = [&](MctsNode& nd, const St& s) {
+    auto load_node = [&](int node, St& s) {
+        if (smem) {
+            u32 w[NQW];
+#pragma unroll
+            for (int k = 0; k < NQW; k++) w[k] = sstates[(i64)node * NQW + k];
+            lx::unpack<Game>(s, w);
+        } else {
+            lx::load_state<Game>(s, pool, pool_rows, base + node);
+        }
+    };
+    auto store_node = [&](int node, const St& s) {     // lane 0 (caller syncs)
+        if (smem) {
+            u32 w[NQW];
+            lx::pack<Game>(s, w);
+#pragma unroll
+            for (int k = 0; k < NQW; k++) sstates[(i64)node * NQW + k] = w[k];
+        } else {
+            lx::store_state<Game>(s, pool, pool_rows, base + node);
+        }
+    };
+    auto meta = [&](MctsNode& nd, const St& s) {       // lane 0 (caller syncs)
         nd.N = 0; nd.W = 0.0; nd.to_move = s.cur; nd.term = s.term; nd.outcome = s.outcome;
         nd.nacts = 0; nd.nexp = 0; nd.acts = -1;
     };
-    // untried order: legal actions sorted by hash_key(key, 0xA11, a), ties by a
-    auto build = [&](MctsNode& nd, const St& s) {
+    // untried order: legal actions sorted by hash_key(key, 0xA11, a), ties by
+    // a, duplicates dropped: lane 0 lists the actions, the lanes hash and rank
+    // a stripe each, lane 0 compacts
+    auto build = [&](int node, const St& s) {
+        MctsNode& nd = nodes[node];
         int* out = acts + aused;
-        if (aused + Game::A + 1 > acap) { overflow = true; nd.acts = (int)aused; nd.nacts = 0; return; }
-        int m = lx::mcts_legal<Game>(s, out);
-        for (int i = 1; i < m; i++) {                    // insertion sort by (hash, action)
-            const int a = out[i];
-            const u64 h = lx::mix64(k_order ^ (u64)(i64)a);
-            int j = i - 1;
-            while (j >= 0) {
-                const u64 hj = lx::mix64(k_order ^ (u64)(i64)out[j]);
-                if (hj < h || (hj == h && out[j] <= a)) break;
-                out[j + 1] = out[j];
-                j--;
-            }
-            out[j + 1] = a;
+        if (aused + Game::A + 1 > acap) {
+            overflow = true;
+            if (L0) { nd.acts = (int)aused; nd.nacts = 0; }
+            __syncwarp();
+            return;
         }
-        int u = 0;                                       // drop duplicates (adjacent after sort)
-        for (int i = 0; i < m; i++)
-            if (u == 0 || out[u - 1] != out[i]) out[u++] = out[i];
-        nd.acts = (int)aused;
-        nd.nacts = u;
+        int m = 0;
+        if (L0) m = lx::mcts_legal<Game>(s, out);
+        m = __shfl_sync(FULL, m, 0);
+        __syncwarp();
+        for (int i = lane; i < m; i += 32) hk[i] = lx::mix64(k_order ^ (u64)(i64)out[i]);
+        __syncwarp();
+        for (int i = lane; i < m; i += 32) {
+            const u64 h = hk[i];
+            const int a = out[i];
+            int rank = 0;
+            for (int j = 0; j < m; j++) {
+                const u64 hj = hk[j];
+                const int aj = out[j];
+                rank += (hj < h || (hj == h && (aj < a || (aj == a && j < i))));
+            }
+            sorted[rank] = a;
+        }
+        __syncwarp();
+        int u = 0;
+        if (L0) {
+            for (int i = 0; i < m; i++)
+                if (u == 0 || out[u - 1] != sorted[i]) out[u++] = sorted[i];
+            nd.acts = (int)aused;
+            nd.nacts = u;
+        }
+        u = __shfl_sync(FULL, u, 0);
+        __syncwarp();
         aused += u;
     };
     auto value_for = [](int player, int outcome) -> double {
@@ -734,29 +803,35 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
     };
     int path[MAXPATH];
     auto backprop = [&](int len, int outcome) {
-        nodes[path[0]].N += 1;
-        for (int i = 1; i < len; i++) {
-            nodes[path[i]].N += 1;
-            nodes[path[i]].W += value_for(nodes[path[i - 1]].to_move, outcome);
+        if (L0) {
+            nodes[path[0]].N += 1;
+            for (int i = 1; i < len; i++) {
+                nodes[path[i]].N += 1;
+                nodes[path[i]].W += value_for(nodes[path[i - 1]].to_move, outcome);
+            }
         }
+        __syncwarp();
     };
     // child of `parent` by its next untried action; returns the backed-up value
     auto expand = [&](int parent, int action, int& child, u64 rkey, bool do_roll) -> int {
         St s;
-        lx::load_state<Game>(s, pool, pool_rows, base + parent);
+        load_node(parent, s);
         if (!s.term) lx::apply_step<Game>(s, action);
         child = nnodes++;
-        lx::store_state<Game>(s, pool, pool_rows, base + child);
-        MctsNode& nd = nodes[child];
-        meta(nd, s);
         int cnt = 0;
         if (!s.term) {
             cnt = lx::legal_count<Game>(s);
             if (cnt == 0 && Game::PASS >= 0 && Game::force_pass(s.phase)) cnt = 1;
         }
-        nd.stuck = !s.term && cnt == 0;
-        kids[nodes[parent].acts + nodes[parent].nexp] = child;
-        nodes[parent].nexp += 1;
+        if (L0) {
+            store_node(child, s);
+            MctsNode& nd = nodes[child];
+            meta(nd, s);
+            nd.stuck = !s.term && cnt == 0;
+            kids[nodes[parent].acts + nodes[parent].nexp] = child;
+            nodes[parent].nexp += 1;
+        }
+        __syncwarp();
         if (s.term || cnt == 0 || !do_roll) return s.outcome;
         return lx::mcts_playout<Game>(s, rkey, rollout_max_turns);
     };
@@ -764,13 +839,14 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
     {   // root
         St s;
         lx::load_state<Game>(s, roots, n, t);
-        lx::store_state<Game>(s, pool, pool_rows, base);
+        if (L0) { store_node(0, s); meta(nodes[0], s); }
+        __syncwarp();
         nnodes = 1;
-        meta(nodes[0], s);
-        build(nodes[0], s);
-        nodes[0].stuck = nodes[0].nacts == 0;
+        build(0, s);
+        if (L0) nodes[0].stuck = nodes[0].nacts == 0;
+        __syncwarp();
     }
-    MctsNode& root = nodes[0];
+    const MctsNode& root = nodes[0];
     int nodes_created = 0;
     // forced prefix: the first min(budget, branching) root children, rollouts
     // keyed by the node count after the whole batch is attached
@@ -786,11 +862,11 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
         nodes_created = k;
         for (int j = 0; j < k; j++) {             // rollouts + backprop in attach order
             const int child = first + j;
-            MctsNode& nd = nodes[child];
+            const MctsNode& nd = nodes[child];
             int outcome = nd.outcome;
             if (!nd.term && !nd.stuck) {
                 St s;
-                lx::load_state<Game>(s, pool, pool_rows, base + child);
+                load_node(child, s);
                 outcome = lx::mcts_playout<Game>(s, rk, rollout_max_turns);
             }
             path[0] = 0; path[1] = child;
@@ -802,14 +878,18 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
         int node = 0, len = 1;
         path[0] = 0;
         while (true) {
-            MctsNode& nd = nodes[node];
+            const MctsNode& nd = nodes[node];
             if (nd.term || nd.stuck) { backprop(len, nd.term ? nd.outcome : 0); break; }
             if (nd.acts < 0) {
                 St s;
-                lx::load_state<Game>(s, pool, pool_rows, base + node);
-                build(nd, s);
+                load_node(node, s);
+                build(node, s);
                 if (overflow) break;
-                if (nd.nacts == 0 && nd.nexp == 0) { nd.stuck = 1; continue; }
+                if (nd.nacts == 0 && nd.nexp == 0) {
+                    if (L0) nodes[node].stuck = 1;
+                    __syncwarp();
+                    continue;
+                }
             }
             if (nd.nexp < nd.nacts) {
                 if (nnodes >= nmax || len + 1 >= MAXPATH) { overflow = true; break; }
@@ -821,16 +901,27 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
                 backprop(len, outcome);
                 break;
             }
-            // UCB1 over the expanded children; ties -> smallest action
+            // UCB1 over the expanded children, lanes over a stripe each, then
+            // the warp's best by (score desc, action asc)
             const double log_n = logs[nd.N < nlogs ? nd.N : nlogs - 1];
-            int best = -1, best_a = 0;
+            int best = -1, best_a = 0x7fffffff;
             double best_s = 0.0;
-            for (int j = 0; j < nd.nexp; j++) {
-                const MctsNode& ch = nodes[kids[nd.acts + j]];
+            for (int j = lane; j < nd.nexp; j += 32) {
+                const int kid = kids[nd.acts + j];
+                const MctsNode& ch = nodes[kid];
                 const double sc = ch.W / (double)ch.N + c * sqrt(log_n / (double)ch.N);
                 const int a = acts[nd.acts + j];
                 if (best < 0 || sc > best_s || (sc == best_s && a < best_a)) {
-                    best = kids[nd.acts + j]; best_s = sc; best_a = a;
+                    best = kid; best_s = sc; best_a = a;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double os = __shfl_xor_sync(FULL, best_s, o);
+                const int oa = __shfl_xor_sync(FULL, best_a, o);
+                const int ob = __shfl_xor_sync(FULL, best, o);
+                if (ob >= 0 && (best < 0 || os > best_s || (os == best_s && oa < best_a))) {
+                    best = ob; best_s = os; best_a = oa;
                 }
             }
             if (len >= MAXPATH) { overflow = true; break; }
@@ -838,7 +929,10 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
             path[len++] = node;
         }
     }
-    if (overflow) { status[t] = 1; actions_out[t] = -1; return; }
+    if (overflow) {
+        if (L0) { status[t] = 1; actions_out[t] = -1; }
+        return;
+    }
     // best root child: (N, mean value, seeded draw), insertion order, strict >
     i64 best_a = -1;
     if (root.nexp == 0) {
@@ -855,7 +949,7 @@ extern "C" __global__ void __launch_bounds__(32) lx_mcts(
             if (better) { bN = ch.N; bQ = q; bU = u; best_a = a; }
         }
     }
-    actions_out[t] = best_a;
+    if (L0) actions_out[t] = best_a;
 }
 #endif
 

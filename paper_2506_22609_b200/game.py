@@ -31,6 +31,7 @@ from .lowering import lower_game
 from .syntax import parse_game
 
 GAMES_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "games")
+MCTS_SHARED_LIMIT = 220 * 1024      # dynamic shared memory per MCTS tree (B200 opt-in: 227 KB)
 
 FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
           "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags", "must_move",
@@ -376,8 +377,8 @@ class B200Game:
                 h[5 * n:nb].reshape(n, A).astype(bool) if masks else None)
 
     def mcts(self, roots, keys, budgets, exploration, rollout_max_turns):
-        """One MCTS decision per root row on the device (lx_mcts, one thread
-        per tree).  Returns (actions int64, ok bool) host arrays; rows with
+        """One MCTS decision per root row on the device (lx_mcts, one warp
+        per tree, the tree in shared memory when it fits).  Returns (actions int64, ok bool) host arrays; rows with
         ok False exceeded a capacity and must be searched on the host."""
         roots.sync()
         import math
@@ -387,21 +388,28 @@ class B200Game:
         nmax = int(budgets.max()) + 2
         A = self.codec.size
         node_bytes = 40                                   # lx::MctsNode
-        arena_bytes = nmax * node_bytes + 8 * (A + 1 + nmax * min(A, 256))
+        arena_bytes = nmax * node_bytes + 8 * (A + 1 + nmax * min(A, 256)) + 12 * (A + 1)
         arena_bytes = (arena_bytes + 15) // 16 * 16
+        # the whole tree in shared memory when it fits the opt-in limit
+        shared = arena_bytes + nmax * self._nq * 16
+        shared = shared if shared <= MCTS_SHARED_LIMIT else 0
         logs = torch.tensor([0.0] + [math.log(k) for k in range(1, nmax + 2)],
                             dtype=torch.float64, device="cuda")
         keys_t = _u64_tensor(keys, n)
         bud_t = torch.as_tensor(budgets).to("cuda")
-        pool = torch.empty((self._nq, n * nmax, 4), dtype=torch.int32, device="cuda")
-        arena = torch.empty(n * arena_bytes, dtype=torch.uint8, device="cuda")
+        if shared:
+            pool = torch.empty(1, dtype=torch.int32, device="cuda")
+            arena = torch.empty(1, dtype=torch.uint8, device="cuda")
+        else:
+            pool = torch.empty((self._nq, n * nmax, 4), dtype=torch.int32, device="cuda")
+            arena = torch.empty(n * arena_bytes, dtype=torch.uint8, device="cuda")
         acts = torch.empty(n, dtype=torch.int64, device="cuda")
         status = torch.empty(n, dtype=torch.int32, device="cuda")
         native.check(native.lib().lx_mcts(
             self.handle, roots.words.data_ptr(), n, keys_t.data_ptr(), bud_t.data_ptr(),
             float(exploration), int(rollout_max_turns), logs.data_ptr(), int(logs.numel()),
             pool.data_ptr(), n * nmax, nmax, arena.data_ptr(), arena_bytes, acts.data_ptr(),
-            status.data_ptr(), self._stream()))
+            status.data_ptr(), int(shared), self._stream()))
         return acts.cpu().numpy(), status.cpu().numpy() == 0
 
     def truncate_rows(self, state, rows):

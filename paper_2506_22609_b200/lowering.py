@@ -1554,6 +1554,8 @@ class GameLowering(MoveLoweringMixin):
 #define LX_ROLLOUT_MINB {r_minb}
 #define LX_REFILL_LANES {r_lanes}
 #define LX_REFILL_WAIT {r_wait}
+#define LX_SELECT_SWAR {int(os.environ.get("LX_SELECT_SWAR", "1"))}
+#define LX_PLY_UNROLL {int(os.environ.get("LX_PLY_UNROLL", "1"))}
 #include "lx_core.cuh"
 
 struct Game {{

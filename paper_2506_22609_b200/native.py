@@ -81,7 +81,7 @@ def lib():
                              ctypes.POINTER(i64), vp]
     L.lx_expand.argtypes = [vp, vp, i64, vp, vp, vp, i64, vp, ctypes.c_int, vp, vp, vp, vp]
     L.lx_mcts.argtypes = [vp, vp, i64, vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.c_int,
-                          vp, i64, ctypes.c_int, vp, i64, vp, vp, vp]
+                          vp, i64, ctypes.c_int, vp, i64, vp, vp, ctypes.c_int, vp]
     L.lx_export.argtypes = [vp, vp, i64, ctypes.POINTER(RefState), vp]
     L.lx_import.argtypes = [vp, vp, i64, ctypes.POINTER(RefState), vp]
     L.lx_observe.argtypes = [vp, vp, i64, i32, vp, vp]

@@ -114,9 +114,13 @@ def test_gavel_on_generated_programs(prog):
 
 
 @pytest.mark.parametrize("name", ["connect_four", "reversi", "english_draughts", "hex"])
-def test_device_search_equals_host_search(name):
-    """lx_mcts (one thread per tree) and the host tree search make the same
-    decisions on a batch of mid-game positions."""
+@pytest.mark.parametrize("shared", [True, False])
+def test_device_search_equals_host_search(name, shared, monkeypatch):
+    """lx_mcts (one warp per tree; the tree in shared memory, or in the
+    global arena) and the host tree search make the same decisions on a
+    batch of mid-game positions."""
+    if not shared:
+        monkeypatch.setattr(lx.game, "MCTS_SHARED_LIMIT", 0)
     g = game(name)
     st = g.init(12, seed=41)
     for _ in range(6):
