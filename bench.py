@@ -597,6 +597,7 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
                                                        "to this batch)",
                                        "bytes_per_env_ply": 2 * game.info["nq"] * 16}}
     out["env_step_api"] = measure_env_api(args, game, lx, B)
+    out["e2e_reference_layout"] = measure_e2e_reference_layout(args, game, lx, rng, B, B_total)
 
     # ---- CPU baseline (oracle port, all host threads, bounded sample): N=1 only
     if B_total != B:
@@ -608,6 +609,31 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
                            "sample": f"{steps} env steps, first {n} envs of episode 10000, "
                                      f"{dt:.1f}s on {threads} threads"}
     return out
+
+
+def measure_e2e_reference_layout(args, game, lx, rng, B, B_total, steps=3):
+    """The drop-in call end to end: engine.playout_random(game, seed, B)
+    (engine.py:123-163) with the final states exported to host numpy arrays
+    in the reference GameState layout (state.py:78-130) every step -- one
+    fused rollout, one lx_export, one device-to-host copy of every reference
+    field.  Host wall time, synchronised."""
+    import torch
+    lx.engine.playout_random(game, seed=1, batch_size=B).final.host()     # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    steps_done, d2h = 0, 0
+    for e in range(steps):
+        po = lx.engine.playout_random(game, seed=rng.episode_seed(0, B_total, 30_000 + e),
+                                      batch_size=B, max_turns=args.max_turns)
+        host = po.final.host()
+        steps_done += int(po.stats[0])
+        d2h = sum(v.nbytes for v in host.values())
+    dt = time.perf_counter() - t0
+    return {"value": steps_done / dt, "unit": UNIT, "h2d_bytes_per_step": 8,
+            "d2h_bytes_per_step": d2h, "steps_timed": steps,
+            "path": "engine.playout_random(game, seed, B).final.host(): fused rollout + "
+                    "lx_export + device->host copy of every reference GameState field "
+                    f"({d2h // B} B/env), host wall time"}
 
 
 def measure_env_api(args, game, lx, B):

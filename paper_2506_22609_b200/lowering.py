@@ -1508,7 +1508,7 @@ class GameLowering(MoveLoweringMixin):
         conn_rebuild = self._conn_rebuild_code()
         self.ngc = {0: 1, 1: len(getattr(self, "groups", ())) or 1,
                     2: len(self.grid[2]) if self.grid else 1}[self.mech_kind]
-        place_code = "        lx::place_bit(s.own0, s.own1, cell_bit(cell), side != 0);   // branchless"
+        place_code = "        lx::place_bit(s.own0, s.own1, cell_bit(cell), side);   // branchless"
         if self.mech_kind == 0:
             mech_code = f"""    static constexpr int MECH = 0;
     static __device__ __forceinline__ BBW legal(const St& s) {{
@@ -1549,13 +1549,19 @@ class GameLowering(MoveLoweringMixin):
         k_def = 8 if self.C <= 16 else (6 if self.C <= 48 else 1)
         r_lanes = int(os.environ.get("LX_REFILL_LANES", str(k_def)))
         r_wait = int(os.environ.get("LX_REFILL_WAIT", str(k_def)))
+        # plies per refill pass of lx_rollout: 2 on boards up to 128 cells (B200
+        # A/B r2e, profiles/r2e_ab_select_unroll.jsonl: C4 +4.4 %, TTT +3.7 %,
+        # Hex +1.4 %, Reversi +1.2 %), 1 beyond (Pente -11 %: its ply is large)
+        # and for movement games (their doubled plies spill to the stack)
+        r_unroll = int(os.environ.get("LX_PLY_UNROLL",
+                                      "2" if self.C <= 128 and self.mech_kind == 0 else "1"))
         src = f"""// generated by paper_2506_22609_b200.lowering for game "{spec.name}"
 #define LX_ROLLOUT_THREADS {r_threads}
 #define LX_ROLLOUT_MINB {r_minb}
 #define LX_REFILL_LANES {r_lanes}
 #define LX_REFILL_WAIT {r_wait}
 #define LX_SELECT_SWAR {int(os.environ.get("LX_SELECT_SWAR", "1"))}
-#define LX_PLY_UNROLL {int(os.environ.get("LX_PLY_UNROLL", "1"))}
+#define LX_PLY_UNROLL {r_unroll}
 #include "lx_core.cuh"
 
 struct Game {{
