@@ -50,6 +50,7 @@ GAME_FILES = {"connect_four": "Connect Four 6x7", "tic_tac_toe": "Tic-Tac-Toe",
 # envs of the benchmarked episode replayed by the oracle).  The parity sample
 # is every env where the oracle finishes in seconds on the box's host cores
 # (TTT, C4), else a 2^20 prefix of the same episode.
+GRAPH_MAX_BATCH = 1 << 16        # per-config episodes this small are replayed from a CUDA graph
 PER_CONFIG = (
     ("configs[0]", "tic_tac_toe", 1024, 400, 1024),
     ("configs[0]@2^22", "tic_tac_toe", 1 << 22, 20, 1 << 22),
@@ -365,7 +366,7 @@ class GpuArm:
         self.first, _ = shard.shard_range(self.rank, self.world_size, self.B)
         self.state = self.game.empty_state(self.B)
         self.stats = torch.zeros(8, dtype=torch.int64, device="cuda")
-        self.work = torch.zeros(4, dtype=torch.int64, device="cuda")
+        self.work = torch.zeros(16, dtype=torch.int64, device="cuda")
         self.acc = torch.zeros(8, dtype=torch.int64, device="cuda")
         self.last_episode = None
 
@@ -473,7 +474,7 @@ def measure_e2e(args, game, rng, B, B_total, first, ws, steps=None):
     seeds_d = [torch.empty(B, dtype=torch.int64, device="cuda") for _ in range(2)]
     outc_d = [torch.empty(B, dtype=torch.int8, device="cuda") for _ in range(2)]
     stats_d = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(2)]
-    work_d = [torch.zeros(4, dtype=torch.int64, device="cuda") for _ in range(2)]
+    work_d = [torch.zeros(16, dtype=torch.int64, device="cuda") for _ in range(2)]
     states = [game.empty_state(B) for _ in range(2)]
     outc_h = [torch.empty(B, dtype=torch.int8).pin_memory() for _ in range(n_it)]
     stats_h = [torch.zeros(8, dtype=torch.int64).pin_memory() for _ in range(n_it)]
@@ -681,7 +682,7 @@ def time_config(arm, game, B, steps, warmup, max_turns):
     torch, rng = arm.torch, arm.rng
     state = game.empty_state(B)
     stats = torch.zeros(8, dtype=torch.int64, device="cuda")
-    work = torch.zeros(4, dtype=torch.int64, device="cuda")
+    work = torch.zeros(16, dtype=torch.int64, device="cuda")
     acc = torch.zeros(8, dtype=torch.int64, device="cuda")
 
     def ep(e):
@@ -691,9 +692,22 @@ def time_config(arm, game, B, steps, warmup, max_turns):
         ep(w)
     torch.cuda.synchronize()
     acc.zero_()
+    graph = None
+    if B <= GRAPH_MAX_BATCH:
+        # launch-bound sizes: the K timed episodes (each its own seed) are
+        # captured once into a CUDA graph and replayed as one launch
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for e in range(steps):
+                ep(10_000 + e)
+        graph.replay()                      # warm replay, then reset the sums
+        torch.cuda.synchronize()
+        acc.zero_()
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else (lambda: [ep(10_000 + e) for e in range(steps)])
     with ClockSampler(arm.local, enabled=B >= (1 << 20)) as clk:
-        ms = arm.timed(lambda: [ep(10_000 + e) for e in range(steps)])
-    return ms, acc.cpu().tolist(), state, 10_000 + steps - 1, clk.summary()
+        ms = arm.timed(run)
+    return ms, acc.cpu().tolist(), state, 10_000 + steps - 1, clk.summary(), graph is not None
 
 
 def parity_check(name, game, state, B, episode, n, max_turns):
@@ -756,9 +770,11 @@ def measure_per_config(arm, value, ms_step, totals, head_extras):
                           "clocks": "headline clocks"})
         else:
             game = arm.lx.load_config_game(name)
-            ms, tot, state, episode, clk = time_config(arm, game, B, steps, 3, args.max_turns)
+            ms, tot, state, episode, clk, graphed = time_config(arm, game, B, steps, 3,
+                                                                args.max_turns)
             val = tot[0] / (ms / 1000.0)
             entry.update({"steps": steps, "warmup": 3, "ms_per_step": ms / steps, "value": val,
+                          "cuda_graph": graphed,
                           "mean_plies": tot[0] / max(tot[5], 1),
                           "totals": {"env_steps": tot[0], "p1_wins": tot[1], "p2_wins": tot[2],
                                      "draws": tot[3], "envs": tot[5]},

@@ -174,16 +174,22 @@ int lx_mcts(const lx_game *g, const void *roots, int64_t n, const uint64_t *keys
             void *stream);
 
 /* Fused register-resident rollout (engine.playout_random, engine.py:123-163;
-   evaluation._run_episode, evaluation.py:197-211).
+   evaluation._run_episode, evaluation.py:197-211).  One kernel launch, no
+   memsets:
    mode bit 0: start envs from seeds (seeds[i] or spawn(seed, first_index+i))
                  else continue from `state`
    mode bit 1: write final states to `state`
    mode bit 2: mark unfinished envs terminated+truncated draws at max_turns
-   work: >= 32 bytes of device scratch (counter + stuck row), reset here.
-   stats: u64[8] device buffer, zeroed here: steps, p1 wins, p2 wins, draws,
-   truncated, envs.  outcomes (B,) int8 / turns (B,) int32, or NULL: per-env
-   outcome (0 draw, 1 P1, 2 P2) and final move_count.  stuck rows ->
-   LX_EEMPTY_MASK only when check != 0 (syncs). */
+   mode bit 3 (LX_ROLLOUT_CLEAR_WORK): zero `work` first (one memset)
+   work: LX_ROLLOUT_WORK_BYTES of device scratch, zero-filled before its first
+   use; every call leaves it zeroed again (the last block clears it), so
+   reusing one buffer per stream needs no clearing.
+   stats: u64[8] device buffer, written: steps, p1 wins, p2 wins, draws,
+   truncated, envs, lowest stuck row (~0 = none), 0.  outcomes (B,) int8 /
+   turns (B,) int32, or NULL: per-env outcome (0 draw, 1 P1, 2 P2) and final
+   move_count.  stuck rows -> LX_EEMPTY_MASK only when check != 0 (syncs). */
+#define LX_ROLLOUT_CLEAR_WORK 8
+#define LX_ROLLOUT_WORK_BYTES 128
 int lx_rollout(const lx_game *g, void *state, int64_t B, int max_turns, int mode, uint64_t seed,
                const uint64_t *seeds, int64_t first_index, uint64_t *stats, void *work,
                int8_t *outcomes, int32_t *turns, int check, int64_t *stuck_row, void *stream);

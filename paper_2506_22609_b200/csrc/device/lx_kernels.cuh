@@ -458,9 +458,8 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
 //             else load it from st
 //   mode & 2: store the final state to st
 //   mode & 4: truncate unfinished envs at max_turns (engine.playout_random)
-// stats (u64[8], zeroed by the caller): steps, p1 wins, p2 wins, draws,
-// truncated, envs finished.  *counter must be zero.  *stuck = min row that
-// had no legal action (init ~0).
+// stats (u64[8], written by the last block): steps, p1 wins, p2 wins, draws,
+// truncated, envs finished, lowest row that had no legal action (~0: none).
 //
 // Game-over handling is batched per warp: a lane whose game ends keeps its
 // final state in registers and waits until LX_REFILL_LANES lanes are waiting
@@ -485,7 +484,14 @@ extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B,
 #if LX_IN_GROUP(0)
 extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB)
 lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* seeds, i64 first,
-           u64* stats, u64* counter, u64* stuck, signed char* outcomes, int* turns) {
+           u64* stats, u64* work, signed char* outcomes, int* turns) {
+    // work (u64[16], zero on entry, left zero on exit): [0] env-chunk counter,
+    // [1] ~(lowest stuck row) by atomicMax (0 = none), [2..7] stats being
+    // accumulated, [8] finished-block ticket.  The last block to finish moves
+    // the sums to `stats` and clears `work`, so a launch needs no memsets.
+    u64* counter = work;
+    u64* stuck_max = work + 1;
+    u64* acc = work + 2;
     constexpr unsigned FULL = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned lanes_below = (1u << lane) - 1u;
@@ -589,7 +595,7 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
                 int hint;
                 const int a = lx::sample_action<Game>(s, smix, hint);
                 if (a < 0) {
-                    atomicMin(stuck, (u64)idx);
+                    atomicMax(stuck_max, ~(u64)idx);
                     playing = false;
                     pending = true;
                 } else {
@@ -614,12 +620,27 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
         n_done += __shfl_xor_sync(0xffffffffu, n_done, o);
     }
     if (lane == 0) {
-        atomicAdd(stats + 0, (u64)n_steps);
-        atomicAdd(stats + 1, (u64)n_p1);
-        atomicAdd(stats + 2, (u64)n_p2);
-        atomicAdd(stats + 3, (u64)n_draw);
-        atomicAdd(stats + 4, (u64)n_trunc);
-        atomicAdd(stats + 5, (u64)n_done);
+        atomicAdd(acc + 0, (u64)n_steps);
+        atomicAdd(acc + 1, (u64)n_p1);
+        atomicAdd(acc + 2, (u64)n_p2);
+        atomicAdd(acc + 3, (u64)n_draw);
+        atomicAdd(acc + 4, (u64)n_trunc);
+        atomicAdd(acc + 5, (u64)n_done);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const u64 ticket = atomicAdd(work + 8, 1ull);
+        if (ticket == (u64)gridDim.x - 1) {            // last block: publish, then clear
+            __threadfence();
+#pragma unroll
+            for (int k = 0; k < 6; k++) stats[k] = atomicExch(acc + k, 0ull);
+            const u64 sm = atomicExch(stuck_max, 0ull);
+            stats[6] = sm ? ~sm : ~0ull;               // lowest stuck row, ~0 = none
+            stats[7] = 0ull;
+            atomicExch(counter, 0ull);
+            atomicExch(work + 8, 0ull);
+        }
     }
 }
 #endif

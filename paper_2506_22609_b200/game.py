@@ -580,7 +580,7 @@ class B200Game:
         if stats is None:
             stats = torch.empty(8, dtype=torch.int64, device="cuda")
         if work is None:
-            work = torch.empty(4, dtype=torch.int64, device="cuda")
+            work = torch.zeros(16, dtype=torch.int64, device="cuda")    # LX_ROLLOUT_WORK_BYTES
         stuck = ctypes.c_int64(-1)
         st = native.lib().lx_rollout(
             self.handle, state.words.data_ptr() if state is not None else None, B,

@@ -80,7 +80,7 @@ int main(int argc, char **argv) {
 
     void *state = dalloc((size_t)B * (size_t)info.state_bytes);
     uint64_t *stats = (uint64_t *)dalloc(8 * sizeof(uint64_t));
-    void *work = dalloc(32);
+    void *work = dalloc(LX_ROLLOUT_WORK_BYTES);   /* zero-filled once; every call leaves it zeroed */
     CHECK(lx_init(g, state, B, NULL, seed, 0, NULL));
     /* continue the initialised envs (mode 0), store finals (2), truncate at the cap (4) */
     int64_t stuck = -1;

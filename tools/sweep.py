@@ -3,7 +3,9 @@
     python tools/sweep.py [--games a,b] [--min-log2 10] [--max-log2 22]
 
 Each point: 3 warm-up episodes, then episodes (seed hash_key(0, B, 10000+e))
-timed with CUDA events until >= 0.25 s; prints one JSON line per point.
+timed with CUDA events until >= 0.25 s; batches up to 2^16 envs replay 20
+captured episodes per CUDA-graph launch (they are launch-bound); prints one
+JSON line per point.
 """
 import argparse
 import json
@@ -30,26 +32,43 @@ for name in a.games.split(","):
         B = 1 << k
         out = g.empty_state(B)
         stats = torch.zeros(8, dtype=torch.int64, device="cuda")
-        work = torch.zeros(4, dtype=torch.int64, device="cuda")
+        work = torch.zeros(16, dtype=torch.int64, device="cuda")
         acc = torch.zeros(8, dtype=torch.int64, device="cuda")
-        for e in range(3):
+
+        def ep(e):
             g.rollout(seed=rng.episode_seed(0, B, e), out=out, batch_size=B, truncate=False,
                       check=False, stats=stats, work=work)
+            acc.add_(stats)
+        for e in range(3):
+            ep(e)
         torch.cuda.synchronize()
+        graph = None
+        G = 20
+        if B <= (1 << 16):          # launch-bound: replay G captured episodes per launch
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for e in range(G):
+                    ep(10000 + e)
+            graph.replay()
+        torch.cuda.synchronize()
+        acc.zero_()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n, ms = 0, 0.0
         while ms < a.seconds * 1000:
             reps = max(1, n)
             ev0.record()
             for e in range(reps):
-                g.rollout(seed=rng.episode_seed(0, B, 10000 + n + e), out=out, batch_size=B,
-                          truncate=False, check=False, stats=stats, work=work)
-                acc.add_(stats)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    ep(10000 + n + e)
             ev1.record()
             torch.cuda.synchronize()
             ms += ev0.elapsed_time(ev1)
             n += reps
+        episodes = n * (G if graph is not None else 1)
         tot = acc.cpu().tolist()
-        print(json.dumps({"game": name, "batch": B, "episodes": n, "ms_per_episode": ms / n,
-                          "env_steps_per_s": tot[0] / (ms / 1000), "mean_plies": tot[0] / tot[5]}),
-              flush=True)
+        print(json.dumps({"game": name, "batch": B, "episodes": episodes,
+                          "ms_per_episode": ms / episodes, "cuda_graph": graph is not None,
+                          "env_steps_per_s": tot[0] / (ms / 1000),
+                          "mean_plies": tot[0] / tot[5]}), flush=True)
