@@ -86,6 +86,37 @@ __device__ __forceinline__ BB<W> sel(bool s, const BB<W>& a, const BB<W>& b) {
     return r;
 }
 
+// Powers of two as run-time constants (constant bank): a funnel shift by a
+// constant written as multiplies by these stays on the FMA pipe as IMAD /
+// IMAD.HI with a constant-bank operand -- the compiler cannot strength-reduce
+// a multiplier it does not know back into an ALU shift.
+#ifndef LX_SHIFT_FMA
+#define LX_SHIFT_FMA 0
+#endif
+#if LX_SHIFT_FMA && defined(__CUDA_ARCH__)
+__constant__ u32 lx_pow2[32] = {
+    1u << 0, 1u << 1, 1u << 2, 1u << 3, 1u << 4, 1u << 5, 1u << 6, 1u << 7,
+    1u << 8, 1u << 9, 1u << 10, 1u << 11, 1u << 12, 1u << 13, 1u << 14, 1u << 15,
+    1u << 16, 1u << 17, 1u << 18, 1u << 19, 1u << 20, 1u << 21, 1u << 22, 1u << 23,
+    1u << 24, 1u << 25, 1u << 26, 1u << 27, 1u << 28, 1u << 29, 1u << 30, 1u << 31};
+// (hi:lo) >> s, low word, for 0 < s < 32: umulhi(lo, 2^(32-s)) + hi * 2^(32-s)
+// (the two parts occupy disjoint bits, so + is |)
+__device__ __forceinline__ u32 fshr_fma(u32 lo, u32 hi, unsigned s) {
+    const u32 m = lx_pow2[32 - s];
+    return __umulhi(lo, m) + hi * m;
+}
+// (hi:lo) << s, high word: hi * 2^s + umulhi(lo, 2^s)
+__device__ __forceinline__ u32 fshl_fma(u32 lo, u32 hi, unsigned s) {
+    const u32 m = lx_pow2[s];
+    return hi * m + __umulhi(lo, m);
+}
+#define LX_FSHR(lo, hi, s) fshr_fma((lo), (hi), (s))
+#define LX_FSHL(lo, hi, s) fshl_fma((lo), (hi), (s))
+#else
+#define LX_FSHR(lo, hi, s) __funnelshift_r((lo), (hi), (s))
+#define LX_FSHL(lo, hi, s) __funnelshift_l((lo), (hi), (s))
+#endif
+
 // gather: result bit x = a bit (x + S).  S > 0 moves bits towards lower
 // indices.  Caller masks with the direction's validity mask.
 template <int W, int S>
@@ -100,7 +131,7 @@ __device__ __forceinline__ BB<W> gather(const BB<W>& a) {
         for (int i = 0; i < W; i++) {
             const u32 lo = (i + q < W) ? a.w[i + q] : 0u;
             const u32 hi = (i + q + 1 < W) ? a.w[i + q + 1] : 0u;
-            r.w[i] = s ? __funnelshift_r(lo, hi, s) : lo;
+            r.w[i] = s ? LX_FSHR(lo, hi, s) : lo;
         }
     } else {
         constexpr int q = (-S) / 32;
@@ -109,7 +140,7 @@ __device__ __forceinline__ BB<W> gather(const BB<W>& a) {
         for (int i = 0; i < W; i++) {
             const u32 hi = (i - q >= 0) ? a.w[i - q] : 0u;
             const u32 lo = (i - q - 1 >= 0) ? a.w[i - q - 1] : 0u;
-            r.w[i] = s ? __funnelshift_l(lo, hi, s) : hi;
+            r.w[i] = s ? LX_FSHL(lo, hi, s) : hi;
         }
     }
     return r;
@@ -184,6 +215,9 @@ __device__ const Sel8 lx_sel8 = Sel8();
 #ifndef LX_SELECT_SWAR
 #define LX_SELECT_SWAR 1
 #endif
+#ifndef LX_SELECT_STASH
+#define LX_SELECT_STASH 1
+#endif
 #if LX_SELECT_SWAR
 // position of the r-th (0-based) set bit of a 32-bit word; r < popc(x).
 // SWAR byte popcounts, their inclusive prefix sums by one multiply, the byte
@@ -222,24 +256,6 @@ __device__ __forceinline__ int select32(u32 x, int r) {
     return pos;
 }
 #endif
-
-// cell index of the r-th set bit (ascending cell order); r < popc(a)
-template <int W>
-__device__ __forceinline__ int select_bit(const BB<W>& a, int r) {
-    u32 word = 0u;
-    int base = 0, rem = r;
-    bool found = false;
-#pragma unroll
-    for (int i = 0; i < W; i++) {
-        const int c = __popc(a.w[i]);
-        const bool here = !found && rem < c;
-        word = here ? a.w[i] : word;
-        base = here ? 32 * i : base;
-        rem = (!found && !here) ? rem - c : rem;
-        found = found || here;
-    }
-    return base + select32(word, rem);
-}
 
 // ---- counter RNG: splitmix64 finaliser (reference rng.py:12-42) ----------
 __device__ __forceinline__ u64 mix64(u64 z) {
@@ -333,6 +349,44 @@ struct Mirror {
     }
 };
 
+// cell index of the r-th set bit (ascending cell order); r < popc(a).
+// Boards of >= 6 words find the word through the shared-memory mirror slot
+// (which such boards already have for their probes): each word and the
+// count of set bits before it are stashed, the word index is the number of
+// prefix counts <= r, and the word and its base come back with one load
+// each -- 4 ALU instructions per word instead of a select chain of ~8.
+template <int W>
+__device__ __forceinline__ int select_bit(const BB<W>& a, int r) {
+    if constexpr (W >= 6 && LX_SELECT_STASH) {
+        u32* m = Mirror<W>::slot();
+        int cum = 0, k = 0;
+#pragma unroll
+        for (int i = 0; i < W; i++) {
+            m[i * LX_MIRROR_STRIDE] = a.w[i];
+            m[(W + i) * LX_MIRROR_STRIDE] = (u32)cum;
+            cum += __popc(a.w[i]);
+            k += cum <= r;
+        }
+        const u32 word = m[k * LX_MIRROR_STRIDE];
+        const int before = (int)m[(W + k) * LX_MIRROR_STRIDE];
+        return 32 * k + select32(word, r - before);
+    }
+    u32 word = 0u;
+    int base = 0, rem = r;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+        const int c = __popc(a.w[i]);
+        const bool here = !found && rem < c;
+        word = here ? a.w[i] : word;
+        base = here ? 32 * i : base;
+        rem = (!found && !here) ? rem - c : rem;
+        found = found || here;
+    }
+    return base + select32(word, rem);
+}
+
+
 // position and in-ply offset of the r-th unit of a bit-sliced multiset:
 // cell x carries c(x) = sum_j 2^j [x in d[j]] units, units are ordered by
 // cell, and r < sum_x c(x).  Returns x; rem = r - (units of cells < x), so
@@ -388,6 +442,7 @@ struct State {
     int last_source, must_move;  // movement games (reference state.py:96-104)
     int ovr, samep;              // transient per ply: extra-turn player, same-piece flag
     int ncached;                 // ntot holds the move-group totals of the position (not stored)
+    int mirror_fresh;            // this ply's board planes are in the shared-memory mirror (not stored)
     int ntot[NGC];
     u64 seed;
 };

@@ -112,6 +112,7 @@ __device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<
     s.ovr = -1;
     s.samep = 0;
     s.ncached = 0;
+    s.mirror_fresh = 0;
 }
 
 template <class G>
@@ -163,7 +164,7 @@ __device__ __forceinline__ void init_state(typename G::St& s, u64 seed) {
     s.last_mover = -1; s.last_kind = -1; s.last_dest = -1; s.last_source = -1;
     s.pass_streak = 0; s.pf0 = 0; s.pf1 = 0; s.ldbp0 = -1; s.ldbp1 = -1;
     s.sc0 = 0; s.sc1 = 0;
-    s.must_move = -1; s.ovr = -1; s.samep = 0; s.ncached = 0;
+    s.must_move = -1; s.ovr = -1; s.samep = 0; s.ncached = 0; s.mirror_fresh = 0;
     s.seed = seed;
     G::start(s);
 }
@@ -225,6 +226,7 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
     s.ovr = -1;
     s.samep = 0;
     s.ncached = 0;
+    s.mirror_fresh = 0;
     G::clear_transient(s);
     if (is_pass) {
         s.last_kind = 4; s.last_dest = -1; s.last_source = -1; s.last_mover = mover;

@@ -31,7 +31,7 @@ from .lowering import lower_game
 from .syntax import parse_game
 
 GAMES_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "games")
-MCTS_SHARED_LIMIT = 220 * 1024      # dynamic shared memory per MCTS tree (B200 opt-in: 227 KB)
+MCTS_SHARED_LIMIT = 190 * 1024      # dynamic shared memory per MCTS tree (B200 opt-in 227 KB, less the kernels' static shared buffers)
 
 FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
           "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags", "must_move",

@@ -467,6 +467,69 @@ class GameLowering(MoveLoweringMixin):
             out = f"lx::imin({out}, {t})"
         return out
 
+    def _probe_in_mirror(self, node):
+        """Captured cells can be removed from the mirrored target plane as they
+        are found when no direction probes a cell another direction captures:
+        k*S_e != j*S_d for 1 <= k <= n+1, 1 <= j <= n."""
+        n_len = node.length
+        dirs = self.custodial_dirs(node)
+        steps = {d: self._shift[d] for d in dirs}
+        return all(k * steps[e] != j * steps[d] for d in dirs for e in dirs if d != e
+                   for k in range(1, n_len + 2) for j in range(1, n_len + 1))
+
+    def capture_probe_block(self, e, ind):
+        """Capture effect (reference effects.py:29-48) whose mask is a probed
+        anchored custodial run with the cells kept in the mirror: the probes
+        clear captured cells from the mirrored target plane and count them,
+        and only a lane that captured copies that plane back to its register
+        board -- instead of diffing and clearing every word of both boards
+        each ply (Pente: captures are rare).  None when not applicable."""
+        node = e.mask
+        if os.environ.get("LX_CAPTURE_FAST", "1") == "0":       # A/B switch
+            return None
+        if not (type(node) is n.CustodialMask and self.anchored_ctx and
+                self.piece_mode == "single" and self.use_probe and node.length != "any"
+                and not self.transient and self.NPL == 0 and self._probe_in_mirror(node)):
+            return None
+        side = self.side(node.mover)
+        n_len = node.length
+        name = f"capture_probe_{self.em.fresh('c')}"
+        lines = []
+        for d in self.custodial_dirs(node):
+            S = self._shift[d]
+            lines.append(f"        {{ const bool ok = {self._max_steps(d)} >= {n_len + 1};")
+            conds = [f"M::probe_if(ok, tg, c + {k * S})" for k in range(1, n_len + 1)]
+            conds.append(f"M::probe_if(ok, side, c + {(n_len + 1) * S})")
+            lines.append("        if (" + " & ".join(conds) + ") {")
+            for k in range(1, n_len + 1):
+                lines.append(f"            M::clear(tg, c + {k * S});")
+            lines.append(f"            ncap += {n_len};")
+            lines.append("        } }")
+        body = "\n".join(lines)
+        self.em.helper(name, f"""    // probes + mirror clears of a capture; returns the number of cells taken
+    static __device__ __forceinline__ int {name}(St& s, int mover) {{
+        typedef lx::Mirror<W> M;
+        const int side = {side};
+        const int tg = 1 - side;
+        int ncap = 0;
+        if (!(s.last_dest >= 0 && s.last_mover == side)) return 0;
+        M::store(s.own0, s.own1);
+        s.mirror_fresh = 1;
+        const int c = cell_bit(s.last_dest);
+        const int r = c / {self.emb_cols};
+        const int col = c - r * {self.emb_cols};
+{body}
+        if (ncap) {{                       // rare: the target plane comes back from the mirror
+            const BBW pl = M::load(tg);
+            if (tg) s.own1 = pl; else s.own0 = pl;
+        }}
+        return ncap;
+    }}""")
+        inc = ""
+        if e.increment_score:
+            inc = f" if (mover) s.sc1 += g; else s.sc0 += g;"
+        return f"{ind}{{ const int g = {name}(s, mover);{inc} (void)g; }}"
+
     def custodial_anchored_probe(self, node):
         """Fixed-length anchored custodial run by probing cells from last_dest:
         anchor+kd (k=1..n) target stones and anchor+(n+1)d a flanker
@@ -478,11 +541,9 @@ class GameLowering(MoveLoweringMixin):
         dirs = self.custodial_dirs(node)
         # captured cells are removed from the mirrored target plane as they are
         # found (result = registers minus mirror) when no direction probes a
-        # cell another direction captures: k*S_e != j*S_d for 1 <= k <= n+1,
-        # 1 <= j <= n; otherwise cells are set in a register bitboard
-        steps = {d: self._shift[d] for d in dirs}
-        in_mirror = all(k * steps[e] != j * steps[d] for d in dirs for e in dirs if d != e
-                        for k in range(1, n_len + 2) for j in range(1, n_len + 1))
+        # cell another direction captures; otherwise cells are set in a
+        # register bitboard
+        in_mirror = self._probe_in_mirror(node)
         for d in dirs:
             S = self._shift[d]
             # branch-free: all probes issue (clamped when off-board), one rare branch
@@ -595,7 +656,9 @@ class GameLowering(MoveLoweringMixin):
         const int side = {side};
         if (!(s.last_dest >= 0 && s.last_mover == mover)) return false;
         const int c = cell_bit(s.last_dest);
-        M::store_plane(side, s.own0, s.own1);   // only the player's stones are probed
+        // only the player's stones are probed; a capture probe earlier in this
+        // ply left the mirror current (captures change the other plane only)
+        if (!s.mirror_fresh) M::store_plane(side, s.own0, s.own1);
         if (!M::probe(side, c)) return false;
         const int r = c / {self.emb_cols};
         const int col = c - r * {self.emb_cols};
@@ -1562,6 +1625,8 @@ class GameLowering(MoveLoweringMixin):
 #define LX_REFILL_WAIT {r_wait}
 #define LX_SELECT_SWAR {int(os.environ.get("LX_SELECT_SWAR", "1"))}
 #define LX_PLY_UNROLL {r_unroll}
+#define LX_SELECT_STASH {int(os.environ.get("LX_SELECT_STASH", "1"))}
+#define LX_SHIFT_FMA {int(os.environ.get("LX_SHIFT_FMA", "0"))}
 #include "lx_core.cuh"
 
 struct Game {{
@@ -1647,9 +1712,12 @@ struct Game {{
 
     def effect(self, e):
         """One effect as a block that sees the board as left by the previous
-        effects (me / op re-read)."""
+        effects (me / op re-read).  Any effect but a mirrored capture may
+        change the boards, so it invalidates the shared-memory mirror."""
         code = self._effect(e)
         ind = "                "
+        if "capture_probe_" not in code:
+            code += f"\n{ind}s.mirror_fresh = 0;"
         return (f"{ind}{{ const BBW me = mover ? s.own1 : s.own0; const BBW op = mover ? s.own0 : s.own1;\n"
                 f"{ind}  (void)me; (void)op;\n{code}\n{ind}}}")
 
@@ -1664,6 +1732,9 @@ struct Game {{
                     f"{ind}  s.own0 = lx::sel(fs, s.own0 | cells, lx::andnot(s.own0, cells));\n"
                     f"{ind}  s.own1 = lx::sel(fs, lx::andnot(s.own1, cells), s.own1 | cells); }}")
         if t is n.CaptureEffect:
+            fast = self.capture_probe_block(e, ind)
+            if fast is not None:
+                return fast
             m = self.mask(e.mask)
             inc = ""
             if e.increment_score:

@@ -162,7 +162,7 @@ def test_full_size_c4_properties_and_shards():
                          outcomes=o)
         acc += s.cpu().numpy()
         parts.append(o)
-    assert acc.tolist() == s1
+    assert acc[:6].tolist() == s1[:6]             # [6] is the stuck row (~0 = none), not a count
     assert torch.equal(torch.cat(parts), out)
 
 
