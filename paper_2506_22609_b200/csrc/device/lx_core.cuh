@@ -289,8 +289,16 @@ __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
 // probe is one LDS instead of a W-way register select, and it runs on the
 // LSU pipe while the bitboard work saturates the ALU pipe.  Layout
 // [word][thread] keeps every access bank-conflict free.
+// Block size of the per-env kernels (lx_init / legal / sample / step /
+// random_step / env_step ...): 256, or 128 for games whose per-thread
+// shared-memory row mirror would not fit 48 KB of static shared memory per
+// block at 256 threads (lowering: LX_BLOCK).  The per-thread shared-memory
+// slots are [word][thread] with this stride.
+#ifndef LX_BLOCK
+#define LX_BLOCK 256
+#endif
 #ifndef LX_MIRROR_STRIDE
-#define LX_MIRROR_STRIDE 256
+#define LX_MIRROR_STRIDE LX_BLOCK
 #endif
 template <int W>
 struct Mirror {
@@ -387,6 +395,16 @@ __device__ __forceinline__ int select_bit(const BB<W>& a, int r) {
 }
 
 
+// Per-thread row planes (generated code's rm_row / rm_build / rm_set, see
+// lowering.GameLowering row mirror): NR words per player, [row][thread].
+template <int NR>
+struct RowMirror {
+    static __device__ __forceinline__ u32* slot() {
+        __shared__ u32 buf[2 * NR * LX_MIRROR_STRIDE];
+        return buf + threadIdx.x;
+    }
+};
+
 // position and in-ply offset of the r-th unit of a bit-sliced multiset:
 // cell x carries c(x) = sum_j 2^j [x in d[j]] units, units are ordered by
 // cell, and r < sum_x c(x).  Returns x; rem = r - (units of cells < x), so
@@ -443,6 +461,7 @@ struct State {
     int ovr, samep;              // transient per ply: extra-turn player, same-piece flag
     int ncached;                 // ntot holds the move-group totals of the position (not stored)
     int mirror_fresh;            // this ply's board planes are in the shared-memory mirror (not stored)
+    int mirror_valid;            // the row mirror holds this state's planes (not stored)
     int ntot[NGC];
     u64 seed;
 };

@@ -57,7 +57,7 @@ template <class G>
 __device__ __forceinline__ const u32* stage_mask_rows(bool valid, const BB<G::W>& legal,
                                                       bool pass_bit) {
     constexpr int NW = (G::A + 31) / 32, STRIDE = NW + 1;
-    __shared__ u32 stage[(256 / 32) * 32 * STRIDE];
+    __shared__ u32 stage[(LX_BLOCK / 32) * 32 * STRIDE];
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     u32* mine = stage + (warp * 32 + lane) * STRIDE;
     if (G::IDENT) {
@@ -275,7 +275,7 @@ struct LxRefPtrs {               // reference GameState field pointers (state.py
 };
 
 #if LX_IN_GROUP(0)
-extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const u64* seeds,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_init(u32* st, i64 B, const u64* seeds,
                                                           u64 seed_base, i64 first) {
     const i64 i = lx::gtid();
     if (i >= B) return;
@@ -289,14 +289,14 @@ extern "C" __global__ void __launch_bounds__(256) lx_init(u32* st, i64 B, const 
 // Static facts of the game and of its device state layout, read by the
 // native runtime at lx_game_create (lx_game_info, include/ludax_b200.h).
 #if LX_IN_GROUP(0)
-extern "C" __constant__ int lx_facts[9] = {
+extern "C" __constant__ int lx_facts[10] = {
     Game::C, Game::A, Game::PASS, Game::W, lx::Layout<Game>::NQ, Game::NX, Game::MECH,
-    lx::Layout<Game>::NWORDS, LX_STEP_K};
+    lx::Layout<Game>::NWORDS, LX_STEP_K, LX_BLOCK};
 
 // mark rows (uint8 (B,), null = all) that are still live terminated +
 // truncated with a draw outcome (engine.playout_random's cap, engine.py:156-160;
 // the MCTS stuck / cap handling, agents.py:430-435)
-extern "C" __global__ void __launch_bounds__(256) lx_truncate(u32* st, i64 B,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_truncate(u32* st, i64 B,
                                                               const unsigned char* rows) {
     const i64 i = lx::gtid();
     if (i >= B || (rows && !rows[i])) return;
@@ -308,7 +308,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_truncate(u32* st, i64 B,
 }
 
 // replace every row's RNG seed (the MCTS rollout re-keying, agents.py:229-233)
-extern "C" __global__ void __launch_bounds__(256) lx_set_seeds(u32* st, i64 B, const u64* seeds) {
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_set_seeds(u32* st, i64 B, const u64* seeds) {
     const i64 i = lx::gtid();
     if (i >= B) return;
     Game::St s;
@@ -323,7 +323,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_set_seeds(u32* st, i64 B, c
 // mover (B,) int8 or null: legality for that player instead of the row's
 // current player, in the row's phase (the reference's `mover=` argument).
 #if LX_IN_GROUP(1)
-extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_legal(const u32* st, i64 B,
                                                            const signed char* mover,
                                                            unsigned char* mask, i64* counts) {
     const i64 i = lx::gtid();
@@ -361,7 +361,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_legal(const u32* st, i64 B,
 // sampled action per row from u (when given) or from the row's own stream;
 // mover as in lx_legal
 #if LX_IN_GROUP(1)
-extern "C" __global__ void __launch_bounds__(256) lx_sample(const u32* st, i64 B,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_sample(const u32* st, i64 B,
                                                             const signed char* mover,
                                                             const double* u, i64* actions) {
     const i64 i = lx::gtid();
@@ -392,7 +392,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_sample(const u32* st, i64 B
 
 // verification pass: *bad = min illegal live row (init to ~0 by the caller)
 #if LX_IN_GROUP(2)
-extern "C" __global__ void __launch_bounds__(256) lx_verify(const u32* st, i64 B,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_verify(const u32* st, i64 B,
                                                             const i64* actions,
                                                             const unsigned char* rows,
                                                             u64* bad) {
@@ -408,7 +408,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_verify(const u32* st, i64 B
 
 // in-place step of live rows (rows & ~terminated)
 #if LX_IN_GROUP(2)
-extern "C" __global__ void __launch_bounds__(256) lx_step(u32* st, i64 B, const i64* actions,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_step(u32* st, i64 B, const i64* actions,
                                                           const unsigned char* rows) {
     const i64 i = lx::gtid();
     if (i >= B) return;
@@ -423,7 +423,7 @@ extern "C" __global__ void __launch_bounds__(256) lx_step(u32* st, i64 B, const 
 
 // fused sample+step for live rows, one ply (engine.random_actions + step_into)
 #if LX_IN_GROUP(2)
-extern "C" __global__ void __launch_bounds__(256) lx_random_step(u32* st, i64 B, int max_turns,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_random_step(u32* st, i64 B, int max_turns,
                                                                  i64* actions_out) {
     constexpr int K = LX_STEP_K;
     const i64 base = (i64)blockIdx.x * blockDim.x * K + threadIdx.x;
@@ -1113,7 +1113,7 @@ __device__ __forceinline__ void env_step_one(typename G::St& s, u32* st, i64 B, 
 }
 }  // namespace lx
 
-extern "C" __global__ void __launch_bounds__(256) lx_env_step(u32* st, i64 B, i64* actions,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_env_step(u32* st, i64 B, i64* actions,
                                                               int max_turns, int flags,
                                                               void* mask, float* rewards,
                                                               unsigned char* terminated,

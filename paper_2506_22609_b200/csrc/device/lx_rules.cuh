@@ -113,6 +113,7 @@ __device__ __forceinline__ void unpack(typename G::St& s, const u32 (&w)[Layout<
     s.samep = 0;
     s.ncached = 0;
     s.mirror_fresh = 0;
+    s.mirror_valid = 0;
 }
 
 template <class G>
@@ -165,6 +166,7 @@ __device__ __forceinline__ void init_state(typename G::St& s, u64 seed) {
     s.pass_streak = 0; s.pf0 = 0; s.pf1 = 0; s.ldbp0 = -1; s.ldbp1 = -1;
     s.sc0 = 0; s.sc1 = 0;
     s.must_move = -1; s.ovr = -1; s.samep = 0; s.ncached = 0; s.mirror_fresh = 0;
+    s.mirror_valid = 0;
     s.seed = seed;
     G::start(s);
 }
@@ -227,6 +229,9 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
     s.samep = 0;
     s.ncached = 0;
     s.mirror_fresh = 0;
+    if constexpr (G::ROW_MIRROR) {          // first ply of this state in this kernel
+        if (!s.mirror_valid) { G::rm_build(s); s.mirror_valid = 1; }
+    }
     G::clear_transient(s);
     if (is_pass) {
         s.last_kind = 4; s.last_dest = -1; s.last_source = -1; s.last_mover = mover;

@@ -116,6 +116,7 @@ class GameLowering(MoveLoweringMixin):
         self.ident = bool((self.bit_of == np.arange(self.C)).all())
         self.W = (self.NB + 31) // 32
         self.em = _Emitter(B, self.W, self.bit_of)
+        self.rm_used = False            # a probe was lowered onto the row mirror
         self.piece_ids = {p.name: i for i, p in enumerate(spec.equipment.pieces)}
         self._setup_piece_types()
         self.anchored_ctx = False          # effects compile with the anchored context
@@ -427,6 +428,161 @@ class GameLowering(MoveLoweringMixin):
         through the shared-memory mirror instead of whole-board shifts."""
         return self.W >= 6
 
+    # -- row mirror (big placement boards) ------------------------------------
+    # Per thread, each player's stones as one 32-bit word per grid row (bit
+    # RM_PAD + column) with RM_PAD zero rows above and below and zero columns
+    # either side, kept in shared memory and updated at each placement /
+    # capture (rebuilt from the registers when a state enters a kernel).  A
+    # probe of cell (r + dr, c + dc) is then a row load at a constant offset
+    # from row r and a bit test: no bounds checks (off-board cells read the
+    # zero padding) and no per-probe address arithmetic.
+    RM_PAD = 4
+
+    @property
+    def row_mirror_ok(self):
+        return (self.use_probe and self.mech_kind == 0 and self.NPL == 0
+                and self.emb_cols + 2 * self.RM_PAD <= 32
+                and os.environ.get("LX_ROW_MIRROR", "1") != "0")
+
+    def _drdc(self, d):
+        S = self._shift[d]
+        cols = self.emb_cols
+        dr = (S + cols // 2) // cols if S >= 0 else -((-S + cols // 2) // cols)
+        return dr, S - dr * cols
+
+    def _rm_code(self):
+        """Row-mirror layout constants and maintenance (emitted when used)."""
+        if not self.rm_used:
+            return ("    static constexpr bool ROW_MIRROR = false;\n"
+                    "    static __device__ __forceinline__ void rm_build(const St&) {}\n"
+                    "    static __device__ __forceinline__ void rm_set(int, int) {}")
+        R, EC, P = self.emb_rows, self.emb_cols, self.RM_PAD
+        build = []
+        for pl, own in ((0, "s.own0"), (1, "s.own1")):
+            for k in range(P):
+                build.append(f"        rm_row({pl}, {-1 - k})[0] = 0u; rm_row({pl}, {R + k})[0] = 0u;")
+            for r in range(R):
+                b0 = r * EC
+                wi, sh = b0 >> 5, b0 & 31
+                lo = f"{own}.w[{wi}]"
+                hi = f"{own}.w[{wi + 1}]" if wi + 1 < self.W else "0u"
+                ext = f"__funnelshift_r({lo}, {hi}, {sh})" if sh else lo
+                build.append(f"        rm_row({pl}, {r})[0] = ({ext} & 0x{(1 << EC) - 1:x}u) << {P};")
+        build = "\n".join(build)
+        return f"""    static constexpr bool ROW_MIRROR = true;
+    static constexpr int RM_ROWS = {R + 2 * P}, RM_PAD = {P}, RM_COLS = {EC};
+    // row `row` (may be negative: padding) of `player`'s plane, this thread's slot
+    static __device__ __forceinline__ u32* rm_row(int player, int row) {{
+        return lx::RowMirror<RM_ROWS>::slot() + (player * RM_ROWS + row + RM_PAD) * LX_MIRROR_STRIDE;
+    }}
+    static __device__ __forceinline__ void rm_build(const St& s) {{
+{build}
+    }}
+    static __device__ __forceinline__ void rm_set(int player, int b) {{
+        const int r = b / RM_COLS, c = b - r * RM_COLS;
+        rm_row(player, r)[0] |= 1u << (c + RM_PAD);
+    }}"""
+
+    def capture_rm_block(self, e, ind):
+        """Capture effect (effects.py:29-48) with a fixed-length anchored
+        custodial mask on the row mirror: the target / flanker rows around the
+        anchor are loaded once as windows (bit Q = the anchor's column) and
+        every direction is three bit tests; a capture clears its cells in the
+        mirror rows and the register board (rare, divergent)."""
+        node = e.mask
+        if not (type(node) is n.CustodialMask and self.anchored_ctx and self.row_mirror_ok
+                and self.piece_mode == "single" and node.length != "any"
+                and not self.transient and self._probe_in_mirror(node)):
+            return None
+        n_len = node.length
+        dirs = [self._drdc(d) + (self._shift[d],) for d in self.custodial_dirs(node)]
+        if any(abs(dr) * (n_len + 1) > self.RM_PAD or abs(dc) * (n_len + 1) > self.RM_PAD
+               for dr, dc, _ in dirs):
+            return None
+        self.rm_used = True
+        Q = max(abs(dc) for dr, dc, _ in dirs) * (n_len + 1)
+        side = self.side(node.mover)
+        tg_rows = sorted({k * dr for dr, dc, _ in dirs for k in range(1, n_len + 1)})
+        sd_rows = sorted({(n_len + 1) * dr for dr, dc, _ in dirs})
+        nm = lambda k: f"m{-k}" if k < 0 else f"p{k}"                      # noqa: E731
+        lines = [f"        const u32 t_{nm(k)} = rm_row(tg, r + {k})[0] >> sh;" for k in tg_rows]
+        lines += [f"        const u32 f_{nm(k)} = rm_row(side, r + {k})[0] >> sh;" for k in sd_rows]
+        for dr, dc, S in dirs:
+            conds = [f"(t_{nm(k * dr)} >> {Q + k * dc})" for k in range(1, n_len + 1)]
+            conds.append(f"(f_{nm((n_len + 1) * dr)} >> {Q + (n_len + 1) * dc})")
+            lines.append(f"        if ((" + " & ".join(conds) + ") & 1u) {")
+            for k in range(1, n_len + 1):
+                lines.append(f"            rm_row(tg, r + {k * dr})[0] &= ~(1u << (col + RM_PAD + {k * dc}));")
+                lines.append(f"            if (tg) lx::clearbit(s.own1, c + {k * S}); "
+                             f"else lx::clearbit(s.own0, c + {k * S});")
+            lines.append(f"            ncap += {n_len};")
+            lines.append("        }")
+        body = "\n".join(lines)
+        name = f"capture_rm_{self.em.fresh('c')}"
+        self.em.helper(name, f"""    // mirrored capture probes: returns the number of cells taken
+    static __device__ __forceinline__ int {name}(St& s, int mover) {{
+        const int side = {side};
+        const int tg = 1 - side;
+        if (!(s.last_dest >= 0 && s.last_mover == side)) return 0;
+        const int c = cell_bit(s.last_dest);
+        const int r = c / {self.emb_cols};
+        const int col = c - r * {self.emb_cols};
+        const int sh = col + RM_PAD - {Q};        // window bit {Q} = the anchor's column
+        int ncap = 0;
+{body}
+        return ncap;
+    }}""")
+        inc = ""
+        if e.increment_score:
+            inc = f" if (mover) s.sc1 += g; else s.sc0 += g;"
+        return f"{ind}{{ const int g = {name}(s, mover);{inc} (void)g; }}"
+
+    def line_rm_probe(self, node):
+        """Anchored line test (exprs.py:484-535) on the row mirror: the rows
+        around the anchor are loaded once as windows (bit P = the anchor's
+        column) and the run along each axis is counted from bit tests."""
+        if not self.row_mirror_ok or node.exclude is not None or self.piece_mode != "single":
+            return None
+        L = node.length
+        P = L if node.exact else L - 1
+        axes = []
+        for d in self.board.orientation_dirs(node.orientation):
+            a = self._drdc(d)
+            b = self._drdc(OPPOSITE[d])
+            axes.append((a, b))
+        if any(abs(x) * P > self.RM_PAD for (a, b) in axes for x in a + b):
+            return None
+        self.rm_used = True
+        side = self.side(node.player)
+        rows = sorted({k * dr for (a, b) in axes for (dr, dc) in (a, b) for k in range(0, P + 1)})
+        nm = lambda k: f"m{-k}" if k < 0 else f"p{k}"                      # noqa: E731
+        Q = max(abs(dc) for (a, b) in axes for (dr, dc) in (a, b)) * P
+        lines = [f"        const u32 w_{nm(k)} = rm_row(side, r + {k})[0] >> sh;" for k in rows]
+        lines.append(f"        if (!((w_p0 >> {Q}) & 1u)) return false;")
+        for (a, b) in axes:
+            lines.append("        {")
+            lines.append("            int run = 0;")
+            for (dr, dc) in (a, b):
+                lines.append("            { u32 on = 1u;")
+                for k in range(1, P + 1):
+                    lines.append(f"              on &= w_{nm(k * dr)} >> {Q + k * dc}; run += on & 1u;")
+                lines.append("            }")
+            lines.append(f"            if (run {'==' if node.exact else '>='} {L - 1}) return true;")
+            lines.append("        }")
+        body = "\n".join(lines)
+        name = f"line_rm_{self.em.fresh('a')}"
+        self.em.helper(name, f"""    static __device__ __forceinline__ bool {name}(const St& s, int mover) {{
+        const int side = {side};
+        if (!(s.last_dest >= 0 && s.last_mover == mover)) return false;
+        const int c = cell_bit(s.last_dest);
+        const int r = c / {self.emb_cols};
+        const int col = c - r * {self.emb_cols};
+        const int sh = col + RM_PAD - {Q};        // window bit {Q} = the anchor's column
+{body}
+        return false;
+    }}""")
+        return f"{name}(s, mover)"
+
     def _bitmap_code(self):
         """cell id <-> bit position maps (identity on row-major boards)."""
         if self.ident:
@@ -633,6 +789,9 @@ class GameLowering(MoveLoweringMixin):
         """Anchored line test (reference exprs.py:484-535) by probing: the run
         of the player's stones through last_dest along some axis has at least
         `length` cells."""
+        rm = self.line_rm_probe(node)
+        if rm is not None:
+            return rm
         if node.exclude is not None or self.piece_mode != "single":
             _fail("probed line with exclude: / several piece types is not lowered yet")
         side = self.side(node.player)
@@ -1571,7 +1730,8 @@ class GameLowering(MoveLoweringMixin):
         conn_rebuild = self._conn_rebuild_code()
         self.ngc = {0: 1, 1: len(getattr(self, "groups", ())) or 1,
                     2: len(self.grid[2]) if self.grid else 1}[self.mech_kind]
-        place_code = "        lx::place_bit(s.own0, s.own1, cell_bit(cell), side);   // branchless"
+        place_code = ("        lx::place_bit(s.own0, s.own1, cell_bit(cell), side);   // branchless\n"
+                      "        if constexpr (ROW_MIRROR) { if (s.mirror_valid) rm_set(side, cell_bit(cell)); }")
         if self.mech_kind == 0:
             mech_code = f"""    static constexpr int MECH = 0;
     static __device__ __forceinline__ BBW legal(const St& s) {{
@@ -1618,15 +1778,21 @@ class GameLowering(MoveLoweringMixin):
         # and for movement games (their doubled plies spill to the stack)
         r_unroll = int(os.environ.get("LX_PLY_UNROLL",
                                       "2" if self.C <= 128 and self.mech_kind == 0 else "1"))
+        # funnel shifts as IMAD pairs on the FMA pipe: a win only where the
+        # ALU pipe is saturated by shift-heavy Kogge-Stone fills (B200 A/B
+        # r2g, profiles/r2g_ab_capture_stash_shiftfma.jsonl: Reversi +2.6 %;
+        # C4 -2.5 %, Yavalath -4.3 %, Hex -1.2 %, Pente / TTT even)
+        r_shift_fma = int(os.environ.get("LX_SHIFT_FMA", "1" if self.has_flip else "0"))
         src = f"""// generated by paper_2506_22609_b200.lowering for game "{spec.name}"
-#define LX_ROLLOUT_THREADS {r_threads}
-#define LX_ROLLOUT_MINB {r_minb}
+#define LX_BLOCK @@BLOCK@@
+#define LX_ROLLOUT_THREADS @@RTHREADS@@
+#define LX_ROLLOUT_MINB @@RMINB@@
 #define LX_REFILL_LANES {r_lanes}
 #define LX_REFILL_WAIT {r_wait}
 #define LX_SELECT_SWAR {int(os.environ.get("LX_SELECT_SWAR", "1"))}
 #define LX_PLY_UNROLL {r_unroll}
 #define LX_SELECT_STASH {int(os.environ.get("LX_SELECT_STASH", "1"))}
-#define LX_SHIFT_FMA {int(os.environ.get("LX_SHIFT_FMA", "0"))}
+#define LX_SHIFT_FMA {r_shift_fma}
 #include "lx_core.cuh"
 
 struct Game {{
@@ -1644,6 +1810,7 @@ struct Game {{
     typedef lx::State<W, NX, NGC> St;
 {self._bitmap_code()}
 @@CONSTS@@
+@@RM@@
 @@HELPERS@@
     static __device__ __forceinline__ void start(St& s) {{
 {chr(10).join(start_code)}
@@ -1687,6 +1854,16 @@ struct Game {{
 """
         nwords = state_words(self.W, NX, self.C, L, nph, self.mech_kind)
         src = src.replace("@@CONSTS@@", em.const_defs())
+        src = src.replace("@@RM@@", self._rm_code())
+        # the row mirror (2 x (rows + 10) words per thread) fits 48 KB of static
+        # shared memory per block at 128 threads, not 256: those games run
+        # their per-env kernels and the rollout at 128 threads (4 rollout
+        # blocks per SM keep 512 threads resident, as 2 x 256 before)
+        if self.rm_used:
+            r_threads = int(os.environ.get("LX_ROLLOUT_THREADS", 128))
+            r_minb = int(os.environ.get("LX_ROLLOUT_MINB", 4))
+        src = src.replace("@@BLOCK@@", "128" if self.rm_used else "256")
+        src = src.replace("@@RTHREADS@@", str(r_threads)).replace("@@RMINB@@", str(r_minb))
         src = src.replace("@@HELPERS@@", "\n".join(em.helpers.values()))
         info = {"name": spec.name, "C": self.C, "A": self.A, "W": self.W, "NX": NX,
                 "pass_index": self.PASS, "layout": dict(self.layout),
@@ -1716,8 +1893,8 @@ struct Game {{
         change the boards, so it invalidates the shared-memory mirror."""
         code = self._effect(e)
         ind = "                "
-        if "capture_probe_" not in code:
-            code += f"\n{ind}s.mirror_fresh = 0;"
+        if "capture_probe_" not in code and "capture_rm_" not in code:
+            code += f"\n{ind}s.mirror_fresh = 0; s.mirror_valid = 0;"
         return (f"{ind}{{ const BBW me = mover ? s.own1 : s.own0; const BBW op = mover ? s.own0 : s.own1;\n"
                 f"{ind}  (void)me; (void)op;\n{code}\n{ind}}}")
 
@@ -1732,6 +1909,9 @@ struct Game {{
                     f"{ind}  s.own0 = lx::sel(fs, s.own0 | cells, lx::andnot(s.own0, cells));\n"
                     f"{ind}  s.own1 = lx::sel(fs, lx::andnot(s.own1, cells), s.own1 | cells); }}")
         if t is n.CaptureEffect:
+            fast = self.capture_rm_block(e, ind)
+            if fast is not None:
+                return fast
             fast = self.capture_probe_block(e, ind)
             if fast is not None:
                 return fast
