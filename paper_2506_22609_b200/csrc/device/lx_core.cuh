@@ -271,11 +271,14 @@ __device__ __forceinline__ u64 seed_mix(u64 seed) { return mix64(HASH_SEED ^ see
 
 // r = min(int64(u * n), max(n-1, 0)) with u = (key >> 11) * 2^-53, computed in
 // IEEE float64 exactly as numpy does (reference compiler.py:440-441)
+// (u * n < 2^31 for every board, so the truncation and clamp stay 32-bit:
+// identical values to numpy's int64 cast, one VIMNMX instead of a 64-bit
+// compare and select)
 __device__ __forceinline__ int draw_index(u64 key, int n) {
     const double u = __dmul_rn((double)(key >> 11), 0x1p-53);
-    i64 r = __double2ll_rz(__dmul_rn(u, (double)n));
-    const i64 hi = n > 1 ? (i64)(n - 1) : 0;
-    return (int)(r < hi ? r : hi);
+    const int r = __double2int_rz(__dmul_rn(u, (double)n));
+    const int hi = n > 1 ? n - 1 : 0;
+    return r < hi ? r : hi;
 }
 
 __device__ __forceinline__ double key_uniform(u64 key) {

@@ -318,6 +318,18 @@ class B200Game:
         del torch
         return st
 
+    def occupied_device(self, state):
+        """(B, C) bool CUDA tensor: cells holding a stone (board_owner >= 0),
+        exported on the device without a host copy (play_match coverage)."""
+        torch = _torch()
+        state.sync()
+        B, C = state.batch_size, self.num_cells
+        buf = torch.empty((2, B, C), dtype=torch.int8, device="cuda")
+        ref = native.RefState(board_owner=buf[0].data_ptr(), board_piece=buf[1].data_ptr())
+        native.check(native.lib().lx_export(self.handle, state.words.data_ptr(), B,
+                                            ctypes.byref(ref), self._stream()))
+        return buf[0] >= 0
+
     # -- per-row scalars (lx_export of the scalar fields only) --
     def meta(self, state):
         """Host numpy arrays of current_player, move_count, terminated,
@@ -393,8 +405,12 @@ class B200Game:
         # the whole tree in shared memory when it fits the opt-in limit
         shared = arena_bytes + nmax * self._nq * 16
         shared = shared if shared <= MCTS_SHARED_LIMIT else 0
-        logs = torch.tensor([0.0] + [math.log(k) for k in range(1, nmax + 2)],
-                            dtype=torch.float64, device="cuda")
+        cache = getattr(self, "_mcts_logs", None)
+        if cache is None or cache.numel() < nmax + 2:
+            cache = torch.tensor([0.0] + [math.log(k) for k in range(1, nmax + 2)],
+                                 dtype=torch.float64, device="cuda")
+            self._mcts_logs = cache
+        logs = cache
         keys_t = _u64_tensor(keys, n)
         bud_t = torch.as_tensor(budgets).to("cuda")
         if shared:
@@ -403,14 +419,15 @@ class B200Game:
         else:
             pool = torch.empty((self._nq, n * nmax, 4), dtype=torch.int32, device="cuda")
             arena = torch.empty(n * arena_bytes, dtype=torch.uint8, device="cuda")
-        acts = torch.empty(n, dtype=torch.int64, device="cuda")
-        status = torch.empty(n, dtype=torch.int32, device="cuda")
+        out = torch.empty(3 * n, dtype=torch.int32, device="cuda")   # actions (i64) | status
+        acts, status = out[:2 * n].view(torch.int64), out[2 * n:]
         native.check(native.lib().lx_mcts(
             self.handle, roots.words.data_ptr(), n, keys_t.data_ptr(), bud_t.data_ptr(),
             float(exploration), int(rollout_max_turns), logs.data_ptr(), int(logs.numel()),
             pool.data_ptr(), n * nmax, nmax, arena.data_ptr(), arena_bytes, acts.data_ptr(),
             status.data_ptr(), int(shared), self._stream()))
-        return acts.cpu().numpy(), status.cpu().numpy() == 0
+        h = out.cpu().numpy()
+        return h[:2 * n].view(np.int64).copy(), h[2 * n:] == 0
 
     def truncate_rows(self, state, rows):
         """Mark rows terminated + truncated with a draw outcome in place (the

@@ -1429,9 +1429,15 @@ class GameLowering(MoveLoweringMixin):
                     f"                solo = false;\n"
                     f"            }}\n"
                     f"#endif") if os.environ.get("LX_COOP_FLOOD", "1") != "0" else ""
+            # the placed cell's plan neighbourhood and target-0 membership from
+            # a per-cell table (one 16-byte load per ply instead of the
+            # one-hot's four shifted copies)
+            need_expr = f"({cond}) && lx::any((a & t0) | (({dil_a}) & R))"
+            if os.environ.get("LX_NEIGHBOR_TABLE", "1") != "0":
+                need_expr = self._need_table(plan, grp, cond)
             out.append(f"""{head}
             const BBW a = lx::onehot<W>(cell_bit(cell));
-            const bool need = ({cond}) && lx::any((a & t0) | (({dil_a}) & R));
+            const bool need = {need_expr};
             const BBW mine = side ? s.own1 : s.own0;
             const BBW free_ = lx::andnot(mine, R);
             BBW f = a;
@@ -1446,6 +1452,34 @@ class GameLowering(MoveLoweringMixin):
             }}
         }}""")
         return "\n".join(out)
+
+    def _need_table(self, plan, grp, cond):
+        """`need` of a reach-set update from a constant per-cell table: words
+        [0, W) = the cell's plan neighbours (as dilating {cell} gives them),
+        word W = bit k set when the cell is in slot grp[k]'s target 0."""
+        W = self.W
+        name = f"NBT_{self.em.fresh('n')}"
+        rows = []
+        for c in range(self.C):
+            b = int(self.bit_of[c])
+            m = 0
+            for d in plan:
+                x = int(self.board.neighbors[d][c])
+                if x != self.C:
+                    m |= 1 << int(self.bit_of[x])
+            flags = 0
+            for k, slot in enumerate(grp):
+                if bool(np.asarray(self.slot_info[slot][1][0])[c]):      # cell-indexed mask
+                    flags |= 1 << k
+            words = [(m >> (32 * i)) & 0xffffffff for i in range(W)] + [flags]
+            rows.append("{" + ", ".join(f"0x{w:08x}u" for w in words) + "}")
+        self.em.helper(name, f"    static __device__ __forceinline__ const u32* {name}(int c) {{\n"
+                             f"        static __device__ const u32 t[{self.C}][{W + 1}] = {{\n            "
+                             + ",\n            ".join(rows) + "};\n        return t[c];\n    }")
+        loads = " | ".join(f"(__ldg({name}(cell) + {i}) & R.w[{i}])" for i in range(W))
+        flag = ("((__ldg(" + name + f"(cell) + {W}) >> (s1 ? 1 : 0)) & 1u)" if len(grp) == 2
+                else f"(__ldg({name}(cell) + {W}) & 1u)")
+        return f"({cond}) && ({flag} || ({loads}) != 0u)"
 
     def _conn_rebuild_code(self):
         """Reach sets from scratch (start position, lx_import)."""

@@ -27,4 +27,6 @@ static inline unsigned __funnelshift_l(unsigned lo, unsigned hi, unsigned s) {
 // strict IEEE double multiply (compiled with -ffp-contract=off)
 static inline double __dmul_rn(double a, double b) { volatile double r = a * b; return r; }
 static inline long long __double2ll_rz(double x) { return (long long)x; }
+static inline int __double2int_rz(double x) { return (int)x; }
 static inline int __clzll(long long x) { return x ? __builtin_clzll((unsigned long long)x) : 64; }
+template <class T> static inline T __ldg(const T* p) { return *p; }
