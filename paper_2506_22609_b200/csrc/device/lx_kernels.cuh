@@ -521,7 +521,9 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
     Game::St s;
     u64 smix = 0;
     i64 idx = -1;
-    bool playing = false, pending = false, active = true;
+    // lane flags as 32-bit ints: bools live in byte lanes of a register and
+    // every update costs a PRMT on the ALU pipe
+    int playing = 0, pending = 0, active = 1;
     int waited = 0;               // plies since a lane started waiting (warp-uniform)
     while (true) {
         const unsigned idle = __ballot_sync(FULL, active && !playing);
