@@ -241,6 +241,10 @@ struct RowStage {
 // env steps/s with bit masks): with 32-48 B states these kernels are issue-
 // and register-bound (ncu: issue 55-65 %, math-pipe throttle the top stall,
 // occupancy limited by registers), not short of bytes in flight.
+// minimum resident blocks per SM of the per-ply HBM kernels (register cap)
+#ifndef LX_STEP_MINB
+#define LX_STEP_MINB 1
+#endif
 #ifndef LX_STEP_K_OVERRIDE
 #define LX_STEP_K_OVERRIDE 1
 #endif
@@ -423,7 +427,7 @@ extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_step(u32* st, i64 B, c
 
 // fused sample+step for live rows, one ply (engine.random_actions + step_into)
 #if LX_IN_GROUP(2)
-extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_random_step(u32* st, i64 B, int max_turns,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK, LX_STEP_MINB) lx_random_step(u32* st, i64 B, int max_turns,
                                                                  i64* actions_out) {
     constexpr int K = LX_STEP_K;
     const i64 base = (i64)blockIdx.x * blockDim.x * K + threadIdx.x;
@@ -1115,7 +1119,7 @@ __device__ __forceinline__ void env_step_one(typename G::St& s, u32* st, i64 B, 
 }
 }  // namespace lx
 
-extern "C" __global__ void __launch_bounds__(LX_BLOCK) lx_env_step(u32* st, i64 B, i64* actions,
+extern "C" __global__ void __launch_bounds__(LX_BLOCK, LX_STEP_MINB) lx_env_step(u32* st, i64 B, i64* actions,
                                                               int max_turns, int flags,
                                                               void* mask, float* rewards,
                                                               unsigned char* terminated,
