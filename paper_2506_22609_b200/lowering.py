@@ -1810,9 +1810,10 @@ class GameLowering(MoveLoweringMixin):
         # A/B r2e, profiles/r2e_ab_select_unroll.jsonl: C4 +4.4 %, TTT +3.7 %,
         # Hex +1.4 %, Reversi +1.2 %), 1 beyond (Pente -11 %: its ply is large)
         # and for movement games (their doubled plies spill to the stack)
-        # (r2j: 3 plies on <= 48 cells: TTT +9 %, C4 +1.3 % over 2)
+        # (r2j/r2k: 3 plies on <= 64 cells: TTT +9 %, C4 +1.3 %, Reversi +1.7 %
+        # over 2; 4 is worse on TTT)
         r_unroll = int(os.environ.get("LX_PLY_UNROLL",
-                                      ("3" if self.C <= 48 else "2")
+                                      ("3" if self.C <= 64 else "2")
                                       if self.C <= 128 and self.mech_kind == 0 else "1"))
         # funnel shifts as IMAD pairs on the FMA pipe: a win only where the
         # ALU pipe is saturated by shift-heavy Kogge-Stone fills (B200 A/B
@@ -1829,7 +1830,7 @@ class GameLowering(MoveLoweringMixin):
 #define LX_PLY_UNROLL {r_unroll}
 #define LX_SELECT_STASH {int(os.environ.get("LX_SELECT_STASH", "1"))}
 #define LX_SHIFT_FMA {r_shift_fma}
-#define LX_STEP_MINB {int(os.environ.get("LX_STEP_MINB", "1"))}
+#define LX_STEP_MINB {int(os.environ.get("LX_STEP_MINB", "4"))}
 #include "lx_core.cuh"
 
 struct Game {{
