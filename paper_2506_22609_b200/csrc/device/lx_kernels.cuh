@@ -212,9 +212,10 @@ struct RowStage {
         const i64 left = B - i0;
         const int nrows = left < 32 ? (int)left : 32;
         const unsigned char* base = row() - lane * NP;
-        if (stride == N) {
-            // rows back to back: the warp's block is contiguous and starts on
-            // a 4-byte boundary (i0 is a multiple of 32) -- 4-byte stores
+        if (stride == N && ((reinterpret_cast<unsigned long long>(dst + i0 * (i64)N) & 3ull) == 0)) {
+            // rows back to back: the warp's block is contiguous; when it starts
+            // on a 4-byte boundary (the caller's array usually does, and i0 is
+            // a multiple of 32) it goes out as 4-byte stores
             u32* d4 = reinterpret_cast<u32*>(dst + i0 * (i64)N);
             const int nbytes = nrows * N, nw = nbytes >> 2;
             for (int q = (int)lane; q < nw; q += 32) {
