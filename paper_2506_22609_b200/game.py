@@ -331,26 +331,37 @@ class B200Game:
         return buf[0] >= 0
 
     # -- per-row scalars (lx_export of the scalar fields only) --
-    def meta(self, state):
+    def meta(self, state, counts=False):
         """Host numpy arrays of current_player, move_count, terminated,
-        truncated, outcome and seeds (one export launch, no boards)."""
+        truncated, outcome and seeds (one export launch, no boards) -- and,
+        with ``counts``, the legal action counts (one lx_legal launch) -- in
+        one device-to-host copy."""
         state.sync()
         torch = _torch()
         B = state.batch_size
-        buf = torch.empty(B * 16, dtype=torch.uint8, device="cuda")
+        nb = 24 * B if counts else 16 * B
+        buf = torch.empty(nb, dtype=torch.uint8, device="cuda")
         o = buf.data_ptr()
-        # [seeds u64 | move_count i32 | player | terminated | truncated | outcome]
-        ref = native.RefState(seeds=o, move_count=o + 8 * B, current_player=o + 12 * B,
-                              terminated=o + 13 * B, truncated=o + 14 * B, outcome=o + 15 * B)
+        # [seeds u64 | counts i64 | move_count i32 | player | terminated | truncated | outcome]
+        c = 8 * B if counts else 0
+        ref = native.RefState(seeds=o, move_count=o + c + 8 * B, current_player=o + c + 12 * B,
+                              terminated=o + c + 13 * B, truncated=o + c + 14 * B,
+                              outcome=o + c + 15 * B)
         native.check(native.lib().lx_export(self.handle, state.words.data_ptr(), B,
                                             ctypes.byref(ref), self._stream()))
+        if counts:
+            native.check(native.lib().lx_legal(self.handle, state.words.data_ptr(), B, None,
+                                               None, o + 8 * B, self._stream()))
         h = buf.cpu().numpy()
-        return {"seeds": h[:8 * B].view(np.uint64).copy(),
-                "move_count": h[8 * B:12 * B].view(np.int32).copy(),
-                "current_player": h[12 * B:13 * B].view(np.int8).copy(),
-                "terminated": h[13 * B:14 * B].astype(bool),
-                "truncated": h[14 * B:15 * B].astype(bool),
-                "outcome": h[15 * B:16 * B].view(np.int8).copy()}
+        out = {"seeds": h[:8 * B].view(np.uint64).copy(),
+               "move_count": h[c + 8 * B:c + 12 * B].view(np.int32).copy(),
+               "current_player": h[c + 12 * B:c + 13 * B].view(np.int8).copy(),
+               "terminated": h[c + 13 * B:c + 14 * B].astype(bool),
+               "truncated": h[c + 14 * B:c + 15 * B].astype(bool),
+               "outcome": h[c + 15 * B:c + 16 * B].view(np.int8).copy()}
+        if counts:
+            out["legal_counts"] = h[8 * B:16 * B].view(np.int64).copy()
+        return out
 
     def expand(self, pool_words, cap, parents, actions, children, seeds, max_turns,
                masks=True):

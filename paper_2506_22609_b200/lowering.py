@@ -410,6 +410,22 @@ class GameLowering(MoveLoweringMixin):
         run y, y+e, .., y+(j-1)e of `pro` cells with y+je in gen, j <= 2^m - 1
         >= max_run.  Log-steps walk(e, 1), walk(e, 2), walk(e, 4) ... with
         exact k-step validity masks (no wrap).  Declares BBW g."""
+        if os.environ.get("LX_KS_PREMASK", "1") != "0":
+            # the propagator masked once to cells with an e-neighbour: p_k(x)
+            # then implies x + k*e is a valid walk (p_2(x) = p(x) & p(x + e)
+            # needs both steps valid, and so on), so the log-steps are raw
+            # shifts -- one LOP3 per word instead of two (the walk masks)
+            S = self._shift[e]
+            v1 = self.em.const(self._walk_ok(e, 1))
+            code = [f"{ind}BBW g = {gen};", f"{ind}BBW p = {pro} & {v1};"]
+            k, covered = 1, 0
+            while covered < max_run:
+                code.append(f"{ind}g = g | (p & lx::gather<W, {S * k}>(g));")
+                covered += k
+                if covered < max_run:
+                    code.append(f"{ind}p = p & lx::gather<W, {S * k}>(p);")
+                k *= 2
+            return code
         code = [f"{ind}BBW g = {gen};", f"{ind}BBW p = {pro};"]
         k, covered = 1, 0
         while covered < max_run:
