@@ -229,6 +229,9 @@ class B200Game:
         dev = _torch().cuda.current_device()
         h = self._native.get(dev)
         if h is None:
+            # torch's current device may not have made its (primary) context
+            # current on this thread yet; the handle binds to that context
+            native.check(native.lib().lx_bind_device(dev))
             i = self.lowered.info
             h = native.NativeGame(self.lowered.source, self.name, expect={
                 "num_cells": i["C"], "num_actions": i["A"], "pass_index": i["pass_index"],
