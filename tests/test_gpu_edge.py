@@ -196,3 +196,23 @@ def test_mcts_rollout_primitive(name):
     want = np.where(fin["terminated"] & ~fin["truncated"], fin["outcome"], 0)
     assert np.array_equal(got, want)
     assert st.digest() != O.digest(fin)        # input state untouched (still mid-game)
+
+
+def test_host_edits_of_exported_fields_reach_the_device():
+    """DeviceState write-back: in-place edits of exported reference
+    fields -- what engine.playout_random does at the cap (engine.py:156-160)
+    -- are imported before the next device call, so the device sees them."""
+    g = game("connect_four")
+    st = g.init(4, seed=1)
+    st.terminated[1] = True                      # host-side edits of the cached export
+    st.truncated[1] = True
+    st.outcome[1] = 0
+    g.step_into(st, np.array([35, 36, 37, 38]), verify=False)
+    assert st.move_count.tolist() == [1, 0, 1, 1]          # row 1 absorbed the step
+    assert st.terminated.tolist() == [False, True, False, False]
+    assert bool(st.truncated[1]) and int(st.outcome[1]) == 0
+    cp = st.copy()                                # copies see the edits too
+    cp.outcome[2] = 1
+    cp.terminated[2] = True
+    fin, _ = g.rollout(state=cp, max_turns=200)
+    assert int(fin.outcome[2]) == 1 and int(fin.move_count[2]) == 1
