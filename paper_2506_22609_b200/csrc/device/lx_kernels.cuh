@@ -128,6 +128,22 @@ template <class G>
 __device__ __forceinline__ void write_mask_bits(u32* __restrict__ mask, i64 B, i64 i, bool valid,
                                                 const BB<G::W>& legal, bool pass_bit) {
     constexpr int NW = (G::A + 31) / 32, STRIDE = NW + 1;
+    if constexpr (G::IDENT && (NW == 1 || NW == 2 || NW == 4) && NW >= G::W) {
+        // rows of 4 / 8 / 16 bytes: each lane stores its own row with one
+        // vector store (consecutive lanes, consecutive rows: coalesced)
+        if (valid) {
+            u32 v[NW];
+#pragma unroll
+            for (int j = 0; j < NW; j++) {
+                v[j] = j < G::W ? legal.w[j] : 0u;
+                if (G::PASS >= 0 && j == (G::C >> 5) && pass_bit) v[j] |= 1u << (G::C & 31);
+            }
+            if constexpr (NW == 1) mask[i] = v[0];
+            else if constexpr (NW == 2) reinterpret_cast<uint2*>(mask)[i] = make_uint2(v[0], v[1]);
+            else reinterpret_cast<uint4*>(mask)[i] = make_uint4(v[0], v[1], v[2], v[3]);
+        }
+        return;
+    }
     const u32* rows = stage_mask_rows<G>(valid, legal, pass_bit);
     const unsigned lane = threadIdx.x & 31u;
     const i64 i0 = i - lane;

@@ -1819,9 +1819,14 @@ class GameLowering(MoveLoweringMixin):
         # only (measured on B200 at 2^22 envs, profiles/r1_tune_refill.jsonl:
         # TTT best 8-12, C4 best 6, Hex/Reversi/Pente best 1); board size bounds
         # the game length.  Env overrides for tuning.
+        # (r2p/r2q re-tune with multi-ply passes: TTT 16 / 12 +6 % over 8 / 8;
+        # C4, Hex, Reversi best as they were; profiles/r2p_ab_refill.jsonl)
         k_def = 8 if self.C <= 16 else (6 if self.C <= 48 else 1)
+        w_def = k_def
+        if self.C <= 16:
+            k_def, w_def = 16, 12
         r_lanes = int(os.environ.get("LX_REFILL_LANES", str(k_def)))
-        r_wait = int(os.environ.get("LX_REFILL_WAIT", str(k_def)))
+        r_wait = int(os.environ.get("LX_REFILL_WAIT", str(w_def)))
         # plies per refill pass of lx_rollout: 2 on boards up to 128 cells (B200
         # A/B r2e, profiles/r2e_ab_select_unroll.jsonl: C4 +4.4 %, TTT +3.7 %,
         # Hex +1.4 %, Reversi +1.2 %), 1 beyond (Pente -11 %: its ply is large)

@@ -216,3 +216,26 @@ def test_host_edits_of_exported_fields_reach_the_device():
     cp.terminated[2] = True
     fin, _ = g.rollout(state=cp, max_turns=200)
     assert int(fin.outcome[2]) == 1 and int(fin.move_count[2]) == 1
+
+
+def test_rollout_work_buffer_is_left_clear_and_clear_mode():
+    """lx_rollout needs no memsets: the last block publishes the stats and
+    leaves the 128-byte work buffer zeroed; LX_ROLLOUT_CLEAR_WORK (mode bit 3)
+    clears a buffer the caller cannot vouch for."""
+    import ctypes
+
+    from paper_2506_22609_b200 import native
+    g = game("connect_four")
+    B = 3000
+    work = torch.zeros(16, dtype=torch.int64, device="cuda")
+    _, s1 = g.rollout(batch_size=B, seed=9, store=False, work=work)
+    assert int(work.abs().sum()) == 0
+    want = s1.cpu().tolist()
+    assert want[6] == -1                                     # no stuck row
+    work.fill_(12345)                                        # dirty scratch
+    stats = torch.empty(8, dtype=torch.int64, device="cuda")
+    stuck = ctypes.c_int64(-1)
+    native.check(native.lib().lx_rollout(g.handle, None, B, 200, 1 | 4 | 8, 9, None, 0,
+                                         stats.data_ptr(), work.data_ptr(), None, None, 1,
+                                         ctypes.byref(stuck), g._stream()))
+    assert stats.cpu().tolist() == want and int(work.abs().sum()) == 0
