@@ -636,19 +636,51 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
         // lane whose game ends on an earlier ply idles for the rest of it)
 #pragma unroll
         for (int u = 0; u < LX_PLY_UNROLL; u++) {
-            if (playing) {
-                int hint;
-                const int a = lx::sample_action<Game>(s, smix, hint);
-                if (a < 0) {
-                    atomicMax(stuck_max, ~(u64)idx);
-                    playing = false;
-                    pending = true;
-                } else {
-                    lx::apply_step<Game>(s, a, hint);
-                    n_steps++;
-                    if (s.term || (int)s.mc >= max_turns) {
-                        playing = false;
-                        pending = true;
+            if constexpr (Game::SPLIT_FLOOD) {
+                // reach-set games: the ply is split around its flood, which the
+                // whole warp runs converged (lx::coop_flood) -- inside a ply
+                // only the playing lanes are active and each would flood alone
+                typename Game::Flood fl;
+                fl.need = 0;
+                fl.f = lx::bb_zero<Game::W>();
+                fl.free_ = fl.f;
+                int a = -1;
+                if (playing) {
+                    int hint;
+                    a = lx::sample_action<Game>(s, smix, hint);
+                    if (a >= 0) lx::apply_step_pre<Game>(s, a, fl);
+                }
+                lx::coop_flood<Game::W>(fl.need != 0, fl.free_, fl.f,
+                                        [](const lx::LW<Game::W>& x) { return Game::flood_dil(x); });
+                if (playing) {
+                    if (a < 0) {
+                        atomicMax(stuck_max, ~(u64)idx);
+                        playing = 0;
+                        pending = 1;
+                    } else {
+                        lx::apply_step_post<Game>(s, a, fl);
+                        n_steps++;
+                        if (s.term || (int)s.mc >= max_turns) {
+                            playing = 0;
+                            pending = 1;
+                        }
+                    }
+                }
+            } else {
+                if (playing) {
+                    int hint;
+                    const int a = lx::sample_action<Game>(s, smix, hint);
+                    if (a < 0) {
+                        atomicMax(stuck_max, ~(u64)idx);
+                        playing = 0;
+                        pending = 1;
+                    } else {
+                        lx::apply_step<Game>(s, a, hint);
+                        n_steps++;
+                        if (s.term || (int)s.mc >= max_turns) {
+                            playing = 0;
+                            pending = 1;
+                        }
                     }
                 }
             }

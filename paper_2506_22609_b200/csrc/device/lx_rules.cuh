@@ -219,12 +219,11 @@ __device__ __forceinline__ int sample_action(const typename G::St& s, u64 smix) 
 // one ply for a live row (reference compiler.py:456-580, order preserved:
 // mechanic write, pass bookkeeping, effects, score clamp, advancement incl.
 // extra-turn override and must_move, no_legal_actions lookahead, ordered end
-// rules evaluated for the mover, counters)
+// rules evaluated for the mover, counters).  Split in two around the
+// mechanic write so lx_rollout can run a reach-set flood with the whole warp
+// converged between them (apply_step_pre / apply_step_post).
 template <class G>
-__device__ __forceinline__ void apply_step(typename G::St& s, int action, int hint = -1) {
-    const int mover = s.cur;
-    const int phase = s.phase;
-    const bool is_pass = (G::PASS >= 0) && action == G::PASS;
+__device__ __forceinline__ void ply_prologue(typename G::St& s) {
     s.ovr = -1;
     s.samep = 0;
     s.ncached = 0;
@@ -233,15 +232,17 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
         if (!s.mirror_valid) { G::rm_build(s); s.mirror_valid = 1; }
     }
     G::clear_transient(s);
-    if (is_pass) {
-        s.last_kind = 4; s.last_dest = -1; s.last_source = -1; s.last_mover = mover;
-    } else {
-        if constexpr (G::MECH == 0) {
-            G::write_place(s, action, mover, phase);
-        } else {
-            G::apply_move(s, action, mover, hint);
-        }
-    }
+}
+
+template <class G>
+__device__ __forceinline__ void ply_pass_write(typename G::St& s, int mover) {
+    s.last_kind = 4; s.last_dest = -1; s.last_source = -1; s.last_mover = mover;
+}
+
+// everything after the mechanic write (mover / phase: the ply's, unchanged)
+template <class G>
+__device__ __forceinline__ void ply_tail(typename G::St& s, int action, bool is_pass, int mover,
+                                         int phase) {
     if (G::L_PASSING) {
         if (is_pass) {
             s.pass_streak += 1;
@@ -281,6 +282,50 @@ __device__ __forceinline__ void apply_step(typename G::St& s, int action, int hi
     s.cur = next_player;
     s.phase = next_phase;
     if (G::L_TURNPOS) s.pos = next_pos;
+}
+
+template <class G>
+__device__ __forceinline__ void apply_step(typename G::St& s, int action, int hint = -1) {
+    const int mover = s.cur;
+    const int phase = s.phase;
+    const bool is_pass = (G::PASS >= 0) && action == G::PASS;
+    ply_prologue<G>(s);
+    if (is_pass) {
+        ply_pass_write<G>(s, mover);
+    } else {
+        if constexpr (G::MECH == 0) {
+            G::write_place(s, action, mover, phase);
+        } else {
+            G::apply_move(s, action, mover, hint);
+        }
+    }
+    ply_tail<G>(s, action, is_pass, mover, phase);
+}
+
+// the first half of a placement ply up to the reach-set flood (G::SPLIT_FLOOD
+// games): fl receives the flood's inputs (fl.need = 0: no flood)
+template <class G>
+__device__ __forceinline__ void apply_step_pre(typename G::St& s, int action,
+                                               typename G::Flood& fl) {
+    const int mover = s.cur;
+    const int phase = s.phase;
+    const bool is_pass = (G::PASS >= 0) && action == G::PASS;
+    ply_prologue<G>(s);
+    if (is_pass) {
+        ply_pass_write<G>(s, mover);
+        fl.need = 0;
+    } else {
+        G::write_place_pre(s, action, mover, phase, fl);
+    }
+}
+
+// the rest of the ply once fl.f holds the flooded set
+template <class G>
+__device__ __forceinline__ void apply_step_post(typename G::St& s, int action,
+                                                const typename G::Flood& fl) {
+    const bool is_pass = (G::PASS >= 0) && action == G::PASS;
+    if (!is_pass) G::flood_post(s, fl);
+    ply_tail<G>(s, action, is_pass, s.cur, s.phase);
 }
 
 // legality of one action (reference mechanics.py:281-338, 499-512,

@@ -1402,7 +1402,11 @@ class GameLowering(MoveLoweringMixin):
         """write_place tail: grow the placing side's reach sets.  One P1 slot
         and one P2 slot with the same direction plan share a single update
         on side-selected operands, so lanes of a warp with different movers
-        do not diverge."""
+        do not diverge.  With a single update group the split form is also
+        emitted (self.split_flood): write_place_pre leaves the flood's inputs
+        in a Flood record, the rollout floods with the whole warp converged,
+        and flood_post merges the result."""
+        self.split_flood = None
         out = []
         by_side = {}
         for k, (sd, targets, plan) in enumerate(self.slot_info):
@@ -1467,6 +1471,21 @@ class GameLowering(MoveLoweringMixin):
                 {store}
             }}
         }}""")
+            if len(groups) == 1 and os.environ.get("LX_SPLIT_FLOOD", "1") != "0":
+                pre = f"""{head}
+            const BBW a = lx::onehot<W>(cell_bit(cell));
+            fl.need = {need_expr};
+            fl.free_ = lx::andnot(side ? s.own1 : s.own0, R);
+            fl.f = a;
+            fl.side = side;
+        }}"""
+                post = f"""        if (fl.need) {{
+            const int side = fl.side;
+{head.split(chr(10), 1)[1]}
+            R = R | fl.f;
+            {store}
+        }}"""
+                self.split_flood = (pre, post, dil_lw, dil_f)
         return "\n".join(out)
 
     def _need_table(self, plan, grp, cond):
@@ -1496,6 +1515,43 @@ class GameLowering(MoveLoweringMixin):
         flag = ("((__ldg(" + name + f"(cell) + {W}) >> (s1 ? 1 : 0)) & 1u)" if len(grp) == 2
                 else f"(__ldg({name}(cell) + {W}) & 1u)")
         return f"({cond}) && ({flag} || ({loads}) != 0u)"
+
+    def _split_flood_code(self, owner, place_code, place_planes):
+        """Game::SPLIT_FLOOD members (lx_rollout's converged flood): Flood,
+        write_place_pre, flood_post and the lane-word dilation; stubs when
+        the game has no single reach-set update."""
+        sf = getattr(self, "split_flood", None)
+        if sf is None or self.mech_kind != 0:
+            return ("    static constexpr bool SPLIT_FLOOD = false;\n"
+                    "    struct Flood { BBW free_, f; int need, side; };\n"
+                    "    static __device__ __forceinline__ void write_place_pre(St& s, int cell, int mover, int phase, Flood& fl) "
+                    "{ (void)s; (void)cell; (void)mover; (void)phase; fl.need = 0; }\n"
+                    "    static __device__ __forceinline__ void flood_post(St&, const Flood&) {}\n"
+                    "#if defined(__CUDA_ARCH__)\n"
+                    "    static __device__ __forceinline__ lx::LW<W> flood_dil(const lx::LW<W>& x) { return x; }\n"
+                    "#endif\n"
+                    "    static __device__ __forceinline__ BBW flood_dil_bb(const BBW& f) { return f; }")
+        pre, post, dil_lw, dil_f = sf
+        return f"""    static constexpr bool SPLIT_FLOOD = true;
+    struct Flood {{ BBW free_, f; int need, side; }};
+    // write_place without the reach-set flood: its inputs go to fl
+    static __device__ __forceinline__ void write_place_pre(St& s, int cell, int mover, int phase, Flood& fl) {{
+        const int side = {owner};
+{place_code}
+        s.last_kind = 0; s.last_dest = cell; s.last_source = -1; s.last_mover = side;
+        s.ldbp0 = side ? s.ldbp0 : cell;
+        s.ldbp1 = side ? cell : s.ldbp1;
+{place_planes}
+{pre}
+    }}
+    // merge a flooded fl.f into the placing side's reach set
+    static __device__ __forceinline__ void flood_post(St& s, const Flood& fl) {{
+{post}
+    }}
+#if defined(__CUDA_ARCH__)
+    static __device__ __forceinline__ lx::LW<W> flood_dil(const lx::LW<W>& x) {{ return {dil_lw}; }}
+#endif
+    static __device__ __forceinline__ BBW flood_dil_bb(const BBW& f) {{ return {dil_f}; }}"""
 
     def _conn_rebuild_code(self):
         """Reach sets from scratch (start position, lx_import)."""
@@ -1804,6 +1860,9 @@ class GameLowering(MoveLoweringMixin):
 {conn_update}
     }}
 {self.placement_stubs()}"""
+            split_code = self._split_flood_code(owner, place_code, place_planes)
+        else:
+            split_code = self._split_flood_code(None, None, None)
         L = self.layout
         # rollout block shape: 256 threads; resident blocks per SM by board
         # size, from a B200 A/B at 2^22 envs over all 11 corpus games (same
@@ -1870,6 +1929,7 @@ struct Game {{
 {self._bitmap_code()}
 @@CONSTS@@
 @@RM@@
+@@SPLIT@@
 @@HELPERS@@
     static __device__ __forceinline__ void start(St& s) {{
 {chr(10).join(start_code)}
@@ -1914,6 +1974,7 @@ struct Game {{
         nwords = state_words(self.W, NX, self.C, L, nph, self.mech_kind)
         src = src.replace("@@CONSTS@@", em.const_defs())
         src = src.replace("@@RM@@", self._rm_code())
+        src = src.replace("@@SPLIT@@", split_code)
         # the row mirror (2 x (rows + 10) words per thread) fits 48 KB of static
         # shared memory per block at 128 threads, not 256: those games run
         # their per-env kernels and the rollout at 128 threads (4 rollout

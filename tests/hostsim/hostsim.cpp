@@ -98,7 +98,22 @@ SIM_API int64_t sim_playout(int64_t B, const uint64_t* seeds, int max_turns, con
             int hint;
             const int a = lx::sample_action<Game>(s, smix, hint);
             if (a < 0) break;
-            lx::apply_step<Game>(s, a, hint);
+            if constexpr (Game::SPLIT_FLOOD) {
+                // the rollout's split ply: pre, the reach-set flood, post
+                // (sim_masks / sim_transcript exercise the fused apply_step)
+                Game::Flood fl;
+                lx::apply_step_pre<Game>(s, a, fl);
+                if (fl.need) {
+                    typename Game::BBW g = (fl.f | Game::flood_dil_bb(fl.f)) & fl.free_;
+                    while (!lx::equal(g, fl.f)) {
+                        fl.f = g;
+                        g = (fl.f | Game::flood_dil_bb(fl.f)) & fl.free_;
+                    }
+                }
+                lx::apply_step_post<Game>(s, a, fl);
+            } else {
+                lx::apply_step<Game>(s, a, hint);
+            }
             u32 w[lx::Layout<Game>::NQ * 4];
             lx::pack<Game>(s, w);
             lx::unpack<Game>(s, w);
