@@ -1471,7 +1471,11 @@ class GameLowering(MoveLoweringMixin):
                 {store}
             }}
         }}""")
-            if len(groups) == 1 and os.environ.get("LX_SPLIT_FLOOD", "1") != "0":
+            # off by default: measured on the B200 (r2r/r2s,
+            # profiles/r2r_ab_split_flood.jsonl) Hex 52.2 -> 47.2 G (its live
+            # Flood record spills at 80 registers; at 128 registers it only
+            # ties the fused ply), Yavalath +1.5 %
+            if len(groups) == 1 and os.environ.get("LX_SPLIT_FLOOD", "0") != "0":
                 pre = f"""{head}
             const BBW a = lx::onehot<W>(cell_bit(cell));
             fl.need = {need_expr};
