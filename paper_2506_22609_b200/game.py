@@ -25,13 +25,13 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import native
+from . import errors, native
 from .errors import CompileError, EmptyMask
 from .lowering import lower_game
 from .syntax import parse_game
 
 GAMES_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "games")
-MCTS_SHARED_LIMIT = 190 * 1024      # dynamic shared memory per MCTS tree (B200 opt-in 227 KB, less the kernels' static shared buffers)
+MCTS_SHARED_LIMIT = 200 * 1024      # dynamic shared memory per MCTS tree (B200 opt-in 227 KB; the runtime checks it with the kernel's static buffers)
 
 FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
           "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags", "must_move",
@@ -435,11 +435,20 @@ class B200Game:
             arena = torch.empty(n * arena_bytes, dtype=torch.uint8, device="cuda")
         out = torch.empty(3 * n, dtype=torch.int32, device="cuda")   # actions (i64) | status
         acts, status = out[:2 * n].view(torch.int64), out[2 * n:]
-        native.check(native.lib().lx_mcts(
+        st = native.lib().lx_mcts(
             self.handle, roots.words.data_ptr(), n, keys_t.data_ptr(), bud_t.data_ptr(),
             float(exploration), int(rollout_max_turns), logs.data_ptr(), int(logs.numel()),
             pool.data_ptr(), n * nmax, nmax, arena.data_ptr(), arena_bytes, acts.data_ptr(),
-            status.data_ptr(), int(shared), self._stream()))
+            status.data_ptr(), int(shared), self._stream())
+        if st == errors.LX_EINVALID and shared:   # the tree does not fit next to the
+            pool = torch.empty((self._nq, n * nmax, 4), dtype=torch.int32, device="cuda")
+            arena = torch.empty(n * arena_bytes, dtype=torch.uint8, device="cuda")
+            st = native.lib().lx_mcts(     # kernel's static shared buffers: global arena
+                self.handle, roots.words.data_ptr(), n, keys_t.data_ptr(), bud_t.data_ptr(),
+                float(exploration), int(rollout_max_turns), logs.data_ptr(), int(logs.numel()),
+                pool.data_ptr(), n * nmax, nmax, arena.data_ptr(), arena_bytes, acts.data_ptr(),
+                status.data_ptr(), 0, self._stream())
+        native.check(st)
         h = out.cpu().numpy()
         return h[:2 * n].view(np.int64).copy(), h[2 * n:] == 0
 

@@ -134,6 +134,23 @@ def test_device_search_equals_host_search(name, shared, monkeypatch):
     assert np.array_equal(dev, host)
 
 
+def test_device_search_shared_overflow_falls_back(monkeypatch):
+    """A tree that passes the host's size check but does not fit beside the
+    kernel's static shared buffers (lx_mcts returns LX_EINVALID) is searched
+    in the global arena with the same decisions."""
+    g = game("reversi")
+    st = g.init(4, seed=3)
+    rows = ~st.terminated
+    budgets = np.full(4, 400, dtype=np.int64)        # ~245 KB of tree per root
+    salt = np.full(4, np.uint64(5), dtype=np.uint64)
+    search = agents._Search(g, 1.4142135623730951, 40)
+    ref = search.run(st, rows, budgets, salt, device=True)
+    monkeypatch.setattr(lx.game, "MCTS_SHARED_LIMIT", 1 << 30)   # skip the host check
+    got = search.run(st, rows, budgets, salt, device=True)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(got, search.run(st, rows, budgets, salt, device=False))
+
+
 def test_device_search_on_generated_programs():
     """Device and host MCTS agree on programs from the reference's generator
     (movement, mixed phases, passes, transient masks ...)."""
