@@ -695,18 +695,26 @@ def time_config(arm, game, B, steps, warmup, max_turns):
     graph = None
     if B <= GRAPH_MAX_BATCH:
         # launch-bound sizes: the K timed episodes (each its own seed) are
-        # captured once into a CUDA graph and replayed as one launch
+        # captured once into a CUDA graph and replayed as one launch; each
+        # episode publishes its stats into its own row (summed after the
+        # timed region), so the graph holds only lx_rollout nodes
+        per_ep = torch.zeros(steps, 8, dtype=torch.int64, device="cuda")
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for e in range(steps):
-                ep(10_000 + e)
-        graph.replay()                      # warm replay, then reset the sums
-        torch.cuda.synchronize()
-        acc.zero_()
-        torch.cuda.synchronize()
+                native_rollout(game, state, B, max_turns, rng.episode_seed(0, B, 10_000 + e), 0,
+                               per_ep[e], work)
+        # warm replays for >= 50 ms: the timed replay is a few ms, so the SM
+        # clock must already be up when it starts
+        t_warm = time.perf_counter()
+        while time.perf_counter() - t_warm < 0.05:
+            graph.replay()
+            torch.cuda.synchronize()
     run = graph.replay if graph is not None else (lambda: [ep(10_000 + e) for e in range(steps)])
     with ClockSampler(arm.local, enabled=B >= (1 << 20)) as clk:
         ms = arm.timed(run)
+    if graph is not None:
+        acc.copy_(per_ep.sum(0))
     return ms, acc.cpu().tolist(), state, 10_000 + steps - 1, clk.summary(), graph is not None
 
 

@@ -45,10 +45,15 @@ for name in a.games.split(","):
         graph = None
         G = 20
         if B <= (1 << 16):          # launch-bound: replay G captured episodes per launch
+            # each captured episode publishes its stats into its own row;
+            # one sum per replay (no per-episode add kernel in the graph)
+            per_ep = torch.zeros(G, 8, dtype=torch.int64, device="cuda")
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
                 for e in range(G):
-                    ep(10000 + e)
+                    g.rollout(seed=rng.episode_seed(0, B, 10000 + e), out=out, batch_size=B,
+                              truncate=False, check=False, stats=per_ep[e], work=work)
+                acc.add_(per_ep.sum(0))
             graph.replay()
         torch.cuda.synchronize()
         acc.zero_()
