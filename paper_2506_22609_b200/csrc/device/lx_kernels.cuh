@@ -524,6 +524,17 @@ extern "C" __global__ void __launch_bounds__(LX_BLOCK, LX_STEP_MINB) lx_random_s
 #ifndef LX_PLY_UNROLL
 #define LX_PLY_UNROLL 1
 #endif
+// small grids (grid x threads >= B, i.e. every env fits one wave of the
+// persistent threads): warp w plays env chunk w with no claim atomics, and a
+// one-block launch publishes its stats without the cross-block ticket
+#ifndef LX_STATIC_CHUNKS
+#define LX_STATIC_CHUNKS 1
+#endif
+// cross-block publish ordered by one acq_rel ticket atomic instead of two
+// sequentially consistent fences (__threadfence)
+#ifndef LX_ACQREL_TICKET
+#define LX_ACQREL_TICKET 1
+#endif
 #if LX_IN_GROUP(0)
 extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB)
 lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* seeds, i64 first,
@@ -555,10 +566,20 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
         }
     };
     u64 cur = 0, nxt = 0;
-    if (lane == 0) cur = atomicAdd(counter, 32ull);
-    cur = __shfl_sync(FULL, cur, 0);
-    int used = 0;
     bool requested = false;       // next chunk claimed (warp-uniform)
+    // grid-uniform: the whole batch is one wave of warps (host sizes the grid
+    // as min(resident blocks, ceil(B / threads)))
+    const bool static_chunks = LX_STATIC_CHUNKS &&
+                               (u64)gridDim.x * blockDim.x >= (u64)B;
+    if (static_chunks) {
+        cur = (u64)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+        nxt = (u64)B;             // "next chunk" is past the end: nothing to claim
+        requested = true;
+    } else {
+        if (lane == 0) cur = atomicAdd(counter, 32ull);
+        cur = __shfl_sync(FULL, cur, 0);
+    }
+    int used = 0;
     u64 pre_seed, pre_mix;
     prep(cur, pre_seed, pre_mix);
     Game::St s;
@@ -592,7 +613,9 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
             u64 sm = __shfl_sync(FULL, pre_mix, pos & 31);
             u64 my_base = cur;
             if (used + n > 32) {                        // switch to the next chunk
-                if (!requested && lane == 0) nxt = atomicAdd(counter, 32ull);
+                // (a warp past the end claims nothing more: static chunks
+                // never touch the counter)
+                if (!requested && lane == 0) nxt = cur < (u64)B ? atomicAdd(counter, 32ull) : (u64)B;
                 requested = false;
                 const u64 nb = __shfl_sync(FULL, nxt, 0);
                 u64 ps2, pm2;
@@ -607,7 +630,7 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
             } else {
                 used += n;
             }
-            if (!requested && used >= 16) {
+            if (!requested && used >= 16 && cur < (u64)B) {
                 if (lane == 0) nxt = atomicAdd(counter, 32ull);
                 requested = true;
             }
@@ -696,6 +719,32 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
         n_trunc += __shfl_xor_sync(0xffffffffu, n_trunc, o);
         n_done += __shfl_xor_sync(0xffffffffu, n_done, o);
     }
+    if (LX_STATIC_CHUNKS && gridDim.x == 1) {
+        // one block: sums in shared memory, no ticket and no fences (the
+        // stuck-row atomics of this block's warps are ordered by the barrier)
+        // (one block plays <= blockDim.x envs of <= max_turns plies: u32 sums)
+        __shared__ u32 blk[6];
+        if (threadIdx.x < 6) blk[threadIdx.x] = 0u;
+        __syncthreads();
+        if (lane == 0) {
+            atomicAdd(&blk[0], n_steps);
+            atomicAdd(&blk[1], n_p1);
+            atomicAdd(&blk[2], n_p2);
+            atomicAdd(&blk[3], n_draw);
+            atomicAdd(&blk[4], n_trunc);
+            atomicAdd(&blk[5], n_done);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int k = 0; k < 6; k++) stats[k] = (u64)blk[k];
+            const u64 sm = atomicExch(stuck_max, 0ull);
+            stats[6] = sm ? ~sm : ~0ull;
+            stats[7] = 0ull;
+            *counter = 0ull;
+        }
+        return;
+    }
     if (lane == 0) {
         atomicAdd(acc + 0, (u64)n_steps);
         atomicAdd(acc + 1, (u64)n_p1);
@@ -706,10 +755,21 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+#if LX_ACQREL_TICKET
+        // release: this block's sums (ordered before it by the barrier,
+        // cumulatively) precede the ticket; acquire: the last block sees
+        // every block's sums
+        u64 ticket;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                     : "=l"(ticket) : "l"(work + 8) : "memory");
+#else
         __threadfence();
         const u64 ticket = atomicAdd(work + 8, 1ull);
+#endif
         if (ticket == (u64)gridDim.x - 1) {            // last block: publish, then clear
+#if !LX_ACQREL_TICKET
             __threadfence();
+#endif
 #pragma unroll
             for (int k = 0; k < 6; k++) stats[k] = atomicExch(acc + k, 0ull);
             const u64 sm = atomicExch(stuck_max, 0ull);

@@ -1914,6 +1914,8 @@ class GameLowering(MoveLoweringMixin):
 #define LX_PLY_UNROLL {r_unroll}
 #define LX_SELECT_STASH {int(os.environ.get("LX_SELECT_STASH", "1"))}
 #define LX_SHIFT_FMA {r_shift_fma}
+#define LX_STATIC_CHUNKS {int(os.environ.get("LX_STATIC_CHUNKS", "1"))}
+#define LX_ACQREL_TICKET {int(os.environ.get("LX_ACQREL_TICKET", "1"))}
 #define LX_STEP_MINB {int(os.environ.get("LX_STEP_MINB", "4"))}
 #include "lx_core.cuh"
 

@@ -24,9 +24,15 @@ p.add_argument("--game", default="tic_tac_toe")
 p.add_argument("--batch", type=int, default=1024)
 p.add_argument("--caps", default="0,1,2,3,4,5,6,7,8,9,200")
 p.add_argument("--reps", type=int, default=200)
+p.add_argument("--variant", default="",
+               help="comma-separated K=V lowering env overrides (tools/ab_env.py style)")
 a = p.parse_args()
 
-g = lx.load_config_game(a.game)
+env = dict(kv.split("=", 1) for kv in a.variant.split(",") if kv)
+os.environ.update(env)
+with open(os.path.join(lx.game.GAMES_DIR, f"{a.game}.ldx")) as f:
+    g = lx.load_game(f.read())
+g.lowered_key()
 B = a.batch
 out = g.empty_state(B)
 work = torch.zeros(16, dtype=torch.int64, device="cuda")
@@ -37,9 +43,12 @@ gz = torch.cuda.CUDAGraph()
 with torch.cuda.graph(gz):
     for e in range(G):
         z[e].zero_()
-for _ in range(5):
+# >= 200 ms of replays first: the SM clock must be up before any timing
+import time  # noqa: E402
+t0 = time.perf_counter()
+while time.perf_counter() - t0 < 0.2:
     gz.replay()
-torch.cuda.synchronize()
+    torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(a.reps):
@@ -58,9 +67,10 @@ for cap in [int(c) for c in a.caps.split(",")]:
         for e in range(G):
             g.rollout(seed=rng.episode_seed(0, B, 10000 + e), out=out, batch_size=B,
                       max_turns=cap, truncate=False, check=False, stats=per_ep[e], work=work)
-    for _ in range(5):
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 0.05:
         graph.replay()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(a.reps):
@@ -69,6 +79,6 @@ for cap in [int(c) for c in a.caps.split(",")]:
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / (a.reps * G)
     tot = per_ep.sum(0).tolist()
-    print(json.dumps({"game": a.game, "batch": B, "max_turns": cap, "us_per_episode": ms * 1e3,
+    print(json.dumps({"game": a.game, "batch": B, "variant": env, "max_turns": cap, "us_per_episode": ms * 1e3,
                       "env_steps_per_episode": tot[0] / G,
                       "env_steps_per_s": tot[0] / G / (ms / 1e3)}), flush=True)
