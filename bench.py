@@ -323,6 +323,8 @@ def run_distributed(args, arm):
     extras = {}
     if not args.no_extras:
         extras["e2e"] = arm.e2e()
+        if hasattr(arm, "e2e_host"):
+            extras["e2e_c_abi"] = arm.e2e_host()
     if rank == 0 and not args.no_extras:
         extras.update(arm.extras(value, ms_max / args.steps, clk.summary().get("sm_mhz"), tot))
     line = None
@@ -415,6 +417,10 @@ class GpuArm:
     def e2e(self):
         return measure_e2e(self.args, self.game, self.rng, self.B, self.B_total, self.first,
                            self.world_size)
+
+    def e2e_host(self):
+        return measure_e2e_host(self.args, self.game, self.rng, self.B, self.B_total, self.first,
+                                self.world_size)
 
     def extras(self, value, ms_step, clock_mhz, totals):
         out = measure_extras(self.args, self.game, self.lx, self.rng, self.B, self.B_total,
@@ -528,6 +534,52 @@ def measure_e2e(args, game, rng, B, B_total, first, ws, steps=None):
             "path": "B200Game.rollout(seeds=host->device) + outcomes/stats device->host, "
                     "double-buffered over H2D / compute / D2H streams, every rank on its "
                     "own shard, max wall time over ranks"}
+
+
+def measure_e2e_host(args, game, rng, B, B_total, first, ws, steps=None):
+    """e2e through the C-ABI host-buffer call lx_playout_host (what a numpy /
+    ctypes binding of the reference's _run_episode calls): every step passes
+    its episode's per-env seeds in pinned host memory and gets the per-env
+    outcomes and the stats back in host memory; one synchronous call per
+    step, the seed upload overlapped with the play inside the call.  Σ env
+    steps over ranks ÷ max over ranks of the host wall time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_22609_b200 import shard
+    K = steps if steps is not None else max(3, min(args.steps, 30))
+    WU = 2
+    n_it = K + WU
+    seeds_h = [torch.from_numpy(rng.spawn_seeds(rng.episode_seed(0, B_total, 30000 + e), B, first)
+                                .view("int64")).pin_memory() for e in range(n_it)]
+    outc_h = [torch.empty(B, dtype=torch.int8).pin_memory() for _ in range(n_it)]
+    stats_h = [torch.zeros(8, dtype=torch.int64).pin_memory() for _ in range(n_it)]
+
+    def step(it):
+        game.playout_host(seeds=seeds_h[it], outcomes=outc_h[it], stats=stats_h[it],
+                          max_turns=args.max_turns, truncate=True)
+    for it in range(WU):
+        step(it)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for it in range(WU, n_it):
+        step(it)
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        dist.barrier()
+    steps_done = sum(int(stats_h[it][0]) for it in range(WU, n_it))
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    n = torch.tensor([steps_done], dtype=torch.int64, device="cuda")
+    shard.max_over_ranks(t)
+    shard.reduce_stats(n)
+    return {"value": int(n.item()) / float(t.item()), "unit": UNIT,
+            "h2d_bytes_per_step": B * 8 * ws, "d2h_bytes_per_step": (B + 64) * ws,
+            "steps_timed": K,
+            "path": "lx_playout_host (C-ABI, host buffers): pinned host seeds in, host outcomes "
+                    "+ stats out, one synchronous call per step, seeds streamed up while the "
+                    "rollout plays"}
 
 
 def rollout_roofline(game, value, totals, clock_mhz):
@@ -788,6 +840,8 @@ def measure_per_config(arm, value, ms_step, totals, head_extras):
                                      "draws": tot[3], "envs": tot[5]},
                           "clocks": clk,
                           "roofline": rollout_roofline(game, val, tot, clk.get("sm_mhz")),
+                          "e2e_c_abi": measure_e2e_host(args, game, arm.rng, B, B, 0, 1,
+                                                        steps=min(steps, 12)),
                           "e2e": measure_e2e(args, game, arm.rng, B, B, 0, 1,
                                              steps=min(steps, 12))})
         entry["unit"] = UNIT

@@ -194,6 +194,36 @@ int lx_rollout(const lx_game *g, void *state, int64_t B, int max_turns, int mode
                const uint64_t *seeds, int64_t first_index, uint64_t *stats, void *work,
                int8_t *outcomes, int32_t *turns, int check, int64_t *stuck_row, void *stream);
 
+/* One batch episode with HOST buffers: what a numpy / ctypes caller of the
+   reference's random-play loop binds (evaluation._run_episode,
+   evaluation.py:197-211: init(batch, seed) then play to the end; and
+   engine.playout_random, engine.py:123-163: its outcomes and move counts).
+   Envs start from seeds[i] (host (B,) uint64, e.g. spawn_seeds(seed, B)) or,
+   when seeds is NULL, from spawn(seed, first_index + i).  Host outputs, any
+   but stats may be NULL: outcomes (B,) int8 (0 draw, 1 P1, 2 P2), turns (B,)
+   int32 final move_count, stats u64[8] as lx_rollout's.  state (device,
+   NQ*16*B bytes, or NULL) receives the final states.  flags:
+     LX_PLAYOUT_TRUNCATE     envs reaching max_turns end as truncated draws
+                             (engine.py:156-160); without it they stop there
+                             unfinished (_run_episode)
+     LX_PLAYOUT_UPLOAD_FIRST upload all seeds before the launch (no overlap)
+   The handle owns the device scratch (grown to the largest B seen; calls on
+   one handle serialize).  Batches of >= LX_PLAYOUT_STREAM_MIN envs stream
+   their seeds up in <= 64 pieces on a copy stream while the rollout already
+   plays (each warp waits only for its chunk's piece), so the upload overlaps
+   the play; the call returns once the outputs are in host memory.  Pinned
+   host memory (cudaHostAlloc / torch pin_memory) gets full PCIe bandwidth;
+   pageable memory works without the overlap.  A live env with no legal
+   action and no pass -> LX_EEMPTY_MASK (*stuck_row = lowest such env), the
+   outputs still written (engine.py:142-147). */
+#define LX_PLAYOUT_TRUNCATE 1
+#define LX_PLAYOUT_UPLOAD_FIRST 2
+#define LX_PLAYOUT_STREAM_MIN 65536
+int lx_playout_host(const lx_game *g, int64_t B, int max_turns, int flags, uint64_t seed,
+                    const uint64_t *seeds, int64_t first_index, int8_t *outcomes,
+                    int32_t *turns, uint64_t *stats, void *state, int64_t *stuck_row,
+                    void *stream);
+
 /* PGX-style environment step (LudaxEnvironment.step; BASELINE north star),
    one launch per ply.  flags (LX_ENV_*):
      STEP       apply one ply to live rows (else only refresh the outputs)

@@ -19,6 +19,18 @@
 
 namespace lx {
 
+__device__ __forceinline__ u64 globaltimer_ns() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ u32 ld_acquire_gpu(const u32* p) {
+    u32 v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <class G>
 __device__ __forceinline__ void load_state(typename G::St& s, const u32* __restrict__ st,
                                            i64 B, i64 i) {
@@ -536,13 +548,22 @@ extern "C" __global__ void __launch_bounds__(LX_BLOCK, LX_STEP_MINB) lx_random_s
 #define LX_ACQREL_TICKET 1
 #endif
 #if LX_IN_GROUP(0)
-extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB)
-lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* seeds, i64 first,
-           u64* stats, u64* work, signed char* outcomes, int* turns) {
+namespace lx {
+template <bool STREAM>
+__device__ __forceinline__ void rollout_body(u32* st, i64 B, int max_turns, int mode,
+                                             u64 seed_base, const u64* seeds, i64 first,
+                                             u64* stats, u64* work, signed char* outcomes,
+                                             int* turns, const u32* ready) {
     // work (u64[16], zero on entry, left zero on exit): [0] env-chunk counter,
     // [1] ~(lowest stuck row) by atomicMax (0 = none), [2..7] stats being
-    // accumulated, [8] finished-block ticket.  The last block to finish moves
-    // the sums to `stats` and clears `work`, so a launch needs no memsets.
+    // accumulated, [8] finished-block ticket, [9] seed-upload stall flag.  The
+    // last block to finish moves the sums to `stats` and clears `work`, so a
+    // launch needs no memsets.
+    // STREAM (lx_rollout_streamed): the seeds are still being uploaded
+    // (lx_playout_host): *ready counts the 32-env chunks already in HBM (the
+    // copy stream writes it after each piece), so a warp waits for its chunk
+    // before reading the seeds -- the upload overlaps the play instead of
+    // preceding it.
     u64* counter = work;
     u64* stuck_max = work + 1;
     u64* acc = work + 2;
@@ -560,8 +581,28 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
         const i64 j = (i64)(base + lane);
         ps = 0;
         pm = 0;
+        if (STREAM && (mode & 1) && base < (u64)B) {                 // warp-uniform
+            const u64 last = base + 31 < (u64)B ? base + 31 : (u64)B - 1;
+            const u32 need = (u32)(last >> 5) + 1u;
+            if (lane == 0) {
+                // bounded: after 4 s the launch gives up waiting (sticky flag,
+                // reported in stats[7]) instead of hanging on a stalled copy
+                const u64 t0 = lx::globaltimer_ns();
+                volatile const u64* stalled = work + 9;
+                while (lx::ld_acquire_gpu(ready) < need && *stalled == 0ull) {
+                    __nanosleep(128);
+                    if (lx::globaltimer_ns() - t0 > 4000000000ull) {
+                        atomicOr(work + 9, 1ull);
+                        break;
+                    }
+                }
+            }
+            __syncwarp();
+        }
         if ((mode & 1) && j < B) {
-            ps = seeds ? seeds[j] : lx::mix64(base_mix ^ (u64)(first + j));
+            // streamed seeds are read from L2 (the DMA wrote them after launch)
+            ps = seeds ? (STREAM ? __ldcg(seeds + j) : seeds[j])
+                       : lx::mix64(base_mix ^ (u64)(first + j));
             pm = lx::seed_mix(ps);
         }
     };
@@ -740,7 +781,7 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
             for (int k = 0; k < 6; k++) stats[k] = (u64)blk[k];
             const u64 sm = atomicExch(stuck_max, 0ull);
             stats[6] = sm ? ~sm : ~0ull;
-            stats[7] = 0ull;
+            stats[7] = atomicExch(work + 9, 0ull);       // seed-upload stall (0: none)
             *counter = 0ull;
         }
         return;
@@ -774,12 +815,31 @@ lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* se
             for (int k = 0; k < 6; k++) stats[k] = atomicExch(acc + k, 0ull);
             const u64 sm = atomicExch(stuck_max, 0ull);
             stats[6] = sm ? ~sm : ~0ull;               // lowest stuck row, ~0 = none
-            stats[7] = 0ull;
+            stats[7] = atomicExch(work + 9, 0ull);       // seed-upload stall (0: none)
             atomicExch(counter, 0ull);
             atomicExch(work + 8, 0ull);
         }
     }
 }
+
+}  // namespace lx
+
+extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB)
+lx_rollout(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* seeds, i64 first,
+           u64* stats, u64* work, signed char* outcomes, int* turns) {
+    lx::rollout_body<false>(st, B, max_turns, mode, seed_base, seeds, first, stats, work,
+                            outcomes, turns, nullptr);
+}
+
+// the same rollout while lx_playout_host streams the seeds up (see STREAM)
+extern "C" __global__ void __launch_bounds__(LX_ROLLOUT_THREADS, LX_ROLLOUT_MINB)
+lx_rollout_streamed(u32* st, i64 B, int max_turns, int mode, u64 seed_base, const u64* seeds,
+                    i64 first, u64* stats, u64* work, signed char* outcomes, int* turns,
+                    const u32* ready) {
+    lx::rollout_body<true>(st, B, max_turns, mode, seed_base, seeds, first, stats, work,
+                           outcomes, turns, ready);
+}
+
 #endif
 
 // MCTS expansion + rollout, one thread per expanded child (reference

@@ -636,6 +636,63 @@ class B200Game:
             state._touch()
         return state, stats
 
+    def playout_host(self, batch_size=None, seed=0, seeds=None, first_index=0, max_turns=200,
+                     truncate=True, outcomes=True, turns=False, stats=None, out=None,
+                     upload_first=False):
+        """One batch episode through the host-buffer C-ABI call lx_playout_host
+        (the reference's evaluation._run_episode / engine.playout_random as a
+        numpy caller binds them, evaluation.py:197-211, engine.py:123-163):
+        per-env seeds in host memory (numpy or a pinned torch CPU tensor; None:
+        spawn(seed, first_index + i)), outcomes / final move counts / stats
+        back in host memory.  ``outcomes`` / ``turns``: True to allocate,
+        a host array to fill, or False; ``out``: optional DeviceState for the
+        final states.  The seed upload overlaps the play (see the header).
+        Returns (outcomes or None, turns or None, stats (8,) uint64)."""
+        torch = _torch()
+
+        def host_ptr(a, dtype, n, what):
+            if a is None or a is False:
+                return None, None
+            if a is True:
+                a = np.empty(n, dtype=dtype)
+            if isinstance(a, torch.Tensor):
+                if a.is_cuda or not a.is_contiguous() or a.numel() != n or \
+                        a.element_size() != np.dtype(dtype).itemsize:
+                    raise ValueError(f"{what}: need a contiguous host tensor of {n} "
+                                     f"{np.dtype(dtype).name}")
+                return a, a.data_ptr()
+            a = np.asarray(a)
+            if not (a.flags.c_contiguous and a.size == n and a.dtype.itemsize ==
+                    np.dtype(dtype).itemsize):
+                raise ValueError(f"{what}: need a contiguous host array of {n} "
+                                 f"{np.dtype(dtype).name}")
+            return a, a.ctypes.data
+        if batch_size is not None:
+            B = int(batch_size)
+        elif seeds is not None:
+            B = len(seeds)
+        elif out is not None:
+            B = out.batch_size
+        else:
+            raise ValueError("batch_size, seeds or out is required")
+        if seeds is not None and not isinstance(seeds, torch.Tensor):
+            seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        seeds_a, seeds_p = host_ptr(seeds, np.uint64, B, "seeds")
+        outc_a, outc_p = host_ptr(outcomes, np.int8, B, "outcomes")
+        turns_a, turns_p = host_ptr(turns, np.int32, B, "turns")
+        stats_a, stats_p = host_ptr(stats if stats is not None else True, np.uint64, 8, "stats")
+        flags = (1 if truncate else 0) | (2 if upload_first else 0)
+        stuck = ctypes.c_int64(-1)
+        st = native.lib().lx_playout_host(
+            self.handle, B, int(max_turns), flags, int(seed) & (2 ** 64 - 1), seeds_p,
+            int(first_index), outc_p, turns_p, stats_p,
+            out.words.data_ptr() if out is not None else None, ctypes.byref(stuck),
+            self._stream())
+        if out is not None:
+            out._touch()
+        native.check(st, stuck.value)
+        return outc_a, turns_a, stats_a
+
     def with_seeds(self, state, seeds):
         """Copy of ``state`` whose rows draw from new RNG streams (the MCTS
         rollout re-keying, reference agents.py:229-233)."""

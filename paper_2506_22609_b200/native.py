@@ -41,7 +41,8 @@ class RefState(ctypes.Structure):
 EXPORTS = ("lx_version", "lx_last_error", "lx_game_create", "lx_bind_device", "lx_compile_only",
            "lx_cache_key", "lx_game_info_get", "lx_game_destroy", "lx_init", "lx_legal",
            "lx_sample", "lx_truncate", "lx_set_seeds", "lx_step", "lx_random_step", "lx_rollout",
-           "lx_export", "lx_import", "lx_observe", "lx_env_step", "lx_expand", "lx_mcts")
+           "lx_export", "lx_import", "lx_observe", "lx_env_step", "lx_expand", "lx_mcts",
+           "lx_playout_host")
 
 
 def build_native():
@@ -79,6 +80,8 @@ def lib():
     L.lx_random_step.argtypes = [vp, vp, i64, i32, vp, vp]
     L.lx_rollout.argtypes = [vp, vp, i64, i32, i32, u64, vp, i64, vp, vp, vp, vp, i32,
                              ctypes.POINTER(i64), vp]
+    L.lx_playout_host.argtypes = [vp, i64, i32, i32, u64, vp, i64, vp, vp, vp, vp,
+                                  ctypes.POINTER(i64), vp]
     L.lx_expand.argtypes = [vp, vp, i64, vp, vp, vp, i64, vp, ctypes.c_int, vp, vp, vp, vp]
     L.lx_mcts.argtypes = [vp, vp, i64, vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.c_int,
                           vp, i64, ctypes.c_int, vp, i64, vp, vp, ctypes.c_int, vp]

@@ -3,7 +3,8 @@
  * memory).  Every buffer is sized from lx_game_info alone:
  *   bind device -> create -> info -> init -> fused rollout -> export
  * and the exported reference-layout arrays are written to a file that
- * tests/test_c_abi.py compares with the CPU oracle.
+ * tests/test_c_abi.py compares with the CPU oracle; then the same episode
+ * once more through lx_playout_host with host buffers only.
  *
  *   c_abi_smoke <lowered.cu> <name> <include_dir> <cache_dir> <B> <seed> <out.bin>
  */
@@ -119,6 +120,32 @@ int main(int argc, char **argv) {
     bad |= dump(f, "seeds", ref.seeds, (size_t)B * 8);
     bad |= dump(f, "stats", stats, 8 * sizeof(uint64_t));
     fclose(f);
+
+    /* the same episode through the host-buffer call: no device memory on the
+       caller's side at all (seeds spawned from `seed`, outcomes / move counts /
+       stats written to host arrays) */
+    int8_t *h_out = (int8_t *)malloc((size_t)B);
+    int32_t *h_turns = (int32_t *)malloc((size_t)B * 4);
+    uint64_t h_stats[8];
+    CHECK(lx_playout_host(g, B, 200, LX_PLAYOUT_TRUNCATE, seed, NULL, 0, h_out, h_turns, h_stats,
+                          NULL, &stuck, NULL));
+    f = fopen(argv[7], "ab");
+    if (!f) return 5;
+    unsigned long long len = (unsigned long long)B;
+    fprintf(f, "host_outcome\n");
+    fwrite(&len, sizeof(len), 1, f);
+    fwrite(h_out, 1, (size_t)B, f);
+    len = (unsigned long long)B * 4;
+    fprintf(f, "host_move_count\n");
+    fwrite(&len, sizeof(len), 1, f);
+    fwrite(h_turns, 1, (size_t)B * 4, f);
+    len = sizeof(h_stats);
+    fprintf(f, "host_stats\n");
+    fwrite(&len, sizeof(len), 1, f);
+    fwrite(h_stats, 1, sizeof(h_stats), f);
+    fclose(f);
+    free(h_out);
+    free(h_turns);
     CHECK(lx_game_destroy(g));
     return bad ? 6 : 0;
 }

@@ -75,3 +75,7 @@ def test_c_caller_rollout_matches_oracle(tmp_path, name, B):
         assert np.array_equal(a, want[f]), f
     stats = np.frombuffer(got["stats"], np.uint64)
     assert int(stats[0]) == steps and int(stats[5]) == B
+    # lx_playout_host (host buffers only) plays the same episode
+    assert np.array_equal(np.frombuffer(got["host_outcome"], np.int8), want["outcome"])
+    assert np.array_equal(np.frombuffer(got["host_move_count"], np.int32), want["move_count"])
+    assert np.array_equal(np.frombuffer(got["host_stats"], np.uint64)[:6], stats[:6])
