@@ -62,6 +62,12 @@ __device__ __forceinline__ i64 gtid() { return (i64)blockIdx.x * blockDim.x + th
 // 4 mask bits -> 4 bytes of 0/1
 __device__ __forceinline__ u32 spread4(u32 x) { return ((x & 0xfu) * 0x00204081u) & 0x01010101u; }
 
+// bool-mask rows of a full warp written from one concatenated bit stream
+// (write_mask_rows; 0: the per-piece row walk, for A/B)
+#ifndef LX_MASK_STREAM
+#define LX_MASK_STREAM 1
+#endif
+
 // Stage the lane's legal-mask row as a bit vector in cell order (cells, then
 // the pass column) in a per-warp shared-memory block of 32 rows x STRIDE
 // words; returns the block.  Every lane of the warp must call it.
@@ -109,6 +115,42 @@ __device__ __forceinline__ void write_mask_rows(unsigned char* __restrict__ mask
     const int nrows = left < 32 ? (int)left : 32;
     const int bytes = nrows * A;
     unsigned char* base = mask + i0 * (i64)A;
+#if LX_MASK_STREAM
+    // (A <= 128: the stream block stays small beside the big boards' row
+    // mirror in the 48 KB of static shared memory)
+    if (A <= 128 && nrows == 32) {
+        // full warp: concatenate the 32 rows into one bit stream (row r at bit
+        // r*A; each lane ORs its row's words in at their offset), so the 2A
+        // 16-byte output pieces are 16-aligned halves of stream words -- no
+        // row-crossing walk per piece (r2z ncu: that walk was ~40 % of the C4
+        // env step's instructions)
+        constexpr int SW = A <= 128 ? A + 1 : 1;
+        __shared__ u32 stream_all[(LX_BLOCK / 32) * SW];
+        u32* S = stream_all + (threadIdx.x >> 5) * SW;
+        for (int k = (int)lane; k < SW; k += 32) S[k] = 0u;
+        __syncwarp();
+        const u32* mine = rows + lane * STRIDE;
+        const int q0 = (int)lane * A;
+#pragma unroll
+        for (int j = 0; j < NW; j++) {
+            const u32 v = mine[j];
+            if (v) {
+                const int q = q0 + 32 * j;
+                const int w = q >> 5, sh = q & 31;
+                atomicOr(&S[w], v << sh);
+                if (sh) atomicOr(&S[w + 1], v >> (32 - sh));
+            }
+        }
+        __syncwarp();
+        for (int k = (int)lane; k < 2 * A; k += 32) {
+            const u32 v = (S[k >> 1] >> ((k & 1) << 4)) & 0xffffu;
+            *reinterpret_cast<uint4*>(base + 16 * k) =
+                make_uint4(spread4(v), spread4(v >> 4), spread4(v >> 8), spread4(v >> 12));
+        }
+        __syncwarp();
+        return;
+    }
+#endif
     for (int p0 = (int)lane * 16; p0 < bytes; p0 += 32 * 16) {
         const int nb = bytes - p0 < 16 ? bytes - p0 : 16;
         u32 v = 0u;

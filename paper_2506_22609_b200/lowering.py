@@ -1916,6 +1916,7 @@ class GameLowering(MoveLoweringMixin):
 #define LX_SHIFT_FMA {r_shift_fma}
 #define LX_STATIC_CHUNKS {int(os.environ.get("LX_STATIC_CHUNKS", "1"))}
 #define LX_ACQREL_TICKET {int(os.environ.get("LX_ACQREL_TICKET", "1"))}
+#define LX_MASK_STREAM {int(os.environ.get("LX_MASK_STREAM", "1"))}
 #define LX_STEP_MINB {int(os.environ.get("LX_STEP_MINB", "4"))}
 #include "lx_core.cuh"
 

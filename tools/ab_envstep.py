@@ -60,5 +60,12 @@ for var in (a.variant or [""]):
         torch.cuda.synchronize()
         out[f"env_{fmt}_G"] = B / (ev0.elapsed_time(ev1) / a.plies / 1e3) / 1e9
         out[f"digest_{fmt}"] = s.game_state.digest() if B <= (1 << 20) else None
+        # checksum of the last ply's mask (equal across variants = same masks)
+        m = s.mask_bool()
+        if m is not None:
+            mi = m.to(torch.int64).reshape(B, -1)
+            w = torch.arange(1, mi.shape[1] + 1, device=mi.device, dtype=torch.int64)
+            out[f"mask_sum_{fmt}"] = int((mi * w).sum().item() +
+                                         (mi.sum(1) * torch.arange(B, device=mi.device)).sum().item())
     res["variants"].append(out)
 print(json.dumps(res))
