@@ -758,13 +758,20 @@ def time_config(arm, game, B, steps, warmup, max_turns):
                                per_ep[e], work)
         # warm replays for >= 50 ms: the timed replay is a few ms, so the SM
         # clock must already be up when it starts
-        t_warm = time.perf_counter()
+        t_warm, n_warm = time.perf_counter(), 0
         while time.perf_counter() - t_warm < 0.05:
             graph.replay()
             torch.cuda.synchronize()
-    run = graph.replay if graph is not None else (lambda: [ep(10_000 + e) for e in range(steps)])
-    with ClockSampler(arm.local, enabled=B >= (1 << 20)) as clk:
-        ms = arm.timed(run)
+            n_warm += 1
+        # the timed region repeats the replay for >= 0.25 s so the clock
+        # sampler sees it (the episodes read no input but their seeds)
+        reps = max(1, int(0.25 / ((time.perf_counter() - t_warm) / n_warm)) + 1)
+    else:
+        reps = 1
+    run = ((lambda: [graph.replay() for _ in range(reps)]) if graph is not None
+           else (lambda: [ep(10_000 + e) for e in range(steps)]))
+    with ClockSampler(arm.local) as clk:
+        ms = arm.timed(run) / reps
     if graph is not None:
         acc.copy_(per_ep.sum(0))
     return ms, acc.cpu().tolist(), state, 10_000 + steps - 1, clk.summary(), graph is not None

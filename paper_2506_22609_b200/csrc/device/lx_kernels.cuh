@@ -584,6 +584,12 @@ extern "C" __global__ void __launch_bounds__(LX_BLOCK, LX_STEP_MINB) lx_random_s
 #ifndef LX_STATIC_CHUNKS
 #define LX_STATIC_CHUNKS 1
 #endif
+// grids of 2..8 blocks launched as one cluster publish through distributed
+// shared memory (the host sets the cluster dimension; without it the ticket
+// path below runs)
+#ifndef LX_CLUSTER_PUBLISH
+#define LX_CLUSTER_PUBLISH 1
+#endif
 // cross-block publish ordered by one acq_rel ticket atomic instead of two
 // sequentially consistent fences (__threadfence)
 #ifndef LX_ACQREL_TICKET
@@ -591,6 +597,124 @@ extern "C" __global__ void __launch_bounds__(LX_BLOCK, LX_STEP_MINB) lx_random_s
 #endif
 #if LX_IN_GROUP(0)
 namespace lx {
+// End of a rollout launch: warp sums -> stats (u64[8]) and a cleared work
+// buffer.  Out of line by default so that the epilogue's code does not
+// perturb the register allocation of the ply loop (inlined, the cluster path
+// cost C4 three registers: 64 -> 67, one block per SM fewer); the row-mirror
+// games inline it (Pente: 124 registers out of line, 103 inlined = one more
+// 128-thread block per SM).  The lowering picks LX_PUBLISH_INLINE per game.
+#ifndef LX_PUBLISH_INLINE
+#define LX_PUBLISH_INLINE 0
+#endif
+#if LX_PUBLISH_INLINE
+#define LX_PUBLISH_ATTR __forceinline__
+#else
+#define LX_PUBLISH_ATTR __noinline__
+#endif
+__device__ LX_PUBLISH_ATTR void publish_stats(u32 n_steps, u32 n_p1, u32 n_p2, u32 n_draw,
+                                           u32 n_trunc, u32 n_done, u64* stats, u64* work) {
+    u64* counter = work;
+    u64* stuck_max = work + 1;
+    u64* acc = work + 2;
+    const unsigned lane = threadIdx.x & 31u;
+    // warp reduce, one atomic per warp per counter
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        n_steps += __shfl_xor_sync(0xffffffffu, n_steps, o);
+        n_p1 += __shfl_xor_sync(0xffffffffu, n_p1, o);
+        n_p2 += __shfl_xor_sync(0xffffffffu, n_p2, o);
+        n_draw += __shfl_xor_sync(0xffffffffu, n_draw, o);
+        n_trunc += __shfl_xor_sync(0xffffffffu, n_trunc, o);
+        n_done += __shfl_xor_sync(0xffffffffu, n_done, o);
+    }
+    // a grid that is one block, or one thread-block cluster (the host
+    // launches grids of 2..8 blocks as a single cluster): per-block sums in
+    // shared memory, rank 0 adds the cluster's blocks through distributed
+    // shared memory -- no ticket, no fences, no global atomics
+    // (a block plays <= blockDim.x envs of <= max_turns plies: u32 sums)
+    u32 ncta = 1;
+    if (LX_CLUSTER_PUBLISH && gridDim.x > 1 && gridDim.x <= 8)
+        asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
+    if ((LX_STATIC_CHUNKS && gridDim.x == 1) || (ncta > 1 && ncta == gridDim.x)) {
+        __shared__ u32 blk[6];
+        if (threadIdx.x < 6) blk[threadIdx.x] = 0u;
+        __syncthreads();
+        if (lane == 0) {
+            atomicAdd(&blk[0], n_steps);
+            atomicAdd(&blk[1], n_p1);
+            atomicAdd(&blk[2], n_p2);
+            atomicAdd(&blk[3], n_draw);
+            atomicAdd(&blk[4], n_trunc);
+            atomicAdd(&blk[5], n_done);
+        }
+        if (ncta > 1) {
+            // release/acquire at cluster scope: every block's sums and stuck /
+            // stall atomics are visible to rank 0 after the barrier
+            asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                         "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+            if (blockIdx.x == 0 && threadIdx.x < 6) {
+                const u32 local = (u32)__cvta_generic_to_shared(&blk[threadIdx.x]);
+                u64 sum = 0;
+                for (u32 r = 0; r < ncta; r++) {
+                    u32 remote, v;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                                 : "=r"(remote) : "r"(local), "r"(r));
+                    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
+                    sum += v;
+                }
+                stats[threadIdx.x] = sum;
+            }
+        } else {
+            __syncthreads();
+            if (threadIdx.x < 6) stats[threadIdx.x] = (u64)blk[threadIdx.x];
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            const u64 sm = atomicExch(stuck_max, 0ull);
+            stats[6] = sm ? ~sm : ~0ull;
+            stats[7] = atomicExch(work + 9, 0ull);       // seed-upload stall (0: none)
+            *counter = 0ull;
+        }
+        if (ncta > 1)                  // keep every block's shared memory until rank 0 read it
+            asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                         "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
+    if (lane == 0) {
+        atomicAdd(acc + 0, (u64)n_steps);
+        atomicAdd(acc + 1, (u64)n_p1);
+        atomicAdd(acc + 2, (u64)n_p2);
+        atomicAdd(acc + 3, (u64)n_draw);
+        atomicAdd(acc + 4, (u64)n_trunc);
+        atomicAdd(acc + 5, (u64)n_done);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#if LX_ACQREL_TICKET
+        // release: this block's sums (ordered before it by the barrier,
+        // cumulatively) precede the ticket; acquire: the last block sees
+        // every block's sums
+        u64 ticket;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                     : "=l"(ticket) : "l"(work + 8) : "memory");
+#else
+        __threadfence();
+        const u64 ticket = atomicAdd(work + 8, 1ull);
+#endif
+        if (ticket == (u64)gridDim.x - 1) {            // last block: publish, then clear
+#if !LX_ACQREL_TICKET
+            __threadfence();
+#endif
+#pragma unroll
+            for (int k = 0; k < 6; k++) stats[k] = atomicExch(acc + k, 0ull);
+            const u64 sm = atomicExch(stuck_max, 0ull);
+            stats[6] = sm ? ~sm : ~0ull;               // lowest stuck row, ~0 = none
+            stats[7] = atomicExch(work + 9, 0ull);       // seed-upload stall (0: none)
+            atomicExch(counter, 0ull);
+            atomicExch(work + 8, 0ull);
+        }
+    }
+}
+
 template <bool STREAM>
 __device__ __forceinline__ void rollout_body(u32* st, i64 B, int max_turns, int mode,
                                              u64 seed_base, const u64* seeds, i64 first,
@@ -792,76 +916,7 @@ __device__ __forceinline__ void rollout_body(u32* st, i64 B, int max_turns, int 
             }
         }
     }
-    // warp reduce, one atomic per warp per counter
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        n_steps += __shfl_xor_sync(0xffffffffu, n_steps, o);
-        n_p1 += __shfl_xor_sync(0xffffffffu, n_p1, o);
-        n_p2 += __shfl_xor_sync(0xffffffffu, n_p2, o);
-        n_draw += __shfl_xor_sync(0xffffffffu, n_draw, o);
-        n_trunc += __shfl_xor_sync(0xffffffffu, n_trunc, o);
-        n_done += __shfl_xor_sync(0xffffffffu, n_done, o);
-    }
-    if (LX_STATIC_CHUNKS && gridDim.x == 1) {
-        // one block: sums in shared memory, no ticket and no fences (the
-        // stuck-row atomics of this block's warps are ordered by the barrier)
-        // (one block plays <= blockDim.x envs of <= max_turns plies: u32 sums)
-        __shared__ u32 blk[6];
-        if (threadIdx.x < 6) blk[threadIdx.x] = 0u;
-        __syncthreads();
-        if (lane == 0) {
-            atomicAdd(&blk[0], n_steps);
-            atomicAdd(&blk[1], n_p1);
-            atomicAdd(&blk[2], n_p2);
-            atomicAdd(&blk[3], n_draw);
-            atomicAdd(&blk[4], n_trunc);
-            atomicAdd(&blk[5], n_done);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-#pragma unroll
-            for (int k = 0; k < 6; k++) stats[k] = (u64)blk[k];
-            const u64 sm = atomicExch(stuck_max, 0ull);
-            stats[6] = sm ? ~sm : ~0ull;
-            stats[7] = atomicExch(work + 9, 0ull);       // seed-upload stall (0: none)
-            *counter = 0ull;
-        }
-        return;
-    }
-    if (lane == 0) {
-        atomicAdd(acc + 0, (u64)n_steps);
-        atomicAdd(acc + 1, (u64)n_p1);
-        atomicAdd(acc + 2, (u64)n_p2);
-        atomicAdd(acc + 3, (u64)n_draw);
-        atomicAdd(acc + 4, (u64)n_trunc);
-        atomicAdd(acc + 5, (u64)n_done);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-#if LX_ACQREL_TICKET
-        // release: this block's sums (ordered before it by the barrier,
-        // cumulatively) precede the ticket; acquire: the last block sees
-        // every block's sums
-        u64 ticket;
-        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
-                     : "=l"(ticket) : "l"(work + 8) : "memory");
-#else
-        __threadfence();
-        const u64 ticket = atomicAdd(work + 8, 1ull);
-#endif
-        if (ticket == (u64)gridDim.x - 1) {            // last block: publish, then clear
-#if !LX_ACQREL_TICKET
-            __threadfence();
-#endif
-#pragma unroll
-            for (int k = 0; k < 6; k++) stats[k] = atomicExch(acc + k, 0ull);
-            const u64 sm = atomicExch(stuck_max, 0ull);
-            stats[6] = sm ? ~sm : ~0ull;               // lowest stuck row, ~0 = none
-            stats[7] = atomicExch(work + 9, 0ull);       // seed-upload stall (0: none)
-            atomicExch(counter, 0ull);
-            atomicExch(work + 8, 0ull);
-        }
-    }
+    publish_stats(n_steps, n_p1, n_p2, n_draw, n_trunc, n_done, stats, work);
 }
 
 }  // namespace lx

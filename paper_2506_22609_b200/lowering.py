@@ -1917,6 +1917,8 @@ class GameLowering(MoveLoweringMixin):
 #define LX_STATIC_CHUNKS {int(os.environ.get("LX_STATIC_CHUNKS", "1"))}
 #define LX_ACQREL_TICKET {int(os.environ.get("LX_ACQREL_TICKET", "1"))}
 #define LX_MASK_STREAM {int(os.environ.get("LX_MASK_STREAM", "1"))}
+#define LX_CLUSTER_PUBLISH {int(os.environ.get("LX_CLUSTER_PUBLISH", "1"))}
+#define LX_PUBLISH_INLINE @@PUBINL@@
 #define LX_STEP_MINB {int(os.environ.get("LX_STEP_MINB", "4"))}
 #include "lx_core.cuh"
 
@@ -1990,6 +1992,10 @@ struct Game {{
             r_threads = int(os.environ.get("LX_ROLLOUT_THREADS", 128))
             r_minb = int(os.environ.get("LX_ROLLOUT_MINB", 4))
         src = src.replace("@@BLOCK@@", "128" if self.rm_used else "256")
+        # rollout epilogue inlined only where that register allocation wins
+        # (row-mirror games; lx_kernels.cuh publish_stats)
+        src = src.replace("@@PUBINL@@", os.environ.get("LX_PUBLISH_INLINE",
+                                                       "1" if self.rm_used else "0"))
         src = src.replace("@@RTHREADS@@", str(r_threads)).replace("@@RMINB@@", str(r_minb))
         src = src.replace("@@HELPERS@@", "\n".join(em.helpers.values()))
         info = {"name": spec.name, "C": self.C, "A": self.A, "W": self.W, "NX": NX,

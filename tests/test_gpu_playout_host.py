@@ -105,3 +105,20 @@ def test_empty_batch_and_bad_arguments():
     assert stats[6] == np.uint64(2 ** 64 - 1)
     with pytest.raises(ValueError):
         g.playout_host(seeds=np.zeros(10, dtype=np.uint64), outcomes=np.zeros(9, np.int8))
+
+
+@pytest.mark.parametrize("B", [1, 31, 256, 257, 1000, 2048, 2049, 5000])
+def test_small_grids_one_block_cluster_and_ticket_publish(B):
+    """Batch sizes across the three stats-publish paths of lx_rollout (one
+    block, one cluster of 2..8 blocks, cross-block ticket): outcomes, move
+    counts and stats equal the oracle's."""
+    g = game("connect_four")
+    seeds = O.spawn_seeds(2718, B)
+    d_out, d_turns, d_stats = device_rollout(g, seeds)
+    want, steps = O.OracleGame("connect_four").playout(seeds=seeds, threads=8)
+    assert np.array_equal(d_out, want["outcome"]) and np.array_equal(d_turns, want["move_count"])
+    assert int(d_stats[0]) == steps and int(d_stats[5]) == B
+    assert int(d_stats[1] + d_stats[2] + d_stats[3]) == B
+    assert d_stats[6] == np.uint64(2 ** 64 - 1) and d_stats[7] == 0
+    h_out, h_turns, h_stats = g.playout_host(seeds=seeds, turns=True)
+    assert np.array_equal(h_out, d_out) and np.array_equal(h_stats, d_stats)
