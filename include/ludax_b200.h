@@ -206,12 +206,16 @@ int lx_rollout(const lx_game *g, void *state, int64_t B, int max_turns, int mode
      LX_PLAYOUT_TRUNCATE     envs reaching max_turns end as truncated draws
                              (engine.py:156-160); without it they stop there
                              unfinished (_run_episode)
-     LX_PLAYOUT_UPLOAD_FIRST upload all seeds before the launch (no overlap)
+     LX_PLAYOUT_UPLOAD_FIRST copy all seeds to device memory before the launch
+                             (no streaming, no zero copy)
    The handle owns the device scratch (grown to the largest B seen; calls on
    one handle serialize).  Batches of >= LX_PLAYOUT_STREAM_MIN envs stream
    their seeds up in <= 64 pieces on a copy stream while the rollout already
    plays (each warp waits only for its chunk's piece), so the upload overlaps
-   the play; the call returns once the outputs are in host memory.  Pinned
+   the play; batches of <= LX_PLAYOUT_ZERO_COPY_MAX envs use no DMA at all
+   (the kernel reads the seeds from and writes its outputs to a mapped pinned
+   block of the handle).  The call returns once the outputs are in host
+   memory.  Pinned
    host memory (cudaHostAlloc / torch pin_memory) gets full PCIe bandwidth;
    pageable memory works without the overlap.  A live env with no legal
    action and no pass -> LX_EEMPTY_MASK (*stuck_row = lowest such env), the
@@ -219,6 +223,7 @@ int lx_rollout(const lx_game *g, void *state, int64_t B, int max_turns, int mode
 #define LX_PLAYOUT_TRUNCATE 1
 #define LX_PLAYOUT_UPLOAD_FIRST 2
 #define LX_PLAYOUT_STREAM_MIN 65536
+#define LX_PLAYOUT_ZERO_COPY_MAX 8192
 int lx_playout_host(const lx_game *g, int64_t B, int max_turns, int flags, uint64_t seed,
                     const uint64_t *seeds, int64_t first_index, int8_t *outcomes,
                     int32_t *turns, uint64_t *stats, void *state, int64_t *stuck_row,

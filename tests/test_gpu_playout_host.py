@@ -122,3 +122,8 @@ def test_small_grids_one_block_cluster_and_ticket_publish(B):
     assert d_stats[6] == np.uint64(2 ** 64 - 1) and d_stats[7] == 0
     h_out, h_turns, h_stats = g.playout_host(seeds=seeds, turns=True)
     assert np.array_equal(h_out, d_out) and np.array_equal(h_stats, d_stats)
+    assert np.array_equal(h_turns, d_turns)
+    # zero-copy (B <= LX_PLAYOUT_ZERO_COPY_MAX) and the device-copy path agree
+    u_out, u_turns, u_stats = g.playout_host(seeds=seeds, turns=True, upload_first=True)
+    assert np.array_equal(u_out, d_out) and np.array_equal(u_turns, d_turns)
+    assert np.array_equal(u_stats, d_stats)
