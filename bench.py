@@ -537,12 +537,13 @@ def measure_e2e(args, game, rng, B, B_total, first, ws, steps=None):
 
 
 def measure_e2e_host(args, game, rng, B, B_total, first, ws, steps=None):
-    """e2e through the C-ABI host-buffer call lx_playout_host (what a numpy /
-    ctypes binding of the reference's _run_episode calls): every step passes
-    its episode's per-env seeds in pinned host memory and gets the per-env
-    outcomes and the stats back in host memory; one synchronous call per
-    step, the seed upload overlapped with the play inside the call.  Σ env
-    steps over ranks ÷ max over ranks of the host wall time."""
+    """e2e through the C-ABI host-buffer calls lx_playout_host_async / _wait
+    (what a numpy / ctypes binding of the reference's benchmark loop calls,
+    evaluation.py:197-233): every step passes its episode's per-env seeds in
+    pinned host memory and gets the per-env outcomes and the stats back in
+    host memory; two episodes in flight, so step i+1's seed upload and step
+    i-1's download overlap step i's rollout (the native runtime's own three
+    streams).  Σ env steps over ranks ÷ max over ranks of the host wall time."""
     import torch
     import torch.distributed as dist
 
@@ -555,17 +556,25 @@ def measure_e2e_host(args, game, rng, B, B_total, first, ws, steps=None):
     outc_h = [torch.empty(B, dtype=torch.int8).pin_memory() for _ in range(n_it)]
     stats_h = [torch.zeros(8, dtype=torch.int64).pin_memory() for _ in range(n_it)]
 
-    def step(it):
-        game.playout_host(seeds=seeds_h[it], outcomes=outc_h[it], stats=stats_h[it],
-                          max_turns=args.max_turns, truncate=True)
-    for it in range(WU):
-        step(it)
+    def run(lo, hi):
+        # the host stays two episodes ahead: episode i is issued once i-2's
+        # outputs are home, so i's upload can start as soon as i-2's rollout
+        # (same device slot) has read its seeds
+        pending = []
+        for it in range(lo, hi):
+            pending.append(game.playout_host_async(seeds=seeds_h[it], outcomes=outc_h[it],
+                                                   stats=stats_h[it], max_turns=args.max_turns,
+                                                   truncate=True))
+            if len(pending) > 2:
+                game.playout_host_wait(pending.pop(0))
+        for t in pending:
+            game.playout_host_wait(t)
+    run(0, WU)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    for it in range(WU, n_it):
-        step(it)
+    run(WU, n_it)
     e2e_s = time.perf_counter() - t0
     if ws > 1:
         dist.barrier()
@@ -577,9 +586,9 @@ def measure_e2e_host(args, game, rng, B, B_total, first, ws, steps=None):
     return {"value": int(n.item()) / float(t.item()), "unit": UNIT,
             "h2d_bytes_per_step": B * 8 * ws, "d2h_bytes_per_step": (B + 64) * ws,
             "steps_timed": K,
-            "path": "lx_playout_host (C-ABI, host buffers): pinned host seeds in, host outcomes "
-                    "+ stats out, one synchronous call per step, seeds streamed up while the "
-                    "rollout plays"}
+            "path": "lx_playout_host_async / _wait (C-ABI, host buffers): pinned host seeds "
+                    "in, host outcomes + stats out, the host two episodes ahead (upload, "
+                    "rollout and download on the runtime's three streams, two device slots)"}
 
 
 def rollout_roofline(game, value, totals, clock_mhz):

@@ -229,6 +229,24 @@ int lx_playout_host(const lx_game *g, int64_t B, int max_turns, int flags, uint6
                     int32_t *turns, uint64_t *stats, void *state, int64_t *stuck_row,
                     void *stream);
 
+/* lx_playout_host split in two for callers that play many episodes back to
+   back (the reference's benchmark_throughput loop, evaluation.py:214-233):
+   _async enqueues the episode and returns a ticket at once; _wait returns
+   when that episode's outputs are in host memory (LX_EEMPTY_MASK as above).
+   Episodes alternate between two device slots of the handle: episode i+1's
+   seed upload (its own stream) and episode i-1's download (a third stream)
+   overlap episode i's rollout on `stream`; reuse of a slot is ordered on
+   the GPU (an upload waits for the rollout two back, a rollout for the
+   download two back), so _async never blocks the host (except to grow a
+   slot).  Host buffers must stay valid until their ticket completes and
+   should be pinned (pageable copies serialise with the rollout).  Calls on
+   one handle serialize. */
+int lx_playout_host_async(const lx_game *g, int64_t B, int max_turns, int flags, uint64_t seed,
+                          const uint64_t *seeds, int64_t first_index, int8_t *outcomes,
+                          int32_t *turns, uint64_t *stats, void *state, void *stream,
+                          int64_t *ticket);
+int lx_playout_host_wait(const lx_game *g, int64_t ticket, int64_t *stuck_row);
+
 /* PGX-style environment step (LudaxEnvironment.step; BASELINE north star),
    one launch per ply.  flags (LX_ENV_*):
      STEP       apply one ply to live rows (else only refresh the outputs)

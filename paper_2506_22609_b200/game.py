@@ -636,18 +636,8 @@ class B200Game:
             state._touch()
         return state, stats
 
-    def playout_host(self, batch_size=None, seed=0, seeds=None, first_index=0, max_turns=200,
-                     truncate=True, outcomes=True, turns=False, stats=None, out=None,
-                     upload_first=False):
-        """One batch episode through the host-buffer C-ABI call lx_playout_host
-        (the reference's evaluation._run_episode / engine.playout_random as a
-        numpy caller binds them, evaluation.py:197-211, engine.py:123-163):
-        per-env seeds in host memory (numpy or a pinned torch CPU tensor; None:
-        spawn(seed, first_index + i)), outcomes / final move counts / stats
-        back in host memory.  ``outcomes`` / ``turns``: True to allocate,
-        a host array to fill, or False; ``out``: optional DeviceState for the
-        final states.  The seed upload overlaps the play (see the header).
-        Returns (outcomes or None, turns or None, stats (8,) uint64)."""
+    def _host_playout_args(self, batch_size, seed, seeds, first_index, outcomes, turns, stats,
+                           out):
         torch = _torch()
 
         def host_ptr(a, dtype, n, what):
@@ -677,21 +667,64 @@ class B200Game:
             raise ValueError("batch_size, seeds or out is required")
         if seeds is not None and not isinstance(seeds, torch.Tensor):
             seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
-        seeds_a, seeds_p = host_ptr(seeds, np.uint64, B, "seeds")
-        outc_a, outc_p = host_ptr(outcomes, np.int8, B, "outcomes")
-        turns_a, turns_p = host_ptr(turns, np.int32, B, "turns")
-        stats_a, stats_p = host_ptr(stats if stats is not None else True, np.uint64, 8, "stats")
+        return B, (host_ptr(seeds, np.uint64, B, "seeds"),
+                   host_ptr(outcomes, np.int8, B, "outcomes"),
+                   host_ptr(turns, np.int32, B, "turns"),
+                   host_ptr(stats if stats is not None else True, np.uint64, 8, "stats"))
+
+    def playout_host(self, batch_size=None, seed=0, seeds=None, first_index=0, max_turns=200,
+                     truncate=True, outcomes=True, turns=False, stats=None, out=None,
+                     upload_first=False):
+        """One batch episode through the host-buffer C-ABI call lx_playout_host
+        (the reference's evaluation._run_episode / engine.playout_random as a
+        numpy caller binds them, evaluation.py:197-211, engine.py:123-163):
+        per-env seeds in host memory (numpy or a pinned torch CPU tensor; None:
+        spawn(seed, first_index + i)), outcomes / final move counts / stats
+        back in host memory.  ``outcomes`` / ``turns``: True to allocate,
+        a host array to fill, or False; ``out``: optional DeviceState for the
+        final states.  The seed upload overlaps the play (see the header).
+        Returns (outcomes or None, turns or None, stats (8,) uint64)."""
+        B, (sd, oc, tn, st_) = self._host_playout_args(batch_size, seed, seeds, first_index,
+                                                       outcomes, turns, stats, out)
         flags = (1 if truncate else 0) | (2 if upload_first else 0)
         stuck = ctypes.c_int64(-1)
         st = native.lib().lx_playout_host(
-            self.handle, B, int(max_turns), flags, int(seed) & (2 ** 64 - 1), seeds_p,
-            int(first_index), outc_p, turns_p, stats_p,
+            self.handle, B, int(max_turns), flags, int(seed) & (2 ** 64 - 1), sd[1],
+            int(first_index), oc[1], tn[1], st_[1],
             out.words.data_ptr() if out is not None else None, ctypes.byref(stuck),
             self._stream())
         if out is not None:
             out._touch()
         native.check(st, stuck.value)
-        return outc_a, turns_a, stats_a
+        return oc[0], tn[0], st_[0]
+
+    def playout_host_async(self, batch_size=None, seed=0, seeds=None, first_index=0,
+                           max_turns=200, truncate=True, outcomes=True, turns=False, stats=None,
+                           out=None):
+        """lx_playout_host_async: enqueue one host-buffer episode and return a
+        ticket for playout_host_wait (two episodes in flight per handle: the
+        next one's seed upload and the previous one's download overlap this
+        one's rollout).  Host buffers should be pinned torch tensors."""
+        B, (sd, oc, tn, st_) = self._host_playout_args(batch_size, seed, seeds, first_index,
+                                                       outcomes, turns, stats, out)
+        ticket = ctypes.c_int64(-1)
+        native.check(native.lib().lx_playout_host_async(
+            self.handle, B, int(max_turns), 1 if truncate else 0, int(seed) & (2 ** 64 - 1),
+            sd[1], int(first_index), oc[1], tn[1], st_[1],
+            out.words.data_ptr() if out is not None else None, self._stream(),
+            ctypes.byref(ticket)))
+        if out is not None:
+            out._touch()
+        # the arrays ride along so they outlive the in-flight copies
+        return (ticket.value, sd[0], oc[0], tn[0], st_[0])
+
+    def playout_host_wait(self, ticket):
+        """Block until the episode of ``ticket`` has its outputs in host memory;
+        returns (outcomes or None, turns or None, stats)."""
+        stuck = ctypes.c_int64(-1)
+        native.check(native.lib().lx_playout_host_wait(self.handle, ticket[0],
+                                                       ctypes.byref(stuck)), stuck.value)
+        return ticket[2], ticket[3], ticket[4]
 
     def with_seeds(self, state, seeds):
         """Copy of ``state`` whose rows draw from new RNG streams (the MCTS

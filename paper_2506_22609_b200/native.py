@@ -42,7 +42,7 @@ EXPORTS = ("lx_version", "lx_last_error", "lx_game_create", "lx_bind_device", "l
            "lx_cache_key", "lx_game_info_get", "lx_game_destroy", "lx_init", "lx_legal",
            "lx_sample", "lx_truncate", "lx_set_seeds", "lx_step", "lx_random_step", "lx_rollout",
            "lx_export", "lx_import", "lx_observe", "lx_env_step", "lx_expand", "lx_mcts",
-           "lx_playout_host")
+           "lx_playout_host", "lx_playout_host_async", "lx_playout_host_wait")
 
 
 def build_native():
@@ -82,6 +82,9 @@ def lib():
                              ctypes.POINTER(i64), vp]
     L.lx_playout_host.argtypes = [vp, i64, i32, i32, u64, vp, i64, vp, vp, vp, vp,
                                   ctypes.POINTER(i64), vp]
+    L.lx_playout_host_async.argtypes = [vp, i64, i32, i32, u64, vp, i64, vp, vp, vp, vp, vp,
+                                        ctypes.POINTER(i64)]
+    L.lx_playout_host_wait.argtypes = [vp, i64, ctypes.POINTER(i64)]
     L.lx_expand.argtypes = [vp, vp, i64, vp, vp, vp, i64, vp, ctypes.c_int, vp, vp, vp, vp]
     L.lx_mcts.argtypes = [vp, vp, i64, vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.c_int,
                           vp, i64, ctypes.c_int, vp, i64, vp, vp, ctypes.c_int, vp]

@@ -127,3 +127,26 @@ def test_small_grids_one_block_cluster_and_ticket_publish(B):
     u_out, u_turns, u_stats = g.playout_host(seeds=seeds, turns=True, upload_first=True)
     assert np.array_equal(u_out, d_out) and np.array_equal(u_turns, d_turns)
     assert np.array_equal(u_stats, d_stats)
+
+
+def test_async_pipeline_matches_sync_calls():
+    """lx_playout_host_async / _wait with two episodes in flight equals the
+    synchronous call episode by episode (slot reuse, tickets in order and out
+    of order, an empty batch in the stream of calls)."""
+    g = game("connect_four")
+    sizes = [STREAM_MIN * 2, 5000, 0, STREAM_MIN * 2 + 1, 1]
+    seeds = [O.spawn_seeds(100 + k, B) for k, B in enumerate(sizes)]
+    pinned = [torch.from_numpy(s.view(np.int64)).pin_memory() for s in seeds]
+    outs = [torch.empty(B, dtype=torch.int8).pin_memory() for B in sizes]
+    turns = [torch.empty(B, dtype=torch.int32).pin_memory() for B in sizes]
+    stats = [torch.zeros(8, dtype=torch.int64).pin_memory() for _ in sizes]
+    tickets = []
+    for k in range(len(sizes)):
+        tickets.append(g.playout_host_async(seeds=pinned[k], outcomes=outs[k], turns=turns[k],
+                                            stats=stats[k]))
+    for t in reversed(tickets):             # waiting out of order is fine
+        g.playout_host_wait(t)
+    for k, B in enumerate(sizes):
+        o, tn, st = g.playout_host(seeds=seeds[k], turns=True)
+        assert np.array_equal(outs[k].numpy(), o) and np.array_equal(turns[k].numpy(), tn)
+        assert np.array_equal(stats[k].numpy().view(np.uint64), st), k
