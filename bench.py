@@ -11,8 +11,13 @@ The headline line is configs[1] (Connect Four, 2^22 envs per GPU).  At N=1
 the line also carries ``per_config``: every BASELINE.json config measured in
 the same run -- Tic-Tac-Toe at B=1024 (configs[0], the reference's CPU-sized
 case) and at 2^22, Connect Four, Hex, Reversi and Pente at 2^22 -- each with
-its own timed episodes, roofline, e2e leg, CPU baseline and an oracle
+its own timed episodes, roofline, e2e legs, CPU baseline and an oracle
 parity check of the benchmarked episode's final states.
+
+``e2e`` goes through the reference-facing C-ABI with host buffers
+(lx_playout_host_async / _wait: pinned host seeds in, host outcomes + stats
+out, every copy inside the timed region); ``e2e_python`` is the same metric
+through the Python B200Game.rollout API with torch-managed copies.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--game G]
   python bench.py --impl reference ...      # CPU reference arm (oracle port)
@@ -322,9 +327,13 @@ def run_distributed(args, arm):
     value = tot[0] / (ms_max / 1000.0)
     extras = {}
     if not args.no_extras:
-        extras["e2e"] = arm.e2e()
+        # e2e: the reference-facing C-ABI with host buffers (lx_playout_host_async
+        # / _wait); e2e_python: the Python B200Game.rollout pipeline beside it
         if hasattr(arm, "e2e_host"):
-            extras["e2e_c_abi"] = arm.e2e_host()
+            extras["e2e"] = arm.e2e_host()
+            extras["e2e_python"] = arm.e2e()
+        else:
+            extras["e2e"] = arm.e2e()
     if rank == 0 and not args.no_extras:
         extras.update(arm.extras(value, ms_max / args.steps, clk.summary().get("sm_mhz"), tot))
     line = None
@@ -856,9 +865,9 @@ def measure_per_config(arm, value, ms_step, totals, head_extras):
                                      "draws": tot[3], "envs": tot[5]},
                           "clocks": clk,
                           "roofline": rollout_roofline(game, val, tot, clk.get("sm_mhz")),
-                          "e2e_c_abi": measure_e2e_host(args, game, arm.rng, B, B, 0, 1,
-                                                        steps=min(steps, 12)),
-                          "e2e": measure_e2e(args, game, arm.rng, B, B, 0, 1,
+                          "e2e": measure_e2e_host(args, game, arm.rng, B, B, 0, 1,
+                                                  steps=min(steps, 12)),
+                          "e2e_python": measure_e2e(args, game, arm.rng, B, B, 0, 1,
                                              steps=min(steps, 12))})
         entry["unit"] = UNIT
         entry["workload"] = (f"{GAME_FILES[name]} uniform-random rollouts, {B} envs, "

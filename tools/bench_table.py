@@ -9,12 +9,12 @@ line = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
 names = {"configs[0]": "configs[0] TTT B=1024", "configs[0]@2^22": "configs[0] TTT B=2²²",
          "configs[1]": "configs[1] C4 B=2²² (headline)", "configs[2]": "configs[2] Hex 11×11 B=2²²",
          "configs[3]": "configs[3] Reversi B=2²²", "configs[4]": "configs[4] Pente 19×19 B=2²²"}
-print("| config | env steps/s | e2e (Python API) | e2e (C-ABI host buffers) | ALU-pipe roofline frac | "
+print("| config | env steps/s | e2e (C-ABI host buffers) | e2e (Python API) | ALU-pipe roofline frac | "
       "CPU port (oracle, threads) | parity (envs checked / mismatches) |")
 print("|---|---|---|---|---|---|---|")
 for e in line["per_config"]:
     e2e = line["e2e"]["value"] if isinstance(e["e2e"], str) else e["e2e"]["value"]
-    hc = e.get("e2e_c_abi") if isinstance(e.get("e2e_c_abi"), dict) else line.get("e2e_c_abi")
+    hc = e.get("e2e_python") if isinstance(e.get("e2e_python"), dict) else line.get("e2e_python")
     e2e_c = f"{hc['value'] / 1e9:.2f} G" if hc else "-"
     rl = e.get("roofline") or {}
     frac = rl.get("frac")
