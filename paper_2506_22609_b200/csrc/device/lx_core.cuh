@@ -285,6 +285,13 @@ __device__ __forceinline__ double key_uniform(u64 key) {
     return __dmul_rn((double)(key >> 11), 0x1p-53);
 }
 
+// draw_index with the uniform already formed (identical arithmetic)
+__device__ __forceinline__ int draw_index_u(double u, int n) {
+    const int r = __double2int_rz(__dmul_rn(u, (double)n));
+    const int hi = n > 1 ? n - 1 : 0;
+    return r < hi ? r : hi;
+}
+
 __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
 
 // Per-thread shared-memory mirror of both boards, for rules that probe a few

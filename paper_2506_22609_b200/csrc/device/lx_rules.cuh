@@ -186,14 +186,29 @@ __device__ __forceinline__ int legal_count(const typename G::St& s) {
 // uniform legal action for the current mover; -1 when stuck
 // (reference compiler.py:430-446, mechanics.py:209-242, 488-492).  `hint`
 // receives the sampled move group (movement games) for apply_step.
+#ifndef LX_EARLY_DRAW
+#define LX_EARLY_DRAW 1
+#endif
 template <class G>
 __device__ __forceinline__ int sample_action(const typename G::St& s, u64 smix, int& hint) {
     hint = -1;
     if constexpr (G::MECH == 0) {
+#if LX_EARLY_DRAW
+        // the uniform depends only on (seed, move_count): formed ahead of the
+        // legality, in the same basic block, so the RNG / FP64 conversion
+        // chain overlaps the bitboard work instead of following the count
+        // (a shorter dependent chain per ply: latency-bound small batches, MCTS)
+        const double u = key_uniform(mix64(smix ^ (u64)s.mc));
+        const BB<G::W> legal = G::legal(s);
+        const int n = popc(legal);
+        if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
+        const int r = draw_index_u(u, n);
+#else
         const BB<G::W> legal = G::legal(s);
         const int n = popc(legal);
         if (n == 0) return G::force_pass(s.phase) ? G::PASS : -1;
         const int r = draw_index(mix64(smix ^ (u64)s.mc), n);
+#endif
         return G::bit_cell(select_bit(legal, r));
     } else {
         int tot[G::NG];

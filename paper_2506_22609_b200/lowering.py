@@ -1919,6 +1919,7 @@ class GameLowering(MoveLoweringMixin):
 #define LX_MASK_STREAM {int(os.environ.get("LX_MASK_STREAM", "1"))}
 #define LX_CLUSTER_PUBLISH {int(os.environ.get("LX_CLUSTER_PUBLISH", "1"))}
 #define LX_PUBLISH_INLINE @@PUBINL@@
+#define LX_EARLY_DRAW @@EARLY@@
 #define LX_STEP_MINB {int(os.environ.get("LX_STEP_MINB", "4"))}
 #include "lx_core.cuh"
 
@@ -1996,6 +1997,11 @@ struct Game {{
         # (row-mirror games; lx_kernels.cuh publish_stats)
         src = src.replace("@@PUBINL@@", os.environ.get("LX_PUBLISH_INLINE",
                                                        "1" if self.rm_used else "0"))
+        # RNG chain ahead of the legality (lx_rules.cuh sample_action): B200
+        # A/B r2zk at 2^22: Pente +2.3 %, C4 -0.4 %, TTT / Hex / Reversi within
+        # noise, no latency gain at B=1024 -- on for the long row-mirror plies
+        src = src.replace("@@EARLY@@", os.environ.get("LX_EARLY_DRAW",
+                                                      "1" if self.rm_used else "0"))
         src = src.replace("@@RTHREADS@@", str(r_threads)).replace("@@RMINB@@", str(r_minb))
         src = src.replace("@@HELPERS@@", "\n".join(em.helpers.values()))
         info = {"name": spec.name, "C": self.C, "A": self.A, "W": self.W, "NX": NX,

@@ -7,7 +7,7 @@ for gb in ${GAMES:-connect_four:4194304 tic_tac_toe:4194304 hex:4194304 reversi:
   g=${gb%%:*}; b=${gb##*:}
   timeout 300 python tools/ncu_rollout.py --game $g --batch $b > gpurun_out/plain_$g.json 2>&1 &&
   timeout 600 ncu --set full --metrics sm__inst_executed_pipe_alu.sum,sm__inst_executed_pipe_alu.avg.peak_sustained,sm__cycles_elapsed.avg \
-      --clock-control none --import-source on -k regex:lx_rollout -s 1 -c 1 \
+      --clock-control none --import-source on -k regex:"^lx_rollout$" -s 1 -c 1 \
       -o gpurun_out/prof_$g python tools/ncu_rollout.py --game $g --batch $b > gpurun_out/ncu_$g.log 2>&1
   echo "$g rc=$?"
   ncu -i gpurun_out/prof_$g.ncu-rep --page source --csv --print-source sass > gpurun_out/sass_$g.csv 2>/dev/null
