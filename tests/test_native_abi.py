@@ -44,3 +44,18 @@ def test_create_without_gpu_fails_cleanly():
                                      b"", ctypes.byref(h))
     assert st == 4      # LX_ECOMPILE: the garbage never reaches the driver
     assert b"NVRTC" in native.lib().lx_last_error()
+
+
+def test_host_buffer_calls_reject_bad_arguments_without_a_gpu():
+    """lx_playout_host / _async / _wait validate their arguments before any
+    driver call (LX_EINVALID = 6), so a bad binding fails cleanly."""
+    L = native.lib()
+    stuck = ctypes.c_int64(0)
+    ticket = ctypes.c_int64(0)
+    stats = (ctypes.c_uint64 * 8)()
+    assert L.lx_playout_host(None, 16, 200, 0, 1, None, 0, None, None, stats, None,
+                             ctypes.byref(stuck), None) == 6
+    assert L.lx_playout_host_async(None, 16, 200, 0, 1, None, 0, None, None, stats, None,
+                                   None, ctypes.byref(ticket)) == 6
+    assert L.lx_playout_host_wait(None, 0, ctypes.byref(stuck)) == 6
+    assert b"NULL" in L.lx_last_error()
