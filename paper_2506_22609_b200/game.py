@@ -33,6 +33,10 @@ from .syntax import parse_game
 GAMES_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "games")
 MCTS_SHARED_LIMIT = 200 * 1024      # dynamic shared memory per MCTS tree (B200 opt-in 227 KB; the runtime checks it with the kernel's static buffers)
 
+# per-cell planes: exported read-only (DeviceState.host)
+READONLY_FIELDS = ("board_piece", "board_owner", "comp_labels", "hopped_mask", "captured_mask",
+                   "promoted_mask")
+
 FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "terminated",
           "truncated", "outcome", "seeds", "scores", "pass_streak", "pass_flags", "must_move",
           "last_mover", "last_kind", "last_source", "last_dest", "last_dest_by_player",
@@ -139,17 +143,26 @@ class DeviceState:
         device (no-op when nothing was read or nothing changed)."""
         if self._host is None:
             return
-        if all(np.array_equal(v, self._snap[k]) for k, v in self._host.items()):
+        if all(np.array_equal(self._host[k], v) for k, v in self._snap.items()):
             return
         self.game._import_into(self, self._host)
-        self._snap = {k: v.copy() for k, v in self._host.items()}
+        self._snap = {k: self._host[k].copy() for k in self._snap}
 
     # -- reference field view --
     def host(self):
-        """dict of numpy arrays in the reference GameState layout."""
+        """dict of numpy arrays in the reference GameState layout.  The
+        per-env scalar fields are writable (edits reach the device, see the
+        class docstring); the per-cell planes (boards, component labels,
+        transient masks) are read-only views, so an in-place edit of them
+        raises instead of being lost -- and the change check copies only the
+        scalar fields (~25 B/env, not the ~110-760 B/env of the planes)."""
         if self._host is None:
             self._host = self.game._export(self)
-            self._snap = {k: v.copy() for k, v in self._host.items()}
+            for k in READONLY_FIELDS:
+                if self._host.get(k) is not None:
+                    self._host[k].setflags(write=False)
+            self._snap = {k: v.copy() for k, v in self._host.items()
+                          if k not in READONLY_FIELDS}
         return self._host
 
     def __getattr__(self, name):
@@ -753,7 +766,10 @@ class B200Game:
                 self.legal_mask(state))
 
     # -- reference layout interchange --
-    def ref_arrays(self, B, device):
+    def ref_arrays(self, B, device, packed=False):
+        """Reference-layout tensors for B envs; ``packed``: all of them views
+        of one byte buffer (16-byte aligned fields), returned with it as
+        (dict, buffer), so a whole export moves in one copy."""
         torch = _torch()
         C, L = self.num_cells, self.layout
         f = {"board_piece": ((B, C), torch.int8), "board_owner": ((B, C), torch.int8),
@@ -780,7 +796,16 @@ class B200Game:
             f["phase"] = ((B,), torch.int8)
         if L.turn_pos:
             f["turn_pos"] = ((B,), torch.int8)
-        return {k: torch.empty(shape, dtype=dt, device=device) for k, (shape, dt) in f.items()}
+        if not packed:
+            return {k: torch.empty(shape, dtype=dt, device=device) for k, (shape, dt) in f.items()}
+        offs, total = {}, 0
+        for k, (shape, dt) in f.items():
+            n = int(np.prod(shape)) * torch.empty(0, dtype=dt).element_size()
+            offs[k] = (total, n)
+            total += (n + 15) // 16 * 16
+        buf = torch.empty(max(total, 16), dtype=torch.uint8, device=device)
+        out = {k: buf[o:o + n].view(f[k][1]).view(f[k][0]) for k, (o, n) in offs.items()}
+        return out, buf
 
     def _ref_struct(self, tensors):
         return native.RefState(**{k: (tensors[k].data_ptr() if k in tensors else None)
@@ -796,13 +821,25 @@ class B200Game:
         return t
 
     def _export(self, state):
-        t = self.export_device(state)
+        """Host numpy arrays of every reference field: one lx_export into one
+        packed device buffer, one device-to-host copy, numpy views into it."""
+        state.sync()
+        t, buf = self.ref_arrays(state.batch_size, "cuda", packed=True)
+        native.check(native.lib().lx_export(self.handle, state.words.data_ptr(),
+                                            state.batch_size, ctypes.byref(self._ref_struct(t)),
+                                            self._stream()))
+        # pinned destination (torch's caching host allocator recycles the
+        # block once the previous export's arrays are gone): the copy runs at
+        # PCIe speed instead of through the driver's pageable staging
+        torch = _torch()
+        host = torch.empty(buf.numel(), dtype=torch.uint8, pin_memory=True)
+        host.copy_(buf)
+        base = buf.data_ptr()
         out = {}
         for k, v in t.items():
-            a = v.cpu().numpy()
-            if k == "seeds":
-                a = a.view(np.uint64)
-            out[k] = a
+            o = v.data_ptr() - base
+            a = host[o:o + v.numel() * v.element_size()].view(v.dtype).view(v.shape).numpy()
+            out[k] = a.view(np.uint64) if k == "seeds" else a
         return out
 
     def _import_into(self, state, arrays):
@@ -814,6 +851,8 @@ class B200Game:
             if v is None or k not in native.REF_FIELDS:
                 continue
             a = np.ascontiguousarray(v)
+            if not a.flags.writeable:          # DeviceState's read-only planes
+                a = a.copy()
             if a.dtype == np.uint64:
                 a = a.view(np.int64)
             t[k] = torch.as_tensor(a).to("cuda")
