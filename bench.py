@@ -682,7 +682,7 @@ def measure_extras(args, game, lx, rng, B, B_total, value, ms_step, clock_mhz, t
     return out
 
 
-def measure_e2e_reference_layout(args, game, lx, rng, B, B_total, steps=3):
+def measure_e2e_reference_layout(args, game, lx, rng, B, B_total, steps=5):
     """The drop-in call end to end: engine.playout_random(game, seed, B)
     (engine.py:123-163) with the final states exported to host numpy arrays
     in the reference GameState layout (state.py:78-130) every step -- one
@@ -693,7 +693,9 @@ def measure_e2e_reference_layout(args, game, lx, rng, B, B_total, steps=3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     steps_done, d2h = 0, 0
+    po = host = None
     for e in range(steps):
+        po = host = None                    # the caller is done with the previous result
         po = lx.engine.playout_random(game, seed=rng.episode_seed(0, B_total, 30_000 + e),
                                       batch_size=B, max_turns=args.max_turns)
         host = po.final.host()

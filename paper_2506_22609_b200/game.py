@@ -43,12 +43,20 @@ FIELDS = ("board_piece", "board_owner", "current_player", "move_count", "termina
           "hopped_mask", "captured_mask", "promoted_mask", "comp_labels", "phase", "turn_pos")
 
 
+_TORCH = None
+
+
 def _torch():
-    import torch
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2506_22609_b200 needs a CUDA device (sm_100a); "
-                           "there is no CPU fallback")
-    return torch
+    # checked once per process (torch.cuda.is_available reads the environment
+    # on every call: ~4 us, hundreds of calls per MCTS match)
+    global _TORCH
+    if _TORCH is None:
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2506_22609_b200 needs a CUDA device (sm_100a); "
+                               "there is no CPU fallback")
+        _TORCH = torch
+    return _TORCH
 
 
 @dataclass(frozen=True)
