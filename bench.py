@@ -336,6 +336,11 @@ def run_distributed(args, arm):
             extras["e2e"] = arm.e2e()
     if rank == 0 and not args.no_extras:
         extras.update(arm.extras(value, ms_max / args.steps, clk.summary().get("sm_mhz"), tot))
+        if hasattr(arm, "e2e_host"):
+            for k in ("e2e", "e2e_python"):
+                rl = e2e_roofline(extras.get(k), tot[0] / args.steps, value, ws)
+                if rl:
+                    extras[k]["roofline"] = rl
     line = None
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
@@ -543,6 +548,52 @@ def measure_e2e(args, game, rng, B, B_total, first, ws, steps=None):
             "path": "B200Game.rollout(seeds=host->device) + outcomes/stats device->host, "
                     "double-buffered over H2D / compute / D2H streams, every rank on its "
                     "own shard, max wall time over ranks"}
+
+
+_PCIE_GBS = None
+
+
+def pcie_h2d_gbs():
+    """Pinned host -> device copy bandwidth of this GPU's link (64 MiB, 10
+    copies, CUDA events), measured once per process: the peak of the e2e
+    legs' roofline (their bound is the per-env seed upload)."""
+    global _PCIE_GBS
+    if _PCIE_GBS is None:
+        import torch
+        n = 64 << 20
+        h = torch.empty(n, dtype=torch.uint8).pin_memory()
+        d = torch.empty(n, dtype=torch.uint8, device="cuda")
+        for _ in range(3):
+            d.copy_(h, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            d.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        _PCIE_GBS = 10 * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+    return _PCIE_GBS
+
+
+def e2e_roofline(e2e, env_steps_per_step, kernel_value, ws=1):
+    """Roofline of an e2e leg: the slower of the device rollout (the
+    device-timed value of the same config) and the host->device upload of the
+    per-env seeds (8 B per env per episode) at the measured PCIe bandwidth."""
+    if not isinstance(e2e, dict) or not env_steps_per_step or not kernel_value:
+        return None
+    pcie = pcie_h2d_gbs() * ws
+    per_step = e2e["h2d_bytes_per_step"] / env_steps_per_step
+    pcie_bound = pcie * 1e9 / per_step
+    bound = min(kernel_value, pcie_bound)
+    return {"bound": "pcie_h2d" if pcie_bound < kernel_value else "device_rollout",
+            "achieved": e2e["value"], "peak": bound, "unit": UNIT, "frac": e2e["value"] / bound,
+            "device_rollout_env_steps_per_s": kernel_value,
+            "pcie_h2d": {"peak_gbs": pcie, "achieved_gbs": e2e["value"] * per_step / 1e9,
+                         "h2d_bytes_per_env_step": per_step,
+                         "bound_env_steps_per_s": pcie_bound,
+                         "peak_source": f"pinned host->device copy of 64 MiB in this run, "
+                                        f"x{ws} GPUs"}}
 
 
 def measure_e2e_host(args, game, rng, B, B_total, first, ws, steps=None):
@@ -871,6 +922,12 @@ def measure_per_config(arm, value, ms_step, totals, head_extras):
                                                   steps=min(steps, 12)),
                           "e2e_python": measure_e2e(args, game, arm.rng, B, B, 0, 1,
                                              steps=min(steps, 12))})
+        if isinstance(entry.get("e2e"), dict):
+            per_step = entry["totals"]["env_steps"] / steps
+            for k in ("e2e", "e2e_python"):
+                rl = e2e_roofline(entry.get(k), per_step, entry.get("value"))
+                if rl:
+                    entry[k]["roofline"] = rl
         entry["unit"] = UNIT
         entry["workload"] = (f"{GAME_FILES[name]} uniform-random rollouts, {B} envs, "
                              f"full episodes (cap {args.max_turns} plies)")
