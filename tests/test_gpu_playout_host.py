@@ -150,3 +150,35 @@ def test_async_pipeline_matches_sync_calls():
         o, tn, st = g.playout_host(seeds=seeds[k], turns=True)
         assert np.array_equal(outs[k].numpy(), o) and np.array_equal(turns[k].numpy(), tn)
         assert np.array_equal(stats[k].numpy().view(np.uint64), st), k
+
+
+# Test program: only the bottom row of a 3x3 board takes stones and no line
+# can form there (P1, P2, P1), so every env is stuck at ply 3 with no pass.
+STUCK = """(game "StuckAtThree"
+  (players 2)
+  (equipment
+    (board (square 3))
+    (pieces ("stone" both)))
+  (rules
+    (play
+      (repeat (P1 P2)
+        (place "stone"
+          (destination (and (empty) (edge bottom))))))
+    (end
+      (if (line "stone" 3) (mover win)))))"""
+
+
+@pytest.mark.parametrize("B", [100, STREAM_MIN + 5])
+def test_stuck_rows_raise_empty_mask_naming_the_lowest_row(B):
+    """A live env with no legal action and no pass is EmptyMask
+    (engine.py:142-147) on every host-buffer path, with the lowest such row."""
+    from paper_2506_22609_b200.errors import EmptyMask
+    g = lx.load_game(STUCK)
+    with pytest.raises(EmptyMask, match=r"\b0\b"):
+        g.playout_host(batch_size=B, seed=1)
+    seeds = O.spawn_seeds(1, B)
+    with pytest.raises(EmptyMask):
+        g.playout_host(seeds=seeds, turns=True)
+    t = g.playout_host_async(seeds=torch.from_numpy(seeds.view(np.int64)).pin_memory())
+    with pytest.raises(EmptyMask):
+        g.playout_host_wait(t)
