@@ -238,9 +238,11 @@ int lx_playout_host(const lx_game *g, int64_t B, int max_turns, int flags, uint6
    overlap episode i's rollout on `stream`; reuse of a slot is ordered on
    the GPU (an upload waits for the rollout two back, a rollout for the
    download two back), so _async never blocks the host (except to grow a
-   slot).  Host buffers must stay valid until their ticket completes and
-   should be pinned (pageable copies serialise with the rollout).  Calls on
-   one handle serialize. */
+   slot).  Batches of <= LX_PLAYOUT_ZERO_COPY_MAX envs use no DMA (a mapped
+   pinned block per slot, as lx_playout_host; the outputs reach the caller's
+   buffers at _wait, or when the slot is reused).  Host buffers must stay
+   valid until their ticket completes and should be pinned (pageable copies
+   serialise with the rollout).  Calls on one handle serialize. */
 int lx_playout_host_async(const lx_game *g, int64_t B, int max_turns, int flags, uint64_t seed,
                           const uint64_t *seeds, int64_t first_index, int8_t *outcomes,
                           int32_t *turns, uint64_t *stats, void *state, void *stream,
