@@ -919,9 +919,9 @@ def measure_per_config(arm, value, ms_step, totals, head_extras):
                           "clocks": clk,
                           "roofline": rollout_roofline(game, val, tot, clk.get("sm_mhz")),
                           "e2e": measure_e2e_host(args, game, arm.rng, B, B, 0, 1,
-                                                  steps=min(steps, 12)),
+                                                  steps=min(steps, 20)),
                           "e2e_python": measure_e2e(args, game, arm.rng, B, B, 0, 1,
-                                             steps=min(steps, 12))})
+                                             steps=min(steps, 20))})
         if isinstance(entry.get("e2e"), dict):
             per_step = entry["totals"]["env_steps"] / steps
             for k in ("e2e", "e2e_python"):
